@@ -1,0 +1,754 @@
+// The device C ABI (include/exg.h): context, device-resident CSR store, factor
+// upload with host level analysis, and the hot-path entry points that replace
+// the reference's spmv / Factorization::solve / apply / mevp_iks /
+// mevp_residual / eval_at_scaled_h / er_begin / er_eval.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "device.hpp"
+#include "exg.h"
+#include "kernels.cuh"
+#include "ctx.hpp"
+
+using exg::dev::Ctrl;
+
+namespace {
+
+struct CudaError {
+    cudaError_t e;
+    const char* where;
+};
+struct ApiError {
+    exg_status st;
+    std::string msg;
+};
+
+inline void ck(cudaError_t e, const char* where) {
+    if (e != cudaSuccess) throw CudaError{e, where};
+}
+
+template <typename T>
+T* dalloc(size_t count) {
+    void* p = nullptr;
+    if (count == 0) count = 1;
+    ck(cudaMalloc(&p, count * sizeof(T)), "cudaMalloc");
+    return static_cast<T*>(p);
+}
+
+template <typename T>
+void dfree(T*& p) {
+    if (p) cudaFree(p);
+    p = nullptr;
+}
+
+__global__ void k_gather(const double* __restrict__ x, const int* __restrict__ idx, int k,
+                         double* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < k) out[i] = x[idx[i]];
+}
+
+}  // namespace
+
+namespace {
+
+exg_status fail(exg_ctx* c, exg_status st, const std::string& msg) {
+    if (c) {
+        c->err = msg;
+        c->last = st;
+    }
+    return st;
+}
+
+#define API_BEGIN try {
+#define API_END(ctx)                                                                   \
+    }                                                                                  \
+    catch (const CudaError& e) {                                                       \
+        return fail(ctx, EXG_E_CUDA, std::string(e.where) + ": " + cudaGetErrorString(e.e)); \
+    }                                                                                  \
+    catch (const ApiError& e) {                                                        \
+        return fail(ctx, e.st, e.msg);                                                 \
+    }                                                                                  \
+    catch (const std::bad_alloc&) {                                                    \
+        return fail(ctx, EXG_E_NOMEM, "host allocation failed");                       \
+    }                                                                                  \
+    return EXG_OK;
+
+void upload_csr(exg_ctx* c, DCsr& m, int n_rows, int n_cols, int nnz, const int* rowptr,
+                const int* col, const double* val) {
+    dfree(m.rowptr);
+    dfree(m.col);
+    dfree(m.val);
+    m.n_rows = n_rows;
+    m.n_cols = n_cols;
+    m.nnz = nnz;
+    m.rowptr = dalloc<int>(n_rows + 1);
+    m.col = dalloc<int>(nnz);
+    m.val = dalloc<double>(nnz);
+    ck(cudaMemcpyAsync(m.rowptr, rowptr, sizeof(int) * (n_rows + 1), cudaMemcpyHostToDevice, c->stream), "upload");
+    if (nnz) {
+        ck(cudaMemcpyAsync(m.col, col, sizeof(int) * nnz, cudaMemcpyHostToDevice, c->stream), "upload");
+        ck(cudaMemcpyAsync(m.val, val, sizeof(double) * nnz, cudaMemcpyHostToDevice, c->stream), "upload");
+    }
+    ck(cudaStreamSynchronize(c->stream), "upload sync");
+}
+
+void ensure_vectors(exg_ctx* c, int n) {
+    if (c->vec_n >= n && c->vin) return;
+    dfree(c->partials);
+    c->partials = dalloc<double>((size_t)std::max(8192, (n + 255) / 256 + 1024) + 2 * 4096);
+    c->mgs_partials_off = (size_t)std::max(8192, (n + 255) / 256 + 1024);
+    double** vs[] = {&c->vin, &c->vout, &c->t, &c->w, &c->xk, &c->xnext, &c->gb,
+                     &c->startv, &c->v1, &c->t1, &c->t2, &c->t3, &c->tmp};
+    for (double** p : vs) {
+        dfree(*p);
+        *p = dalloc<double>(n);
+    }
+    c->vec_n = n;
+}
+
+void ensure_inputs(exg_ctx* c, int ni) {
+    if (c->n_inputs >= ni && c->u_k) return;
+    dfree(c->u_k);
+    dfree(c->u_k1);
+    c->u_k = dalloc<double>(std::max(ni, 1));
+    c->u_k1 = dalloc<double>(std::max(ni, 1));
+    c->n_inputs = ni;
+}
+
+void ensure_krylov(exg_ctx* c, int mmax) {
+    if (c->mmax_alloc >= mmax && c->V) return;
+    const int n = c->n;
+    dfree(c->V);
+    dfree(c->hbar);
+    dfree(c->hinv);
+    dfree(c->coef);
+    dfree(c->dscratch);
+    c->ldv = ((long long)n + 31) / 32 * 32;
+    c->V = dalloc<double>((size_t)(mmax + 1) * c->ldv);
+    c->hld = mmax + 2;
+    c->hbar = dalloc<double>((size_t)(mmax + 1) * c->hld);
+    c->hinv = dalloc<double>((size_t)mmax * mmax);
+    c->coef = dalloc<double>(mmax);
+    c->dscratch = dalloc<double>((size_t)20 * mmax * mmax);
+    c->mmax_alloc = mmax;
+    c->basis_valid = false;
+}
+
+void require_factors(exg_ctx* c) {
+    if (!c->l_ptr) throw ApiError{EXG_E_CONTRACT, "no factorization uploaded (exg_set_factors)"};
+}
+
+const DCsr& mat(exg_ctx* c, int which) {
+    if (which < 0 || which > 2) throw ApiError{EXG_E_CONTRACT, "bad matrix id"};
+    const DCsr& m = c->mats[which];
+    if (!m.rowptr) throw ApiError{EXG_E_CONTRACT, "matrix not uploaded (exg_set_csr)"};
+    return m;
+}
+
+// x = Q U^{-1} L^{-1} P b, with the fused epilogue final[q] = add[q] + coef*x
+void solve_dev(exg_ctx* c, const double* b, double* final_out, double coef, const double* add,
+               const Ctrl* ctrl) {
+    const int n = c->n;
+    ck(cudaMemsetAsync(c->trsv_buf, 0xFF, 16 + 2 * sizeof(double) * (size_t)n, c->stream), "memset");
+    unsigned int* tickets = reinterpret_cast<unsigned int*>(c->trsv_buf);
+    double* y = reinterpret_cast<double*>(c->trsv_buf + 16);
+    double* x = y + n;
+    exg::dev::TrsvArgs a{};
+    a.n = n;
+    a.order = c->l_order;
+    a.ptr = c->l_ptr;
+    a.col = c->l_col;
+    a.val = c->l_val;
+    a.in = b;
+    a.in_perm = c->row_perm;
+    a.out = y;
+    a.ticket = tickets;
+    a.ctrl = ctrl;
+    exg::dev::trsv(c->L(), false, false, a);
+    exg::dev::TrsvArgs u{};
+    u.n = n;
+    u.order = c->u_order;
+    u.ptr = c->u_ptr;
+    u.col = c->u_col;
+    u.val = c->u_val;
+    u.diag = c->u_diag;
+    u.in = y;
+    u.out = x;
+    u.ticket = tickets + 1;
+    u.final_out = final_out;
+    u.out_perm = c->col_perm;
+    u.add = add;
+    u.coef = coef;
+    u.ctrl = ctrl;
+    exg::dev::trsv(c->L(), true, c->opt.trsv_mode == EXG_TRSV_FAST, u);
+    c->cnt.trsv_calls++;
+}
+
+void sync_ctrl(exg_ctx* c) {
+    ck(cudaMemcpyAsync(c->h_ctrl, c->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, c->stream), "ctrl d2h");
+    ck(cudaStreamSynchronize(c->stream), "ctrl sync");
+}
+
+exg_status ctrl_status(exg_ctx* c) {
+    const Ctrl& h = *c->h_ctrl;
+    switch (h.status) {
+        case 0: return EXG_OK;
+        case 2: throw ApiError{EXG_E_NONFINITE, "dense_expm: non-finite entry"};
+        case 3: throw ApiError{EXG_E_SINGULAR, "dense_solve: singular matrix"};
+        case 4: throw ApiError{EXG_E_ZERO_START, "mevp: zero start vector"};
+        case 5: {
+            char buf[128];
+            snprintf(buf, sizeof buf, "mevp: dimension cap reached, last residual %f", h.last_residual);
+            throw ApiError{EXG_E_NO_CONVERGENCE, buf};
+        }
+        case 6: throw ApiError{EXG_E_SINGULAR_REDUCED, "mevp: invariant subspace with singular reduced matrix"};
+        default: throw ApiError{EXG_E_CONTRACT, "mevp: unknown device status"};
+    }
+}
+
+// Arnoldi MEVP on the device (arnoldi_mevp, krylov.cpp:103-173).  v: device
+// start vector.  er_mode: apply the er_eval early-out with ||x_k||_inf of xk.
+// Returns with h_ctrl synchronised.
+void mevp_dev(exg_ctx* c, const double* v, double h, const exg_mevp_cfg& cfg, int er_mode,
+              const double* xk) {
+    require_factors(c);
+    const DCsr& C = mat(c, EXG_MAT_C);
+    if (cfg.m_max < 1) throw ApiError{EXG_E_CONTRACT, "mevp: m_max must be >= 1"};
+    if (h < 0.0) throw ApiError{EXG_E_CONTRACT, "mevp: negative step size"};
+    ensure_krylov(c, cfg.m_max);
+    const int n = c->n;
+    c->basis_valid = false;
+    // configuration part of the control block
+    Ctrl& hc = *c->h_ctrl;
+    std::memset(&hc, 0, sizeof(Ctrl));
+    hc.h = h;
+    hc.eps = cfg.eps;
+    hc.breakdown_tol = cfg.breakdown_tol;
+    hc.m_max = cfg.m_max;
+    hc.check_stride = cfg.check_stride > 0 ? cfg.check_stride : 1;
+    ck(cudaMemcpyAsync(c->ctrl, &hc, sizeof(Ctrl), cudaMemcpyHostToDevice, c->stream), "ctrl h2d");
+    auto L = c->L();
+    exg::dev::start(L, v, xk, n, c->partials, c->V, c->ctrl, er_mode);
+    c->cnt.mevp_calls++;
+
+    // MGS launch shape: 1024-thread blocks, K register elements per thread
+    int K = 1, blocks = 1;
+    {
+        const int ks[] = {1, 2, 4, 8, 16};
+        for (int kk : ks) {
+            K = kk;
+            const int occ = std::max(1, exg::dev::mgs_max_blocks(kk));
+            const long long cap = (long long)c->num_sms * occ;
+            blocks = (int)std::min<long long>(cap, ((long long)n + 1024LL * kk - 1) / (1024LL * kk));
+            if ((long long)blocks * 1024 * kk >= n) break;
+        }
+        if ((long long)blocks * 1024 * K < n) throw ApiError{EXG_E_CONTRACT, "vector too long for the MGS kernel"};
+        blocks = std::min(blocks, 4096);
+    }
+    exg::dev::MgsArgs ma{n, c->ldv, c->V, c->w, c->hbar, c->hld, c->partials + c->mgs_partials_off, c->bar, c->ctrl};
+    exg::dev::DenseArgs da{c->ctrl, c->hbar, c->hld, c->hinv, c->coef, c->dscratch, 0, 0, h};
+    const bool gspmv = c->opt.weight_mode == EXG_WEIGHT_GSPMV;
+    if (gspmv) mat(c, EXG_MAT_G);
+    sync_ctrl(c);  // start-vector decisions (early-out, zero start)
+    if (hc.status == 0 && !hc.converged) {
+        for (int jj = 0; jj < cfg.m_max; ++jj) {
+            // w = -G^{-1}(C v_j)   (krylov.cpp:120-121)
+            exg::dev::spmv(L, C.rowptr, C.col, C.val, C.n_rows, nullptr, c->t, c->ctrl, c->V, c->ldv);
+            solve_dev(c, c->t, c->w, -1.0, nullptr, c->ctrl);
+            exg::dev::mgs(L, ma, blocks, K);
+            exg::dev::dense(L, da, jj + 1);
+            if (gspmv) {
+                const DCsr& G = c->mats[EXG_MAT_G];
+                exg::dev::spmv_norm(L, G.rowptr, G.col, G.val, n, c->V, c->ldv, c->partials, c->done,
+                                    c->ctrl, 1, nullptr);
+            } else {
+                exg::dev::apply_weight(L, c->u_ptr, c->u_col, c->u_val, c->u_diag, c->l_ptr, c->l_col,
+                                       c->l_val, n, c->col_perm, c->row_perm, nullptr, c->tmp, nullptr,
+                                       c->partials, c->done, c->ctrl, c->V, c->ldv, nullptr);
+            }
+            exg::dev::iter_end(L, c->ctrl);
+            c->cnt.arnoldi_iters++;
+            sync_ctrl(c);
+            if (hc.status || hc.converged) break;
+        }
+    }
+    ctrl_status(c);
+    if (hc.skip) return;
+    // result at h: beta V_m e^{hH^-1} e_1 (krylov.cpp:170-171)
+    hc.h_sub = h;
+    ck(cudaMemcpyAsync(&c->ctrl->h_sub, &h, sizeof(double), cudaMemcpyHostToDevice, c->stream), "h_sub");
+    da.mode = 1;
+    da.h_eval = h;
+    exg::dev::dense(L, da, hc.m);
+    c->basis_valid = true;
+}
+
+double* resolve_in(exg_ctx* c, const double* p, size_t count, int ptr_kind, double* staging) {
+    if (ptr_kind == EXG_PTR_DEVICE) return const_cast<double*>(p);
+    ck(cudaMemcpyAsync(staging, p, count * sizeof(double), cudaMemcpyHostToDevice, c->stream), "h2d");
+    return staging;
+}
+
+void deliver(exg_ctx* c, double* user, const double* dev, size_t count, int ptr_kind) {
+    if (ptr_kind == EXG_PTR_DEVICE) {
+        if (user != dev)
+            ck(cudaMemcpyAsync(user, dev, count * sizeof(double), cudaMemcpyDeviceToDevice, c->stream), "d2d");
+    } else {
+        ck(cudaMemcpyAsync(user, dev, count * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
+        ck(cudaStreamSynchronize(c->stream), "d2h sync");
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+exg_status exg_create(int device, exg_ctx** out) {
+    exg_ctx* c = nullptr;
+    API_BEGIN
+    c = new exg_ctx();
+    c->device = device;
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+    cudaDeviceProp prop;
+    ck(cudaGetDeviceProperties(&prop, device), "props");
+    if (prop.major < 10) throw ApiError{EXG_E_CUDA, "exsim-B200 requires an sm_100a (Blackwell) GPU"};
+    c->num_sms = prop.multiProcessorCount;
+    c->bar = dalloc<unsigned int>(4);
+    c->done = dalloc<unsigned int>(4);
+    ck(cudaMemset(c->bar, 0, 4 * sizeof(unsigned int)), "memset");
+    ck(cudaMemset(c->done, 0, 4 * sizeof(unsigned int)), "memset");
+    c->weight = dalloc<double>(4);
+    c->ctrl = static_cast<Ctrl*>(static_cast<void*>(dalloc<char>(exg::dev::ctrl_size())));
+    void* hp = nullptr;
+    ck(cudaMallocHost(&hp, exg::dev::ctrl_size()), "cudaMallocHost");
+    c->h_ctrl = static_cast<Ctrl*>(hp);
+    std::memset(c->h_ctrl, 0, exg::dev::ctrl_size());
+    *out = c;
+    return EXG_OK;
+    }
+    catch (const CudaError& e) {
+        if (c) exg_destroy(c);
+        *out = nullptr;
+        return EXG_E_CUDA;
+    }
+    catch (const ApiError& e) {
+        if (c) exg_destroy(c);
+        *out = nullptr;
+        return e.st;
+    }
+}
+
+void exg_destroy(exg_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    for (DCsr& m : c->mats) {
+        dfree(m.rowptr);
+        dfree(m.col);
+        dfree(m.val);
+    }
+    int* ip[] = {c->l_ptr, c->l_col, c->u_ptr, c->u_col, c->row_perm, c->col_perm, c->l_order, c->u_order, c->probe_idx};
+    for (int* p : ip)
+        if (p) cudaFree(p);
+    double* dp[] = {c->l_val, c->u_val, c->u_diag, c->vin, c->vout, c->t, c->w, c->xk, c->xnext,
+                    c->gb, c->startv, c->v1, c->t1, c->t2, c->t3, c->tmp, c->u_k, c->u_k1, c->V,
+                    c->hbar, c->hinv, c->coef, c->dscratch, c->partials, c->weight, c->probe_out};
+    for (double* p : dp)
+        if (p) cudaFree(p);
+    if (c->trsv_buf) cudaFree(c->trsv_buf);
+    if (c->bar) cudaFree(c->bar);
+    if (c->done) cudaFree(c->done);
+    if (c->ctrl) cudaFree(c->ctrl);
+    if (c->h_ctrl) cudaFreeHost(c->h_ctrl);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+exg_status exg_last_error(exg_ctx* c, char* buf, size_t len) {
+    if (!c) return EXG_E_CONTRACT;
+    if (buf && len) {
+        std::strncpy(buf, c->err.c_str(), len - 1);
+        buf[len - 1] = 0;
+    }
+    return c->last;
+}
+
+exg_status exg_set_options(exg_ctx* c, const exg_options_dev* o) {
+    if (!c || !o) return EXG_E_CONTRACT;
+    c->opt = *o;
+    return EXG_OK;
+}
+
+exg_status exg_set_csr(exg_ctx* c, int which, int n_rows, int n_cols, int nnz, const int* rowptr,
+                       const int* col, const double* val) {
+    API_BEGIN
+    if (which < 0 || which > 2 || n_rows < 0 || n_cols < 0 || nnz < 0 || rowptr[n_rows] != nnz)
+        throw ApiError{EXG_E_CONTRACT, "exg_set_csr: bad matrix"};
+    upload_csr(c, c->mats[which], n_rows, n_cols, nnz, rowptr, col, val);
+    if (which == EXG_MAT_B) ensure_inputs(c, n_cols);
+    API_END(c)
+}
+
+exg_status exg_update_values(exg_ctx* c, int which, const double* val) {
+    API_BEGIN
+    const DCsr& m = mat(c, which);
+    ck(cudaMemcpy(m.val, val, sizeof(double) * m.nnz, cudaMemcpyHostToDevice), "update values");
+    API_END(c)
+}
+
+exg_status exg_set_factors(exg_ctx* c, int n, const int* Lp, const int* Li, const double* Lx,
+                           const int* Up, const int* Ui, const double* Ux, const int* row_perm,
+                           const int* col_perm) {
+    API_BEGIN
+    if (n <= 0) throw ApiError{EXG_E_CONTRACT, "exg_set_factors: empty factorization"};
+    // split: L strictly lower (c < r; the unit diagonal is implicit, as
+    // Factorization::solve skips c >= r), U strictly upper + diagonal
+    std::vector<int> lp(n + 1, 0), up(n + 1, 0);
+    std::vector<int> lc, uc;
+    std::vector<double> lv, uv, ud(n, 0.0);
+    lc.reserve(Lp[n]);
+    lv.reserve(Lp[n]);
+    uc.reserve(Up[n]);
+    uv.reserve(Up[n]);
+    for (int r = 0; r < n; ++r) {
+        for (int k = Lp[r]; k < Lp[r + 1]; ++k)
+            if (Li[k] < r) {
+                lc.push_back(Li[k]);
+                lv.push_back(Lx[k]);
+            }
+        lp[r + 1] = (int)lc.size();
+        for (int k = Up[r]; k < Up[r + 1]; ++k) {
+            if (Ui[k] == r)
+                ud[r] = Ux[k];
+            else if (Ui[k] > r) {
+                uc.push_back(Ui[k]);
+                uv.push_back(Ux[k]);
+            }
+        }
+        up[r + 1] = (int)uc.size();
+    }
+    // level analysis (critical-path depth) and level-ordered row lists
+    std::vector<int> lev(n, 0);
+    int l_levels = 0, u_levels = 0;
+    for (int r = 0; r < n; ++r) {
+        int lv_ = 0;
+        for (int k = lp[r]; k < lp[r + 1]; ++k) lv_ = std::max(lv_, lev[lc[k]] + 1);
+        lev[r] = lv_;
+        l_levels = std::max(l_levels, lv_ + 1);
+    }
+    auto order_by = [n](const std::vector<int>& lv_, int nl, bool desc) {
+        std::vector<int> cnt(nl + 1, 0), ord(n);
+        for (int r = 0; r < n; ++r) cnt[lv_[r] + 1]++;
+        for (int i = 0; i < nl; ++i) cnt[i + 1] += cnt[i];
+        if (!desc)
+            for (int r = 0; r < n; ++r) ord[cnt[lv_[r]]++] = r;
+        else
+            for (int r = n - 1; r >= 0; --r) ord[cnt[lv_[r]]++] = r;
+        return ord;
+    };
+    const std::vector<int> lord = order_by(lev, l_levels, false);
+    for (int r = n - 1; r >= 0; --r) {
+        int lv_ = 0;
+        for (int k = up[r]; k < up[r + 1]; ++k) lv_ = std::max(lv_, lev[uc[k]] + 1);
+        lev[r] = lv_;  // reuse: U levels (only c > r are read, already final)
+        u_levels = std::max(u_levels, lv_ + 1);
+    }
+    const std::vector<int> uord = order_by(lev, u_levels, true);
+
+    int* ip[] = {c->l_ptr, c->l_col, c->u_ptr, c->u_col, c->row_perm, c->col_perm, c->l_order, c->u_order};
+    for (int* p : ip)
+        if (p) cudaFree(p);
+    dfree(c->l_val);
+    dfree(c->u_val);
+    dfree(c->u_diag);
+    dfree(c->trsv_buf);
+    c->n = n;
+    auto up_i = [&](int*& d, const int* h, size_t cnt) {
+        d = dalloc<int>(cnt);
+        if (cnt) ck(cudaMemcpy(d, h, cnt * sizeof(int), cudaMemcpyHostToDevice), "factor upload");
+    };
+    auto up_d = [&](double*& d, const double* h, size_t cnt) {
+        d = dalloc<double>(cnt);
+        if (cnt) ck(cudaMemcpy(d, h, cnt * sizeof(double), cudaMemcpyHostToDevice), "factor upload");
+    };
+    up_i(c->l_ptr, lp.data(), n + 1);
+    up_i(c->l_col, lc.data(), lc.size());
+    up_d(c->l_val, lv.data(), lv.size());
+    up_i(c->u_ptr, up.data(), n + 1);
+    up_i(c->u_col, uc.data(), uc.size());
+    up_d(c->u_val, uv.data(), uv.size());
+    up_d(c->u_diag, ud.data(), n);
+    up_i(c->row_perm, row_perm, n);
+    up_i(c->col_perm, col_perm, n);
+    up_i(c->l_order, lord.data(), n);
+    up_i(c->u_order, uord.data(), n);
+    c->trsv_buf = dalloc<char>(16 + 2 * sizeof(double) * (size_t)n);
+    ensure_vectors(c, n);
+    c->cnt.l_levels = l_levels;
+    c->cnt.u_levels = u_levels;
+    c->cnt.nnz_l = (long long)lc.size();
+    c->cnt.nnz_u = (long long)uc.size();
+    c->mmax_alloc = 0;  // Krylov workspace re-sized on next use
+    dfree(c->V);
+    c->basis_valid = false;
+    API_END(c)
+}
+
+exg_status exg_spmv(exg_ctx* c, int which, const double* x, double* y, int ptr_kind) {
+    API_BEGIN
+    const DCsr& m = mat(c, which);
+    double* xs = const_cast<double*>(x);
+    double* ys = y;
+    double* sx = nullptr;
+    double* sy = nullptr;
+    if (ptr_kind == EXG_PTR_HOST) {
+        sx = dalloc<double>(m.n_cols);
+        sy = dalloc<double>(m.n_rows);
+        ck(cudaMemcpyAsync(sx, x, sizeof(double) * m.n_cols, cudaMemcpyHostToDevice, c->stream), "h2d");
+        xs = sx;
+        ys = sy;
+    }
+    exg::dev::spmv(c->L(), m.rowptr, m.col, m.val, m.n_rows, xs, ys, nullptr, nullptr, 0);
+    if (ptr_kind == EXG_PTR_HOST) {
+        ck(cudaMemcpyAsync(y, sy, sizeof(double) * m.n_rows, cudaMemcpyDeviceToHost, c->stream), "d2h");
+        ck(cudaStreamSynchronize(c->stream), "sync");
+        dfree(sx);
+        dfree(sy);
+    }
+    ck(cudaGetLastError(), "spmv launch");
+    API_END(c)
+}
+
+exg_status exg_solve(exg_ctx* c, const double* b, double* x, int ptr_kind) {
+    API_BEGIN
+    require_factors(c);
+    const int n = c->n;
+    const double* bd = resolve_in(c, b, n, ptr_kind, c->vin);
+    double* xd = ptr_kind == EXG_PTR_DEVICE ? x : c->vout;
+    solve_dev(c, bd, xd, 1.0, nullptr, nullptr);
+    ck(cudaGetLastError(), "solve launch");
+    deliver(c, x, xd, n, ptr_kind);
+    API_END(c)
+}
+
+exg_status exg_apply(exg_ctx* c, const double* x, double* y, int ptr_kind) {
+    API_BEGIN
+    require_factors(c);
+    const int n = c->n;
+    const double* xd = resolve_in(c, x, n, ptr_kind, c->vin);
+    double* yd = ptr_kind == EXG_PTR_DEVICE ? y : c->vout;
+    exg::dev::apply_weight(c->L(), c->u_ptr, c->u_col, c->u_val, c->u_diag, c->l_ptr, c->l_col,
+                           c->l_val, n, c->col_perm, c->row_perm, xd, c->tmp, yd, c->partials,
+                           c->done, nullptr, nullptr, 0, c->weight);
+    ck(cudaGetLastError(), "apply launch");
+    deliver(c, y, yd, n, ptr_kind);
+    API_END(c)
+}
+
+exg_status exg_mevp_iks(exg_ctx* c, const double* v, double h, const exg_mevp_cfg* cfg,
+                        double* out, exg_mevp_info* info, int ptr_kind) {
+    API_BEGIN
+    require_factors(c);
+    const int n = c->n;
+    const double* vd = resolve_in(c, v, n, ptr_kind, c->vin);
+    if (info) std::memset(info, 0, sizeof(*info));
+    try {
+        mevp_dev(c, vd, h, *cfg, 0, nullptr);
+    } catch (const ApiError& e) {
+        if (info) info->last_residual = c->h_ctrl->last_residual;
+        throw;
+    }
+    double* od = ptr_kind == EXG_PTR_DEVICE ? out : c->vout;
+    exg::dev::combine(c->L(), c->V, c->ldv, c->coef, n, od, c->ctrl, 0, nullptr, nullptr, nullptr, 0.0);
+    ck(cudaGetLastError(), "mevp launch");
+    deliver(c, out, od, n, ptr_kind);
+    if (info) {
+        const Ctrl& h_ = *c->h_ctrl;
+        info->m = h_.m;
+        info->happy = h_.happy;
+        info->beta = h_.beta;
+        info->h_next = h_.h_next;
+        info->h_sub = h;
+        info->last_residual = h_.last_residual;
+    }
+    API_END(c)
+}
+
+exg_status exg_basis_residual(exg_ctx* c, double h, double* residual) {
+    API_BEGIN
+    if (!c->basis_valid) throw ApiError{EXG_E_CONTRACT, "mevp_residual: empty basis"};
+    const Ctrl& hc = *c->h_ctrl;
+    if (hc.happy || hc.h_next == 0.0) {
+        *residual = 0.0;
+        return EXG_OK;
+    }
+    const DCsr& G = mat(c, EXG_MAT_G);
+    auto L = c->L();
+    exg::dev::DenseArgs da{c->ctrl, c->hbar, c->hld, c->hinv, c->coef, c->dscratch, 0, 2, h};
+    exg::dev::dense(L, da, hc.m);
+    exg::dev::spmv_norm(L, G.rowptr, G.col, G.val, c->n, c->V + (long long)hc.m * c->ldv, 0,
+                        c->partials, c->done, nullptr, 0, c->weight);
+    // weight lands in c->weight; combine on the device
+    double* res = c->weight + 1;
+    // ctrl->weight is not set by the free-standing norm: copy it in
+    ck(cudaMemcpyAsync(&c->ctrl->weight, c->weight, sizeof(double), cudaMemcpyDeviceToDevice, c->stream), "w");
+    exg::dev::basis_residual_final(L, c->ctrl, res);
+    ck(cudaMemcpyAsync(residual, res, sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
+    sync_ctrl(c);
+    ctrl_status(c);
+    API_END(c)
+}
+
+exg_status exg_basis_eval(exg_ctx* c, double h, double* out, int ptr_kind) {
+    API_BEGIN
+    if (!c->basis_valid) throw ApiError{EXG_E_CONTRACT, "eval_at_scaled_h: empty basis"};
+    if (h < 0.0 || h > c->h_ctrl->h_sub)
+        throw ApiError{EXG_E_CONTRACT, "eval_at_scaled_h: h outside [0, h_sub]"};
+    auto L = c->L();
+    exg::dev::DenseArgs da{c->ctrl, c->hbar, c->hld, c->hinv, c->coef, c->dscratch, 0, 1, h};
+    exg::dev::dense(L, da, c->h_ctrl->m);
+    double* od = ptr_kind == EXG_PTR_DEVICE ? out : c->vout;
+    exg::dev::combine(L, c->V, c->ldv, c->coef, c->n, od, c->ctrl, 0, nullptr, nullptr, nullptr, 0.0);
+    deliver(c, out, od, c->n, ptr_kind);
+    sync_ctrl(c);
+    ctrl_status(c);
+    API_END(c)
+}
+
+exg_status exg_er_begin(exg_ctx* c, const double* x_k, const double* u_k, const double* u_k1,
+                        double h, int ptr_kind) {
+    API_BEGIN
+    require_factors(c);
+    const DCsr& B = mat(c, EXG_MAT_B);
+    const DCsr& C = mat(c, EXG_MAT_C);
+    if (h <= 0.0) throw ApiError{EXG_E_CONTRACT, "er_step: step size must be positive"};
+    const int n = c->n;
+    const int ni = B.n_cols;
+    ensure_inputs(c, ni);
+    auto kind = ptr_kind == EXG_PTR_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    if (x_k != c->xk) ck(cudaMemcpyAsync(c->xk, x_k, sizeof(double) * n, kind, c->stream), "x_k");
+    if (ni) {
+        ck(cudaMemcpyAsync(c->u_k, u_k, sizeof(double) * ni, kind, c->stream), "u_k");
+        ck(cudaMemcpyAsync(c->u_k1, u_k1, sizeof(double) * ni, kind, c->stream), "u_k1");
+    }
+    auto L = c->L();
+    // rhs = F + B u_k (F == 0 for linear stamps) ; B slope
+    exg::dev::spmv_b2(L, B.rowptr, B.col, B.val, B.n_rows, c->u_k, c->u_k1, h, c->t1, c->t2);
+    solve_dev(c, c->t1, c->v1, -1.0, c->xk, nullptr);      // v1 = x_k - G^{-1} rhs
+    solve_dev(c, c->t2, c->gb, 1.0, nullptr, nullptr);     // gb_slope = G^{-1} B slope
+    exg::dev::spmv(L, C.rowptr, C.col, C.val, C.n_rows, c->gb, c->t3, nullptr, nullptr, 0);
+    solve_dev(c, c->t3, c->startv, 1.0, c->v1, nullptr);   // start = v1 + G^{-1} C gb
+    c->h_built = h;
+    c->basis_valid = false;
+    ck(cudaGetLastError(), "er_begin launch");
+    API_END(c)
+}
+
+exg_status exg_er_eval(exg_ctx* c, double h_try, const exg_mevp_cfg* cfg, double* x_next,
+                       int* m_out, exg_mevp_info* info, int ptr_kind) {
+    API_BEGIN
+    require_factors(c);
+    const int n = c->n;
+    bool fresh = true;
+    if (c->basis_valid && h_try <= c->h_ctrl->h_sub && c->mats[EXG_MAT_G].rowptr) {
+        double r = 0.0;
+        exg_status st = exg_basis_residual(c, h_try, &r);
+        if (st != EXG_OK) return st;
+        if (r < cfg->eps) {
+            auto L = c->L();
+            exg::dev::DenseArgs da{c->ctrl, c->hbar, c->hld, c->hinv, c->coef, c->dscratch, 0, 1, h_try};
+            exg::dev::dense(L, da, c->h_ctrl->m);
+            fresh = false;
+        }
+    }
+    if (fresh) mevp_dev(c, c->startv, h_try, *cfg, 1, c->xk);
+    exg::dev::combine(c->L(), c->V, c->ldv, c->coef, n, c->xnext, c->ctrl, 1, c->xk, c->gb,
+                      c->startv, h_try);
+    ck(cudaGetLastError(), "er_eval launch");
+    if (m_out) *m_out = (fresh && !c->h_ctrl->skip) ? c->h_ctrl->m : -1;
+    if (info) {
+        const Ctrl& h_ = *c->h_ctrl;
+        info->m = h_.m;
+        info->happy = h_.happy;
+        info->beta = h_.beta;
+        info->h_next = h_.h_next;
+        info->h_sub = h_.h_sub;
+        info->last_residual = h_.last_residual;
+    }
+    if (x_next) deliver(c, x_next, c->xnext, n, ptr_kind);
+    API_END(c)
+}
+
+exg_status exg_er_step(exg_ctx* c, const double* x_k, const double* u_k, const double* u_k1,
+                       double h, const exg_mevp_cfg* cfg, double* x_next, int* m_out,
+                       int ptr_kind) {
+    exg_status st = exg_er_begin(c, x_k, u_k, u_k1, h, ptr_kind);
+    if (st != EXG_OK) return st;
+    return exg_er_eval(c, h, cfg, x_next, m_out, nullptr, ptr_kind);
+}
+
+exg_status exg_gather(exg_ctx* c, const int* idx, int k, double* out) {
+    API_BEGIN
+    if (k <= 0) return EXG_OK;
+    if (k > c->probe_cap) {
+        dfree(c->probe_idx);
+        dfree(c->probe_out);
+        c->probe_idx = dalloc<int>(k);
+        c->probe_out = dalloc<double>(k);
+        c->probe_cap = k;
+    }
+    ck(cudaMemcpyAsync(c->probe_idx, idx, sizeof(int) * k, cudaMemcpyHostToDevice, c->stream), "idx");
+    k_gather<<<(k + 255) / 256, 256, 0, c->stream>>>(c->xnext, c->probe_idx, k, c->probe_out);
+    c->launches++;
+    ck(cudaMemcpyAsync(out, c->probe_out, sizeof(double) * k, cudaMemcpyDeviceToHost, c->stream), "d2h");
+    ck(cudaStreamSynchronize(c->stream), "gather sync");
+    API_END(c)
+}
+
+exg_status exg_counters_get(exg_ctx* c, exg_counters* out) {
+    if (!c || !out) return EXG_E_CONTRACT;
+    *out = c->cnt;
+    out->kernel_launches = c->launches;
+    return EXG_OK;
+}
+
+exg_status exg_counters_reset(exg_ctx* c) {
+    if (!c) return EXG_E_CONTRACT;
+    c->launches = 0;
+    c->cnt.arnoldi_iters = c->cnt.mevp_calls = c->cnt.trsv_calls = 0;
+    return EXG_OK;
+}
+
+exg_status exg_synchronize(exg_ctx* c) {
+    API_BEGIN
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    API_END(c)
+}
+
+exg_status exg_device_alloc(exg_ctx* c, size_t bytes, void** ptr) {
+    API_BEGIN
+    ck(cudaMalloc(ptr, bytes), "cudaMalloc");
+    API_END(c)
+}
+
+exg_status exg_device_free(exg_ctx* c, void* ptr) {
+    API_BEGIN
+    ck(cudaFree(ptr), "cudaFree");
+    API_END(c)
+}
+
+exg_status exg_memcpy(exg_ctx* c, void* dst, const void* src, size_t bytes, int kind) {
+    API_BEGIN
+    ck(cudaMemcpyAsync(dst, src, bytes, (cudaMemcpyKind)kind, c->stream), "memcpy");
+    ck(cudaStreamSynchronize(c->stream), "memcpy sync");
+    API_END(c)
+}
+
+void* exg_stream(exg_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+}  // extern "C"

@@ -1,0 +1,61 @@
+// Internal definition of the device context (exg_ctx of include/exg.h).
+#pragma once
+
+#include <string>
+
+#include "device.hpp"
+#include "exg.h"
+#include "kernels.cuh"
+
+struct DCsr {
+    int n_rows = 0, n_cols = 0, nnz = 0;
+    int* rowptr = nullptr;
+    int* col = nullptr;
+    double* val = nullptr;
+};
+
+struct exg_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int num_sms = 148;
+    long long launches = 0;
+    exg_counters cnt{};
+    std::string err;
+    exg_status last = EXG_OK;
+    exg_options_dev opt{EXG_TRSV_EXACT, EXG_WEIGHT_APPLY};
+
+    DCsr mats[3];  // C, G, B
+    // factors
+    int n = 0;
+    int *l_ptr = nullptr, *l_col = nullptr, *u_ptr = nullptr, *u_col = nullptr;
+    double *l_val = nullptr, *u_val = nullptr, *u_diag = nullptr;
+    int *row_perm = nullptr, *col_perm = nullptr, *l_order = nullptr, *u_order = nullptr;
+    // solve scratch: [2 tickets + pad (16 B)][y n][x n], memset to 0xFF per solve
+    char* trsv_buf = nullptr;
+    // n-vectors
+    int vec_n = 0;
+    double *vin = nullptr, *vout = nullptr, *t = nullptr, *w = nullptr, *xk = nullptr,
+           *xnext = nullptr, *gb = nullptr, *startv = nullptr, *v1 = nullptr, *t1 = nullptr,
+           *t2 = nullptr, *t3 = nullptr, *tmp = nullptr;
+    int n_inputs = 0;
+    double *u_k = nullptr, *u_k1 = nullptr;
+    // Krylov workspace
+    int mmax_alloc = 0;
+    long long ldv = 0;
+    double *V = nullptr, *hbar = nullptr, *hinv = nullptr, *coef = nullptr, *dscratch = nullptr;
+    int hld = 0;
+    double* partials = nullptr;
+    size_t mgs_partials_off = 0;
+    unsigned int *bar = nullptr, *done = nullptr;
+    double* weight = nullptr;
+    exg::dev::Ctrl* ctrl = nullptr;
+    exg::dev::Ctrl* h_ctrl = nullptr;  // pinned mirror
+    bool basis_valid = false;
+    double h_built = 0.0;
+    double *probe_out = nullptr;
+    int* probe_idx = nullptr;
+    int probe_cap = 0;
+
+    exg::dev::Launch L() { return exg::dev::Launch{stream, num_sms, &launches}; }
+};
+

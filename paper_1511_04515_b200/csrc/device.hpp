@@ -1,0 +1,88 @@
+// Device-side argument blocks and kernel launch wrappers (internal).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace exg {
+namespace dev {
+
+struct Ctrl;
+
+struct TrsvArgs {
+    int n;
+    const int* order;   // rows in level order
+    const int* ptr;     // off-diagonal CSR (pivot coordinates)
+    const int* col;
+    const double* val;
+    const double* diag; // U only
+    const double* in;   // L: b (original coords, gathered through in_perm); U: L's output
+    const int* in_perm; // row_perm (L)
+    double* out;        // pivot-coordinate result, sentinel-initialised
+    unsigned int* ticket;
+    // optional fused epilogue: final_out[out_perm[r]] = (add ? add[q] : 0) + coef * x
+    double* final_out;
+    const int* out_perm;
+    const double* add;
+    double coef;
+    const Ctrl* ctrl;   // early exit when the MEVP has converged
+};
+
+struct MgsArgs {
+    int n;
+    long long ldv;
+    double* V;
+    const double* w;
+    double* hbar;
+    int hld;
+    double* partials;
+    unsigned int* bar;
+    Ctrl* ctrl;
+};
+
+struct DenseArgs {
+    Ctrl* ctrl;
+    const double* hbar;
+    int hld;
+    double* hinv;     // persistent H_m^-1 (m x m, row-major)
+    double* coef;     // final coefficients
+    double* scratch;  // global scratch (used when the block does not fit smem)
+    int use_smem;
+    int mode;
+    double h_eval;
+};
+
+// ---- launch wrappers (kernels.cu) ------------------------------------------
+struct Launch {
+    cudaStream_t stream;
+    int num_sms;
+    long long* launches;  // counter of this library's kernel launches
+};
+
+void spmv(const Launch& L, const int* rowptr, const int* col, const double* val, int n_rows,
+          const double* x, double* y, const Ctrl* ctrl, const double* vbase, long long ldv);
+void spmv_b2(const Launch& L, const int* rowptr, const int* col, const double* val, int n_rows,
+             const double* u_k, const double* u_k1, double h, double* t1, double* t2);
+void trsv(const Launch& L, bool upper, bool reverse, const TrsvArgs& a);
+void apply_weight(const Launch& L, const int* uptr, const int* ucol, const double* uval,
+                  const double* udiag, const int* lptr, const int* lcol, const double* lval, int n,
+                  const int* col_perm, const int* row_perm, const double* x, double* t,
+                  double* y_out, double* partials, unsigned int* done, Ctrl* ctrl,
+                  const double* vbase, long long ldv, double* weight_out);
+void spmv_norm(const Launch& L, const int* rowptr, const int* col, const double* val, int n,
+               const double* vbase, long long ldv, double* partials, unsigned int* done,
+               Ctrl* ctrl, int from_ctrl_m, double* weight_out);
+void start(const Launch& L, const double* v, const double* xk, int n, double* partials,
+           double* v0, Ctrl* ctrl, int er_mode);
+int mgs_max_blocks(int K);
+void mgs(const Launch& L, const MgsArgs& a, int n_blocks, int K);
+void dense(const Launch& L, const DenseArgs& a, int m);
+void iter_end(const Launch& L, Ctrl* ctrl);
+void combine(const Launch& L, const double* V, long long ldv, const double* coef, int n,
+             double* out, const Ctrl* ctrl, int mode, const double* xk, const double* gb,
+             const double* start, double h);
+void basis_residual_final(const Launch& L, Ctrl* ctrl, double* out);
+size_t ctrl_size();
+
+}  // namespace dev
+}  // namespace exg

@@ -1,0 +1,198 @@
+// extern "C" glue for the host-side API declared in include/exg_host.h.
+#include <cmath>
+#include <cstring>
+#include <limits>
+
+#include "host.hpp"
+
+
+namespace {
+thread_local std::string g_host_err;
+}
+
+const char* exg_host_last_error() { return g_host_err.c_str(); }
+
+#define HOST_GUARD_BEGIN try {
+#define HOST_GUARD_END                        \
+    }                                         \
+    catch (const exg::Error& e) {             \
+        g_host_err = e.what;                  \
+        return e.status;                      \
+    }                                         \
+    catch (const std::bad_alloc&) {           \
+        g_host_err = "host allocation failed"; \
+        return EXG_E_NOMEM;                   \
+    }                                         \
+    catch (const std::exception& e) {         \
+        g_host_err = e.what();                \
+        return EXG_E_CONTRACT;                \
+    }                                         \
+    return EXG_OK;
+
+extern "C" {
+
+const char* exg_host_error_message(void) { return g_host_err.c_str(); }
+
+exg_status exg_system_generate(const exg_gen_params* p, exg_system** out) {
+    HOST_GUARD_BEGIN
+    auto* s = new exg_system();
+    try {
+        exg::generate(*p, s->sys);
+    } catch (...) {
+        delete s;
+        throw;
+    }
+    *out = s;
+    HOST_GUARD_END
+}
+
+exg_status exg_system_build(int n_elems, const exg_element* elems, int n_sources,
+                            const exg_source* sources, int n_pwl, const double* pwl_t,
+                            const double* pwl_v, int n_models, const exg_mos_model* models,
+                            const exg_options* opts, exg_system** out) {
+    HOST_GUARD_BEGIN
+    auto* s = new exg_system();
+    s->sys.opts = opts ? *opts : exg::default_options();
+    s->sys.elems.assign(elems, elems + n_elems);
+    s->sys.src_desc.assign(sources, sources + n_sources);
+    if (n_pwl > 0) {
+        s->sys.pwl_t.assign(pwl_t, pwl_t + n_pwl);
+        s->sys.pwl_v.assign(pwl_v, pwl_v + n_pwl);
+    }
+    if (n_models > 0) s->sys.models.assign(models, models + n_models);
+    try {
+        exg::build_mna(s->sys);
+    } catch (...) {
+        delete s;
+        throw;
+    }
+    *out = s;
+    HOST_GUARD_END
+}
+
+void exg_system_free(exg_system* s) { delete s; }
+int exg_system_n(const exg_system* s) { return s->sys.n; }
+int exg_system_n_nodes(const exg_system* s) { return s->sys.n_nodes; }
+int exg_system_n_inputs(const exg_system* s) { return s->sys.n_inputs(); }
+
+exg_status exg_system_csr(const exg_system* s, int which, int* n_rows, int* n_cols, int* nnz,
+                          const int** rowptr, const int** col, const double** val) {
+    const exg::Csr* m = which == EXG_MAT_C ? &s->sys.C : which == EXG_MAT_G ? &s->sys.G
+                                                     : which == EXG_MAT_B ? &s->sys.B : nullptr;
+    if (!m) return EXG_E_CONTRACT;
+    *n_rows = m->n_rows;
+    *n_cols = m->n_cols;
+    *nnz = m->nnz();
+    *rowptr = m->rowptr.data();
+    *col = m->col.data();
+    *val = m->val.data();
+    return EXG_OK;
+}
+
+exg_status exg_system_elements(const exg_system* s, int* n_elems, const exg_element** elems,
+                               int* n_sources, const exg_source** sources, int* n_pwl,
+                               const double** pwl_t, const double** pwl_v, int* n_models,
+                               const exg_mos_model** models) {
+    *n_elems = static_cast<int>(s->sys.elems.size());
+    *elems = s->sys.elems.data();
+    *n_sources = static_cast<int>(s->sys.src_desc.size());
+    *sources = s->sys.src_desc.data();
+    *n_pwl = static_cast<int>(s->sys.pwl_t.size());
+    *pwl_t = s->sys.pwl_t.data();
+    *pwl_v = s->sys.pwl_v.data();
+    *n_models = static_cast<int>(s->sys.models.size());
+    *models = s->sys.models.data();
+    return EXG_OK;
+}
+
+exg_status exg_system_options(const exg_system* s, exg_options* out) {
+    *out = s->sys.opts;
+    return EXG_OK;
+}
+
+int exg_system_unknown_of_label(const exg_system* s, int label) {
+    if (label < 0 || label >= static_cast<int>(s->sys.unknown_of_label.size())) return -1;
+    return s->sys.unknown_of_label[label];
+}
+
+exg_status exg_sources_eval(const exg_system* s, double t, double* u) {
+    HOST_GUARD_BEGIN
+    const auto v = exg::eval_sources(s->sys, t);
+    std::memcpy(u, v.data(), sizeof(double) * v.size());
+    HOST_GUARD_END
+}
+
+int exg_breakpoints(const exg_system* s, double t0, double t1, double* out, int cap) {
+    try {
+        const auto v = exg::source_breakpoints(s->sys, t0, t1);
+        for (int i = 0; i < static_cast<int>(v.size()) && i < cap; ++i) out[i] = v[i];
+        return static_cast<int>(v.size());
+    } catch (const exg::Error& e) {
+        g_host_err = e.what;
+        return -1;
+    }
+}
+
+exg_status exg_lu_factor(int n, const int* rowptr, const int* col, const double* val,
+                         double pivot_tol, exg_factor** out) {
+    HOST_GUARD_BEGIN
+    exg::Csr A;
+    A.n_rows = A.n_cols = n;
+    A.rowptr.assign(rowptr, rowptr + n + 1);
+    A.col.assign(col, col + rowptr[n]);
+    A.val.assign(val, val + rowptr[n]);
+    auto* f = new exg_factor();
+    try {
+        exg::lu_factor(A, pivot_tol, f->f);
+    } catch (...) {
+        delete f;
+        throw;
+    }
+    *out = f;
+    HOST_GUARD_END
+}
+
+void exg_factor_free(exg_factor* f) { delete f; }
+
+exg_status exg_factor_get(const exg_factor* fp, int* n, const int** Lp, const int** Li,
+                          const double** Lx, const int** Up, const int** Ui, const double** Ux,
+                          const int** row_perm, const int** col_perm) {
+    const exg::Factor& f = fp->f;
+    *n = f.n;
+    *Lp = f.L.rowptr.data();
+    *Li = f.L.col.data();
+    *Lx = f.L.val.data();
+    *Up = f.U.rowptr.data();
+    *Ui = f.U.col.data();
+    *Ux = f.U.val.data();
+    *row_perm = f.row_perm.data();
+    *col_perm = f.col_perm.data();
+    return EXG_OK;
+}
+
+exg_status exg_factor_timing(const exg_factor* f, double* order_s, double* numeric_s) {
+    *order_s = f->f.order_s;
+    *numeric_s = f->f.numeric_s;
+    return EXG_OK;
+}
+
+exg_status exg_step_control_from(const exg_system* s, exg_step_control* c) {
+    const exg_options& o = s->sys.opts;
+    c->err_budget = o.err_budget;
+    c->alpha = 0.5;
+    c->beta = 2.0;
+    c->grow_threshold = 5;
+    c->grow_only_on_clean = 1;
+    c->eps = o.krylov_eps;
+    c->m_max = o.m_max;
+    c->max_rejects = 40;
+    c->h_init = 0.0;
+    c->hmin = std::isnan(o.hmin) ? 0.0 : o.hmin;
+    c->hmax = std::isnan(o.hmax) ? std::numeric_limits<double>::infinity() : o.hmax;
+    c->fixed_step = 0;
+    c->method = EXG_METHOD_ER;
+    c->gamma = 0.1;
+    return EXG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,1062 @@
+// sm_100a kernels of the invert-Krylov ER hot path (fp64, HBM-bound).
+// See kernels.cuh for the reference routine each kernel restates.
+#include <algorithm>
+#include <cfloat>
+#include <climits>
+
+#include "device.hpp"
+#include "kernels.cuh"
+
+namespace exg {
+namespace dev {
+
+// ============================================================================
+// CSR SpMV, row-sequential (bit-identical to spmv, sparse_matrix.cpp:76-80).
+// One warp owns 32 consecutive rows; their nonzeros are staged into shared
+// memory with coalesced loads, then each lane accumulates its own row in the
+// reference's column order.  Rows whose 32-row segment exceeds the staging
+// capacity read global memory directly.
+// ============================================================================
+constexpr int kSpmvWarps = 8;
+constexpr int kSpmvCap = 384;  // entries staged per warp (4.5 KB)
+
+template <typename XFn, typename OutFn>
+__device__ __forceinline__ void spmv_warp_rows(const int* __restrict__ rowptr,
+                                               const int* __restrict__ col,
+                                               const double* __restrict__ val, int n_rows,
+                                               int warp_global, XFn xfn, OutFn out,
+                                               int (*s_col)[kSpmvCap], double (*s_val)[kSpmvCap]) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int r0 = warp_global * 32;
+    if (r0 >= n_rows) return;
+    const int r_end = min(r0 + 32, n_rows);
+    const int k0 = rowptr[r0], k1 = rowptr[r_end];
+    const int r = r0 + lane;
+    if (k1 - k0 <= kSpmvCap) {
+        for (int k = k0 + lane; k < k1; k += 32) {
+            s_col[w][k - k0] = col[k];
+            s_val[w][k - k0] = val[k];
+        }
+        __syncwarp();
+        if (r < n_rows) {
+            double s = 0.0;
+            const int a = rowptr[r] - k0, b = rowptr[r + 1] - k0;
+            for (int k = a; k < b; ++k) s += s_val[w][k] * xfn(s_col[w][k]);
+            out(r, s);
+        }
+        __syncwarp();
+    } else if (r < n_rows) {
+        double s = 0.0;
+        for (int k = rowptr[r]; k < rowptr[r + 1]; ++k) s += val[k] * xfn(col[k]);
+        out(r, s);
+    }
+}
+
+__global__ void __launch_bounds__(kSpmvWarps * 32)
+    k_spmv(const int* __restrict__ rowptr, const int* __restrict__ col,
+           const double* __restrict__ val, int n_rows, const double* __restrict__ x,
+           double* __restrict__ y, const Ctrl* ctrl, const double* __restrict__ xcol_base,
+           long long ldv) {
+    // when xcol_base is set, x = V[ctrl->j] (column of the Krylov basis)
+    if (ctrl && (ctrl->converged || ctrl->status)) return;
+    const double* xs = x;
+    if (xcol_base) xs = xcol_base + (long long)ctrl->j * ldv;
+    __shared__ int s_col[kSpmvWarps][kSpmvCap];
+    __shared__ double s_val[kSpmvWarps][kSpmvCap];
+    const int wg = blockIdx.x * kSpmvWarps + (threadIdx.x >> 5);
+    spmv_warp_rows(rowptr, col, val, n_rows, wg, [&](int c) { return xs[c]; },
+                   [&](int r, double s) { y[r] = s; }, s_col, s_val);
+}
+
+// t1 = 0.0 + 1.0 * (B u_k)  (add(residual_F == 0, spmv(B, u_k)), integrate.cpp:224)
+// t2 = B * slope, slope = (u_k1 - u_k) * (1/h)              (integrate.cpp:220-221,228)
+__global__ void __launch_bounds__(kSpmvWarps * 32)
+    k_spmv_b2(const int* __restrict__ rowptr, const int* __restrict__ col,
+              const double* __restrict__ val, int n_rows, const double* __restrict__ u_k,
+              const double* __restrict__ u_k1, double h, double* __restrict__ t1,
+              double* __restrict__ t2) {
+    __shared__ int s_col[kSpmvWarps][kSpmvCap];
+    __shared__ double s_val[kSpmvWarps][kSpmvCap];
+    const int wg = blockIdx.x * kSpmvWarps + (threadIdx.x >> 5);
+    spmv_warp_rows(rowptr, col, val, n_rows, wg, [&](int c) { return u_k[c]; },
+                   [&](int r, double s) { t1[r] = 0.0 + 1.0 * s; }, s_col, s_val);
+    const double ih = 1.0 / h;
+    spmv_warp_rows(rowptr, col, val, n_rows, wg,
+                   [&](int c) { return (u_k1[c] + -1.0 * u_k[c]) * ih; },
+                   [&](int r, double s) { t2[r] = s; }, s_col, s_val);
+}
+
+// ============================================================================
+// Sparse triangular solves, sync-free.
+//
+// Rows are visited in level order (host level analysis at exg_set_factors);
+// blocks take consecutive slices of that order through an atomic ticket, so a
+// row only ever waits on rows already owned by running (or finished) blocks:
+// no deadlock, no per-level launches.  The value itself is the ready flag:
+// the output vector is pre-filled with an all-ones NaN sentinel and every row
+// publishes its result with one 64-bit relaxed store; dependents poll the
+// value with L1-bypassing relaxed loads.
+//
+// EXACT: every row accumulates in the reference's order (L: increasing
+// column; U: increasing column, then divides by the diagonal) —
+// bit-identical to Factorization::solve.  FAST: U rows accumulate in
+// decreasing column order, so the most recently solved dependency comes last
+// and the row's work overlaps its wait (deterministic, not bit-identical).
+// ============================================================================
+constexpr int kTrsvThreads = 128;
+
+template <bool UPPER, bool REVERSE>
+__global__ void __launch_bounds__(kTrsvThreads)
+    k_trsv(TrsvArgs a) {
+    __shared__ unsigned int s_blk;
+    if (a.ctrl && a.ctrl->converged) return;
+    if (threadIdx.x == 0) s_blk = atomicAdd(a.ticket, 1u) + 1u;  // ticket starts at 0xFFFFFFFF
+    __syncthreads();
+    const unsigned int i = s_blk * kTrsvThreads + threadIdx.x;
+    if (i >= (unsigned)a.n) return;
+    const int r = a.order[i];
+    double s = UPPER ? a.in[r] : a.in[a.in_perm[r]];
+    const int k0 = a.ptr[r], k1 = a.ptr[r + 1];
+    constexpr int CH = 4;
+    if (!REVERSE) {
+        int k = k0;
+        for (; k + CH <= k1; k += CH) {
+            int c[CH];
+            double v[CH];
+            unsigned long long y[CH];
+#pragma unroll
+            for (int q = 0; q < CH; ++q) {
+                c[q] = a.col[k + q];
+                v[q] = a.val[k + q];
+            }
+#pragma unroll
+            for (int q = 0; q < CH; ++q) y[q] = ld_relaxed(a.out + c[q]);
+#pragma unroll
+            for (int q = 0; q < CH; ++q) {
+                while (y[q] == kSentinel) y[q] = ld_relaxed(a.out + c[q]);
+                s -= v[q] * __longlong_as_double(y[q]);
+            }
+        }
+        for (; k < k1; ++k) {
+            const int c = a.col[k];
+            unsigned long long y = ld_relaxed(a.out + c);
+            while (y == kSentinel) y = ld_relaxed(a.out + c);
+            s -= a.val[k] * __longlong_as_double(y);
+        }
+    } else {
+        int k = k1 - 1;
+        for (; k - CH + 1 >= k0; k -= CH) {
+            int c[CH];
+            double v[CH];
+            unsigned long long y[CH];
+#pragma unroll
+            for (int q = 0; q < CH; ++q) {
+                c[q] = a.col[k - q];
+                v[q] = a.val[k - q];
+            }
+#pragma unroll
+            for (int q = 0; q < CH; ++q) y[q] = ld_relaxed(a.out + c[q]);
+#pragma unroll
+            for (int q = 0; q < CH; ++q) {
+                while (y[q] == kSentinel) y[q] = ld_relaxed(a.out + c[q]);
+                s -= v[q] * __longlong_as_double(y[q]);
+            }
+        }
+        for (; k >= k0; --k) {
+            const int c = a.col[k];
+            unsigned long long y = ld_relaxed(a.out + c);
+            while (y == kSentinel) y = ld_relaxed(a.out + c);
+            s -= a.val[k] * __longlong_as_double(y);
+        }
+    }
+    if (UPPER) s = s / a.diag[r];
+    st_relaxed(a.out + r, s);
+    if (a.final_out) {
+        // out[col_perm[r]] = coef * x (+ add[col_perm[r]]): scatter + the
+        // caller's vector update, fused (sparse_lu.cpp:289, integrate.cpp)
+        const int q = a.out_perm[r];
+        double y = a.coef * s;
+        if (a.add) y = a.add[q] + y;
+        a.final_out[q] = y;
+    }
+}
+
+// ============================================================================
+// Factor apply y = P^T L U Q^T x (sparse_lu.cpp:293-304), row-sequential.
+// apply_u: t[r] = diag*x[cp[r]] + sum_{c>r} U_rc x[cp[c]]  (diagonal first)
+// apply_l: y[r] = sum_{c<r} L_rc t[c] + 1.0*t[r]          (diagonal last)
+// apply_l also reduces ||y||^2 (the residual weight, krylov.cpp:238) and,
+// when ctrl is set, takes the Arnoldi convergence decision in its last block.
+// ============================================================================
+__global__ void __launch_bounds__(kSpmvWarps * 32)
+    k_apply_u_diag(const int* __restrict__ uptr, const int* __restrict__ ucol,
+                   const double* __restrict__ uval, const double* __restrict__ udiag, int n,
+                   const int* __restrict__ col_perm, const double* __restrict__ x,
+                   double* __restrict__ t, const Ctrl* ctrl, const double* __restrict__ vbase,
+                   long long ldv) {
+    const double* xs = x;
+    if (ctrl) {
+        if (!ctrl->need_weight || ctrl->converged || ctrl->status) return;
+        xs = vbase + (long long)ctrl->m * ldv;
+    }
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    double s = 0.0;
+    s += udiag[r] * xs[col_perm[r]];
+    for (int k = uptr[r]; k < uptr[r + 1]; ++k) s += uval[k] * xs[col_perm[ucol[k]]];
+    t[r] = s;
+}
+
+__device__ void decide(Ctrl* c);
+
+__global__ void __launch_bounds__(256)
+    k_apply_l_norm(const int* __restrict__ lptr, const int* __restrict__ lcol,
+                   const double* __restrict__ lval, int n, const double* __restrict__ t,
+                   double* __restrict__ y_out, const int* __restrict__ row_perm,
+                   double* __restrict__ partials, unsigned int* __restrict__ done_counter,
+                   Ctrl* ctrl, double* __restrict__ weight_out) {
+    __shared__ double sh[33];
+    __shared__ bool s_last;
+    if (ctrl && (!ctrl->need_weight || ctrl->converged || ctrl->status)) return;
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    double sq = 0.0;
+    if (r < n) {
+        double s = 0.0;
+        for (int k = lptr[r]; k < lptr[r + 1]; ++k) s += lval[k] * t[lcol[k]];
+        s += 1.0 * t[r];
+        if (y_out) y_out[row_perm[r]] = s;
+        sq = s * s;
+    }
+    const double bs = block_sum(sq, sh);
+    if (threadIdx.x == 0) {
+        partials[blockIdx.x] = bs;
+        __threadfence();
+        const unsigned int prev = atomicAdd(done_counter, 1u);
+        s_last = (prev == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    // last block: fixed-order final sum of the block partials
+    double acc = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) acc += ld_cg(partials + b);
+    const double tot = block_sum(acc, sh);
+    if (threadIdx.x == 0) {
+        *done_counter = 0u;
+        const double w = sqrt(tot);
+        if (weight_out) *weight_out = w;
+        if (ctrl) {
+            ctrl->weight = w;
+            decide(ctrl);
+        }
+    }
+}
+
+// residual test of the Arnoldi iteration (krylov.cpp:150-168)
+__device__ void decide(Ctrl* c) {
+    if (c->status || c->converged) return;
+    if (c->need_weight) {
+        const double res = fabs(c->beta * c->h_next * c->s) * c->weight;
+        c->last_residual = res;
+        c->need_weight = 0;
+        if (res < c->eps) c->converged = 1;
+    }
+}
+
+// after every iteration: cap check and advance (krylov.cpp:118,165-168)
+__global__ void k_iter_end(Ctrl* c) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    c->arnoldi_iters++;
+    if (c->status || c->converged) return;
+    if (c->need_weight) decide(c);  // weight computed by another path
+    if (c->converged) return;
+    if (c->m >= c->m_max) {
+        c->status = 5;  // EXG_E_NO_CONVERGENCE
+        return;
+    }
+    c->j = c->m;
+}
+
+// ============================================================================
+// ||G v|| weight (mevp_residual, krylov.cpp:204; EXG_WEIGHT_GSPMV mode)
+// ============================================================================
+__global__ void __launch_bounds__(256)
+    k_spmv_norm(const int* __restrict__ rowptr, const int* __restrict__ col,
+                const double* __restrict__ val, int n, const double* __restrict__ vbase,
+                long long ldv, double* __restrict__ partials, unsigned int* done_counter,
+                Ctrl* ctrl, int from_ctrl_m, double* weight_out) {
+    __shared__ double sh[33];
+    __shared__ bool s_last;
+    const double* x = vbase;
+    if (ctrl && from_ctrl_m) {
+        if (!ctrl->need_weight || ctrl->converged || ctrl->status) return;
+        x = vbase + (long long)ctrl->m * ldv;
+    }
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    double sq = 0.0;
+    if (r < n) {
+        double s = 0.0;
+        for (int k = rowptr[r]; k < rowptr[r + 1]; ++k) s += val[k] * x[col[k]];
+        sq = s * s;
+    }
+    const double bs = block_sum(sq, sh);
+    if (threadIdx.x == 0) {
+        partials[blockIdx.x] = bs;
+        __threadfence();
+        s_last = atomicAdd(done_counter, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    double acc = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) acc += ld_cg(partials + b);
+    const double tot = block_sum(acc, sh);
+    if (threadIdx.x == 0) {
+        *done_counter = 0u;
+        const double w = sqrt(tot);
+        if (weight_out) *weight_out = w;
+        if (ctrl && from_ctrl_m) {
+            ctrl->weight = w;
+            decide(ctrl);
+        }
+    }
+}
+
+// ============================================================================
+// MEVP start: beta = ||v||, ||x_k||_inf, early-out (integrate.cpp:244),
+// zero-start check (krylov.cpp:106), V[0] = v * (1/beta) (krylov.cpp:113).
+// Two kernels: per-block partials, then every block redundantly finalises
+// (same fixed order => same beta everywhere) and scales its slice.
+// ============================================================================
+__global__ void __launch_bounds__(256)
+    k_start_partials(const double* __restrict__ v, const double* __restrict__ xk, int n,
+                     double* __restrict__ partials /* [2*grid] */) {
+    __shared__ double sh[33];
+    double sq = 0.0, mx = 0.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        sq += v[i] * v[i];
+        if (xk) {
+            const double a = fabs(xk[i]);
+            mx = mx < a ? a : mx;  // std::max(m, |x|)
+        }
+    }
+    const double bs = block_sum(sq, sh);
+    // max reduction (order-independent)
+    for (int o = 16; o > 0; o >>= 1) {
+        const double t = __shfl_down_sync(0xffffffffu, mx, o);
+        mx = mx < t ? t : mx;
+    }
+    __shared__ double shm[32];
+    if ((threadIdx.x & 31) == 0) shm[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double m = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = m < shm[w] ? shm[w] : m;
+        partials[blockIdx.x] = bs;
+        partials[gridDim.x + blockIdx.x] = m;
+    }
+}
+
+__global__ void __launch_bounds__(256)
+    k_start_finish(const double* __restrict__ v, int n, const double* __restrict__ partials,
+                   int n_part, double* __restrict__ v0, Ctrl* ctrl, int er_mode) {
+    __shared__ double sh[33];
+    __shared__ double s_beta;
+    __shared__ int s_go;
+    double acc = 0.0;
+    for (int b = threadIdx.x; b < n_part; b += blockDim.x) acc += partials[b];
+    const double tot = block_sum(acc, sh);
+    if (threadIdx.x == 0) {
+        double xinf = 0.0;
+        for (int b = 0; b < n_part; ++b) xinf = xinf < partials[n_part + b] ? partials[n_part + b] : xinf;
+        const double beta = sqrt(tot);
+        int go = 1;
+        if (er_mode && beta <= 1e-9 * (1.0 + xinf)) go = 0;  // equilibrium early-out
+        if (go && beta == 0.0) go = -1;                          // ZeroStartVectorError
+        s_beta = beta;
+        s_go = go;
+        if (blockIdx.x == 0) {
+            ctrl->beta = beta;
+            ctrl->xinf = xinf;
+            ctrl->skip = go == 0;
+            ctrl->fresh = go == 1;
+            ctrl->status = go < 0 ? 4 : 0;
+            ctrl->converged = go != 1;  // nothing to iterate
+            ctrl->j = 0;
+            ctrl->m = 0;
+            ctrl->happy = 0;
+            ctrl->need_weight = 0;
+            ctrl->last_residual = __longlong_as_double(0x7FF0000000000000ll);  // +inf
+        }
+    }
+    __syncthreads();
+    if (s_go != 1) return;
+    const double ib = 1.0 / s_beta;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        v0[i] = v[i] * ib;
+}
+
+// ============================================================================
+// Modified Gram–Schmidt with one conditional re-orthogonalisation
+// (krylov.cpp:46-78), one cooperative persistent kernel per Arnoldi step.
+// Each thread keeps K elements of w in registers for the whole step, so each
+// MGS pass streams only v_i from HBM.  The passes keep the reference's
+// sequential dependence (h_i is the dot of the ALREADY-updated w with v_i) and
+// its per-element update order; only the dot-product summation order differs
+// (fixed tree: thread -> warp -> block -> ordered sum over blocks).
+// ============================================================================
+template <int K>
+__device__ __forceinline__ double grid_sum(double v, double* sh, double* partials, int slot,
+                                           unsigned int* bar) {
+    const double bs = block_sum(v, sh);
+    double* pp = partials + slot * 4096;
+    if (threadIdx.x == 0) pp[blockIdx.x] = bs;
+    grid_barrier(bar, gridDim.x);
+    if (gridDim.x == 1) return bs;
+    double acc = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) acc += ld_cg(pp + b);
+    return block_sum(acc, sh);
+}
+
+template <int K>
+__global__ void __launch_bounds__(1024)
+    k_mgs(MgsArgs a) {
+    __shared__ double sh[33];
+    Ctrl* c = a.ctrl;
+    if (c->converged || c->status) return;
+    const int j = c->j;
+    const int n = a.n;
+    const long long ld = a.ldv;
+    const int nthr = gridDim.x * blockDim.x;
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    double w[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const int e = g + k * nthr;
+        w[k] = e < n ? a.w[e] : 0.0;
+    }
+    int slot = 0;
+    double p = 0.0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) p += w[k] * w[k];
+    const double pre = sqrt(grid_sum<K>(p, sh, a.partials, slot ^= 1, a.bar));
+    double* hcol = a.hbar + (long long)j * a.hld;
+    for (int pass = 0; pass < 2; ++pass) {
+        for (int i = 0; i <= j; ++i) {
+            const double* vi = a.V + (long long)i * ld;
+            double vv[K];
+            double d = 0.0;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const int e = g + k * nthr;
+                vv[k] = e < n ? vi[e] : 0.0;
+                d += w[k] * vv[k];
+            }
+            const double hij = grid_sum<K>(d, sh, a.partials, slot ^= 1, a.bar);
+            const double mh = -hij;
+#pragma unroll
+            for (int k = 0; k < K; ++k) w[k] += mh * vv[k];
+            if (g == 0) hcol[i] = pass == 0 ? hij : hcol[i] + hij;
+        }
+        double q = 0.0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) q += w[k] * w[k];
+        const double post = sqrt(grid_sum<K>(q, sh, a.partials, slot ^= 1, a.bar));
+        if (pass == 1 || !(post < kReorthFactor * pre)) {
+            const bool happy = post <= c->breakdown_tol * pre;
+            if (!happy) {
+                const double ip = 1.0 / post;
+                double* vn = a.V + (long long)(j + 1) * ld;
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    const int e = g + k * nthr;
+                    if (e < n) vn[e] = w[k] * ip;
+                }
+            }
+            if (g == 0) {
+                hcol[j + 1] = post;
+                c->pre = pre;
+                c->post = post;
+                c->happy = happy;
+                c->h_next = happy ? 0.0 : post;
+                c->m = j + 1;
+            }
+            return;
+        }
+    }
+}
+
+template __global__ void k_mgs<1>(MgsArgs);
+template __global__ void k_mgs<2>(MgsArgs);
+template __global__ void k_mgs<4>(MgsArgs);
+template __global__ void k_mgs<8>(MgsArgs);
+template __global__ void k_mgs<16>(MgsArgs);
+
+// ============================================================================
+// Dense m x m block in one CTA (m <= MMAX): H_m, its inverse with the shift
+// fallback, Pade scaling-and-squaring exponential, the residual scalar s and
+// the final coefficients beta * e^{hH^-1} e_1.  Every loop keeps the
+// reference's per-element operation order (dense_matrix.cpp), parallelising
+// only across independent elements, so the results are bit-identical.
+// ============================================================================
+struct DenseCtx {
+    int m;
+    double* S;  // scratch base
+    int* flag;  // shared flags
+};
+
+__device__ __forceinline__ void bsync() { __syncthreads(); }
+
+// c = a * b  (i-k-j with the zero skip of multiply, :33-45); c must not alias
+__device__ void d_mmul(int m, const double* a, const double* b, double* c) {
+    for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) {
+        const int i = idx / m, jj = idx - i * m;
+        double s = 0.0;
+        for (int k = 0; k < m; ++k) {
+            const double aik = a[i * m + k];
+            if (aik == 0.0) continue;
+            s += aik * b[k * m + jj];
+        }
+        c[idx] = s;
+    }
+    bsync();
+}
+
+// c = a + beta * b (add_scaled, :60-67); c may alias a or b
+__device__ void d_axpby(int m, const double* a, double beta, const double* b, double* c) {
+    for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) c[idx] = a[idx] + beta * b[idx];
+    bsync();
+}
+__device__ void d_scale(int m, double f, const double* a, double* c) {
+    for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) c[idx] = f * a[idx];
+    bsync();
+}
+__device__ void d_copy(int m, const double* a, double* c) {
+    for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) c[idx] = a[idx];
+    bsync();
+}
+__device__ void d_ident(int m, double* c) {
+    for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) c[idx] = (idx / m == idx % m) ? 1.0 : 0.0;
+    bsync();
+}
+
+// max column sum (norm1, :17-25); result broadcast through sh_val
+__device__ double d_norm1(int m, const double* a, double* colsum, double* sh_val) {
+    for (int cc = threadIdx.x; cc < m; cc += blockDim.x) {
+        double s = 0.0;
+        for (int r = 0; r < m; ++r) s += fabs(a[r * m + cc]);
+        colsum[cc] = s;
+    }
+    bsync();
+    if (threadIdx.x == 0) {
+        double best = 0.0;
+        for (int cc = 0; cc < m; ++cc) best = best < colsum[cc] ? colsum[cc] : best;  // std::max
+        *sh_val = best;
+    }
+    bsync();
+    return *sh_val;
+}
+
+// dense_solve (:69-118): A X = B by partial-pivot LU.  x holds B on entry and
+// X on exit (m x m).  Returns false on an exactly-zero pivot column
+// (SingularMatrixError).
+__device__ bool d_solve(int m, const double* a, double* x, double* lu, int* sh_i, double* sh_d) {
+    d_copy(m, a, lu);
+    for (int k = 0; k < m; ++k) {
+        if (threadIdx.x < 32) {
+            const int lane = threadIdx.x;
+            const double dkk = fabs(lu[k * m + k]);
+            double lb = -1.0;
+            int li = INT_MAX;
+            for (int r = k + 1 + lane; r < m; r += 32) {
+                const double v = fabs(lu[r * m + k]);
+                if (v > lb) {
+                    lb = v;
+                    li = r;
+                }
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ob = __shfl_down_sync(0xffffffffu, lb, o);
+                const int oi = __shfl_down_sync(0xffffffffu, li, o);
+                if (ob > lb || (ob == lb && oi < li)) {
+                    lb = ob;
+                    li = oi;
+                }
+            }
+            if (lane == 0) {
+                int p = k;
+                double best = dkk;
+                if (!isnan(dkk) && li != INT_MAX && lb > dkk) {
+                    p = li;
+                    best = lb;
+                }
+                sh_i[0] = p;
+                sh_d[0] = best;
+            }
+        }
+        bsync();
+        const int p = sh_i[0];
+        if (sh_d[0] == 0.0) return false;
+        if (p != k) {
+            for (int jj = threadIdx.x; jj < m; jj += blockDim.x) {
+                double t = lu[k * m + jj];
+                lu[k * m + jj] = lu[p * m + jj];
+                lu[p * m + jj] = t;
+                t = x[k * m + jj];
+                x[k * m + jj] = x[p * m + jj];
+                x[p * m + jj] = t;
+            }
+            bsync();
+        }
+        const double d = lu[k * m + k];
+        for (int r = k + 1 + threadIdx.x; r < m; r += blockDim.x) lu[r * m + k] = lu[r * m + k] / d;
+        bsync();
+        // rows r > k: lu[r][k+1..m) and x[r][0..m)
+        const int wl = m - k - 1, wx = m;
+        const int per_row = wl + wx;
+        for (int idx = threadIdx.x; idx < (m - k - 1) * per_row; idx += blockDim.x) {
+            const int r = k + 1 + idx / per_row;
+            const int q = idx - (r - k - 1) * per_row;
+            const double f = lu[r * m + k];
+            if (f == 0.0) continue;
+            if (q < wl) {
+                const int jj = k + 1 + q;
+                lu[r * m + jj] -= f * lu[k * m + jj];
+            } else {
+                const int jj = q - wl;
+                x[r * m + jj] -= f * x[k * m + jj];
+            }
+        }
+        bsync();
+    }
+    // back substitution, one thread per right-hand-side column
+    for (int jj = threadIdx.x; jj < m; jj += blockDim.x) {
+        for (int k = m - 1; k >= 0; --k) {
+            const double d = lu[k * m + k];
+            double s = x[k * m + jj];
+            for (int cc = k + 1; cc < m; ++cc) s -= lu[k * m + cc] * x[cc * m + jj];
+            x[k * m + jj] = s / d;
+        }
+    }
+    bsync();
+    return true;
+}
+
+// dense_inverse (:120-124) with cond1 = ||A||_1 ||A^-1||_1
+__device__ bool d_inverse(int m, const double* a, double* inv, double* lu, double* colsum,
+                          int* sh_i, double* sh_d, double* cond) {
+    d_ident(m, inv);
+    if (!d_solve(m, a, inv, lu, sh_i, sh_d)) return false;
+    const double na = d_norm1(m, a, colsum, sh_d + 1);
+    const double ni = d_norm1(m, inv, colsum, sh_d + 1);
+    *cond = na * ni;
+    return true;
+}
+
+// invert_reduced (krylov.cpp:85-101)
+__device__ bool d_invert_reduced(int m, const double* hm, double* hinv, double* sh_m,
+                                 double* lu, double* colsum, int* sh_i, double* sh_d) {
+    double scale = d_norm1(m, hm, colsum, sh_d + 2);
+    scale = scale < 1e-300 ? 1e-300 : scale;  // std::max(norm1, 1e-300)
+    const double deltas[3] = {0.0, 1e-12 * scale, 1e-9 * scale};
+    for (int t = 0; t < 3; ++t) {
+        d_copy(m, hm, sh_m);
+        for (int i = threadIdx.x; i < m; i += blockDim.x) sh_m[i * m + i] -= deltas[t];
+        bsync();
+        double cond = 0.0;
+        if (d_inverse(m, sh_m, hinv, lu, colsum, sh_i, sh_d, &cond) && cond < kCondLimit) return true;
+    }
+    return false;
+}
+
+// pade_expm (:137-181).  w: 10 scratch matrices.
+__device__ bool d_pade(int m, const double* a, const double* b, int degree, double* out,
+                       double* w, double* colsum, int* sh_i, double* sh_d) {
+    const int mm = m * m;
+    double* ident = w;
+    double* a2 = w + mm;
+    double* u = w + 2 * mm;
+    double* v = w + 3 * mm;
+    double* t1 = w + 4 * mm;
+    double* t2 = w + 5 * mm;
+    double* t3 = w + 6 * mm;
+    double* t4 = w + 7 * mm;
+    double* t5 = w + 8 * mm;
+    double* lu = w + 9 * mm;
+    d_ident(m, ident);
+    d_mmul(m, a, a, a2);
+    if (degree <= 9) {
+        double* usum = t1;
+        double* vsum = t2;
+        double* pw = t3;
+        for (int idx = threadIdx.x; idx < mm; idx += blockDim.x) {
+            usum[idx] = 0.0;
+            vsum[idx] = 0.0;
+        }
+        d_copy(m, ident, pw);
+        for (int k = 0; k <= degree; k += 2) {
+            d_axpby(m, vsum, b[k], pw, vsum);
+            d_axpby(m, usum, b[k + 1], pw, usum);
+            if (k + 2 <= degree) {
+                d_mmul(m, pw, a2, t4);
+                d_copy(m, t4, pw);
+            }
+        }
+        d_mmul(m, a, usum, u);
+        d_copy(m, vsum, v);
+    } else {
+        double* a4 = t1;
+        double* a6 = t2;
+        d_mmul(m, a2, a2, a4);
+        d_mmul(m, a4, a2, a6);
+        // u1 = a6 * (b13 a6 + b11 a4 + b9 a2)
+        d_scale(m, b[13], a6, t3);
+        d_scale(m, b[11], a4, t4);
+        d_axpby(m, t3, 1.0, t4, t3);
+        d_scale(m, b[9], a2, t4);
+        d_axpby(m, t3, 1.0, t4, t3);
+        d_mmul(m, a6, t3, t5);  // u1
+        // u2 = b7 a6 + b5 a4 + b3 a2 + b1 I
+        d_scale(m, b[7], a6, t3);
+        d_scale(m, b[5], a4, t4);
+        d_axpby(m, t3, 1.0, t4, t3);
+        d_scale(m, b[3], a2, t4);
+        d_axpby(m, t3, 1.0, t4, t3);
+        d_axpby(m, t3, b[1], ident, t3);  // u2
+        d_axpby(m, t5, 1.0, t3, t4);      // u1 + u2
+        d_mmul(m, a, t4, u);
+        // v1 = a6 * (b12 a6 + b10 a4 + b8 a2)
+        d_scale(m, b[12], a6, t3);
+        d_scale(m, b[10], a4, t4);
+        d_axpby(m, t3, 1.0, t4, t3);
+        d_scale(m, b[8], a2, t4);
+        d_axpby(m, t3, 1.0, t4, t3);
+        d_mmul(m, a6, t3, t5);  // v1
+        d_scale(m, b[6], a6, t3);
+        d_scale(m, b[4], a4, t4);
+        d_axpby(m, t3, 1.0, t4, t3);
+        d_scale(m, b[2], a2, t4);
+        d_axpby(m, t3, 1.0, t4, t3);
+        d_axpby(m, t3, b[0], ident, t3);  // v2
+        d_axpby(m, t5, 1.0, t3, v);
+    }
+    // (V - U) X = (V + U)
+    d_axpby(m, v, 1.0, u, out);
+    d_axpby(m, v, -1.0, u, t1);
+    return d_solve(m, t1, out, lu, sh_i, sh_d);
+}
+
+// dense_expm (:185-225).  Returns 0 ok, 2 non-finite input, 3 singular solve.
+// w: 13 scratch matrices.
+__device__ int d_expm(int m, const double* M, double* out, double* w, double* colsum, int* sh_i,
+                      double* sh_d) {
+    const double c_b3[4] = {120, 60, 12, 1};
+    const double c_b5[6] = {30240, 15120, 3360, 420, 30, 1};
+    const double c_b7[8] = {17297280, 8648640, 1995840, 277200, 25200, 1512, 56, 1};
+    const double c_b9[10] = {17643225600., 8821612800., 2075673600., 302702400., 30270240.,
+                             2162160.,     110880.,     3960.,       90.,        1.};
+    const double c_b13[14] = {64764752532480000., 32382376266240000., 7771770303897600.,
+                              1187353796428800.,  129060195264000.,   10559470521600.,
+                              670442572800.,      33522128640.,       1323241920.,
+                              40840800.,          960960.,            16380.,
+                              182.,               1.};
+    const int mm = m * m;
+    if (threadIdx.x == 0) sh_i[1] = 0;
+    bsync();
+    for (int idx = threadIdx.x; idx < mm; idx += blockDim.x)
+        if (!isfinite(M[idx])) sh_i[1] = 1;
+    bsync();
+    if (sh_i[1]) return 2;
+    const double nrm = d_norm1(m, M, colsum, sh_d + 3);
+    const double theta3 = 1.495585217958292e-2, theta5 = 2.539398330063230e-1,
+                 theta7 = 9.504178996162932e-1, theta9 = 2.097847961257068e0,
+                 theta13 = 5.371920351148152e0;
+    bool ok;
+    if (nrm <= theta3) {
+        ok = d_pade(m, M, c_b3, 3, out, w, colsum, sh_i, sh_d);
+    } else if (nrm <= theta5) {
+        ok = d_pade(m, M, c_b5, 5, out, w, colsum, sh_i, sh_d);
+    } else if (nrm <= theta7) {
+        ok = d_pade(m, M, c_b7, 7, out, w, colsum, sh_i, sh_d);
+    } else if (nrm <= theta9) {
+        ok = d_pade(m, M, c_b9, 9, out, w, colsum, sh_i, sh_d);
+    } else {
+        int s = 0;
+        double sn = nrm;
+        while (sn > theta13) {
+            sn *= 0.5;
+            ++s;
+        }
+        double* a = w + 10 * mm;
+        const double f = ldexp(1.0, -s);
+        for (int idx = threadIdx.x; idx < mm; idx += blockDim.x) a[idx] = M[idx] * f;
+        bsync();
+        ok = d_pade(m, a, c_b13, 13, out, w, colsum, sh_i, sh_d);
+        double* t = w + 11 * mm;
+        for (int k = 0; k < s && ok; ++k) {
+            d_mmul(m, out, out, t);
+            d_copy(m, t, out);
+        }
+    }
+    return ok ? 0 : 3;
+}
+
+// Per-iteration dense step (krylov.cpp:129-163) and the final / re-check
+// evaluations (krylov.cpp:170-171, :191-215).
+//   mode 0: Arnoldi iteration check at ctrl->h
+//   mode 1: final coefficients coef[i] = beta * e^{h H^-1}(i,0) at h_eval
+//   mode 2: residual scalar s at h_eval for the cached basis (mevp_residual)
+__global__ void __launch_bounds__(256)
+    k_dense(DenseArgs a) {
+    extern __shared__ double dyn_smem[];
+    __shared__ int sh_i[4];
+    __shared__ double sh_d[8];
+    Ctrl* c = a.ctrl;
+    if (a.mode == 0 && (c->converged || c->status)) return;
+    if (a.mode == 1 && (c->status || c->skip)) return;
+    const int m = c->m;
+    const int mm = m * m;
+    double* S = a.use_smem ? dyn_smem : a.scratch;
+    double* hm = S;
+    double* hinv_tmp = S + mm;
+    double* e = S + 2 * mm;
+    double* sc = S + 3 * mm;
+    double* shm = S + 4 * mm;
+    double* lu = S + 5 * mm;
+    double* colsum = S + 6 * mm;  // m entries (one matrix reserved)
+    double* w = S + 7 * mm;       // 13 matrices
+    if (a.mode == 0) {
+        // H_m from the Hessenberg columns (reduced_from_cols, krylov.cpp:15-20)
+        for (int idx = threadIdx.x; idx < mm; idx += blockDim.x) {
+            const int i = idx / m, jj = idx - i * m;
+            hm[idx] = (i <= jj + 1) ? a.hbar[(long long)jj * a.hld + i] : 0.0;
+        }
+        bsync();
+        const bool inv = d_invert_reduced(m, hm, hinv_tmp, shm, lu, colsum, sh_i, sh_d);
+        if (c->happy) {
+            if (!inv) {
+                if (threadIdx.x == 0) c->status = 6;  // SingularReducedMatrixError
+                return;
+            }
+            for (int idx = threadIdx.x; idx < mm; idx += blockDim.x) a.hinv[idx] = hinv_tmp[idx];
+            if (threadIdx.x == 0) {
+                c->last_residual = 0.0;
+                c->converged = 1;
+                c->need_weight = 0;
+            }
+            return;
+        }
+        const bool check = (m % c->check_stride == 0) || m == c->m_max;
+        if (!check || !inv) {
+            if (threadIdx.x == 0) c->need_weight = 0;
+            return;
+        }
+        for (int idx = threadIdx.x; idx < mm; idx += blockDim.x) {
+            a.hinv[idx] = hinv_tmp[idx];
+            sc[idx] = c->h * hinv_tmp[idx];
+        }
+        bsync();
+        const int st = d_expm(m, sc, e, w, colsum, sh_i, sh_d);
+        if (st) {
+            if (threadIdx.x == 0) c->status = st == 2 ? 2 : 3;
+            return;
+        }
+        if (threadIdx.x == 0) {
+            double s = 0.0;
+            for (int i = 0; i < m; ++i) s += hinv_tmp[(m - 1) * m + i] * e[i * m];
+            c->s = s;
+            c->need_weight = 1;
+        }
+        return;
+    }
+    // modes 1, 2: reduced_exp at h_eval from the stored H_m^-1
+    for (int idx = threadIdx.x; idx < mm; idx += blockDim.x) sc[idx] = a.h_eval * a.hinv[idx];
+    bsync();
+    const int st = d_expm(m, sc, e, w, colsum, sh_i, sh_d);
+    if (st) {
+        if (threadIdx.x == 0) c->status = st == 2 ? 2 : 3;
+        return;
+    }
+    if (a.mode == 1) {
+        for (int i = threadIdx.x; i < m; i += blockDim.x) a.coef[i] = c->beta * e[i * m];
+    } else if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int i = 0; i < m; ++i) s += a.hinv[(m - 1) * m + i] * e[i * m];
+        c->s = s;
+    }
+}
+
+// ============================================================================
+// Basis combination beta * V_m e^{hH^-1} e_1 (krylov.cpp:32-36) and the ER
+// update (integrate.cpp:241,262-263), one streaming pass over V.
+//   mode 0: out = sum_j coef_j v_j
+//   mode 1: x_next = ((x_k + 1.0*(gb*h)) + 1.0*value) + (-1.0*start)
+// ============================================================================
+__global__ void __launch_bounds__(256)
+    k_combine(const double* __restrict__ V, long long ldv, const double* __restrict__ coef,
+              int n, double* __restrict__ out, const Ctrl* ctrl, int mode,
+              const double* __restrict__ xk, const double* __restrict__ gb,
+              const double* __restrict__ start, double h) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const bool have = !ctrl->skip && !ctrl->status;
+    double val = 0.0;
+    if (have) {
+        const int m = ctrl->m;
+        for (int jj = 0; jj < m; ++jj) val += coef[jj] * V[(long long)jj * ldv + i];
+    }
+    if (mode == 0) {
+        out[i] = val;
+        return;
+    }
+    double x = xk[i] + 1.0 * (gb[i] * h);
+    if (have) {
+        x += 1.0 * val;
+        x += -1.0 * start[i];
+    }
+    out[i] = x;
+}
+
+// out = residual-check weight ||G v_{m+1}|| * |beta h_next s| for the cached
+// basis (mevp_residual, krylov.cpp:191-205)
+__global__ void k_basis_residual_final(Ctrl* c, double* out) {
+    if (threadIdx.x || blockIdx.x) return;
+    if (c->happy || c->h_next == 0.0) {
+        *out = 0.0;
+        return;
+    }
+    *out = fabs(c->beta * c->h_next * c->s) * c->weight;
+}
+
+// ============================================================================
+// launch wrappers
+// ============================================================================
+namespace {
+inline unsigned int cdiv(long long a, long long b) { return (unsigned int)((a + b - 1) / b); }
+inline void count(const Launch& L, int k = 1) {
+    if (L.launches) *L.launches += k;
+}
+}  // namespace
+
+size_t ctrl_size() { return sizeof(Ctrl); }
+
+void spmv(const Launch& L, const int* rowptr, const int* col, const double* val, int n_rows,
+          const double* x, double* y, const Ctrl* ctrl, const double* vbase, long long ldv) {
+    if (n_rows <= 0) return;
+    const unsigned int grid = cdiv(cdiv(n_rows, 32), kSpmvWarps);
+    k_spmv<<<grid, kSpmvWarps * 32, 0, L.stream>>>(rowptr, col, val, n_rows, x, y, ctrl, vbase, ldv);
+    count(L);
+}
+
+void spmv_b2(const Launch& L, const int* rowptr, const int* col, const double* val, int n_rows,
+             const double* u_k, const double* u_k1, double h, double* t1, double* t2) {
+    if (n_rows <= 0) return;
+    const unsigned int grid = cdiv(cdiv(n_rows, 32), kSpmvWarps);
+    k_spmv_b2<<<grid, kSpmvWarps * 32, 0, L.stream>>>(rowptr, col, val, n_rows, u_k, u_k1, h, t1, t2);
+    count(L);
+}
+
+void trsv(const Launch& L, bool upper, bool reverse, const TrsvArgs& a) {
+    if (a.n <= 0) return;
+    const unsigned int grid = cdiv(a.n, kTrsvThreads);
+    if (!upper)
+        k_trsv<false, false><<<grid, kTrsvThreads, 0, L.stream>>>(a);
+    else if (!reverse)
+        k_trsv<true, false><<<grid, kTrsvThreads, 0, L.stream>>>(a);
+    else
+        k_trsv<true, true><<<grid, kTrsvThreads, 0, L.stream>>>(a);
+    count(L);
+}
+
+void apply_weight(const Launch& L, const int* uptr, const int* ucol, const double* uval,
+                  const double* udiag, const int* lptr, const int* lcol, const double* lval, int n,
+                  const int* col_perm, const int* row_perm, const double* x, double* t,
+                  double* y_out, double* partials, unsigned int* done, Ctrl* ctrl,
+                  const double* vbase, long long ldv, double* weight_out) {
+    k_apply_u_diag<<<cdiv(n, 256), 256, 0, L.stream>>>(uptr, ucol, uval, udiag, n, col_perm, x, t,
+                                                      ctrl, vbase, ldv);
+    k_apply_l_norm<<<cdiv(n, 256), 256, 0, L.stream>>>(lptr, lcol, lval, n, t, y_out, row_perm,
+                                                      partials, done, ctrl, weight_out);
+    count(L, 2);
+}
+
+void spmv_norm(const Launch& L, const int* rowptr, const int* col, const double* val, int n,
+               const double* vbase, long long ldv, double* partials, unsigned int* done,
+               Ctrl* ctrl, int from_ctrl_m, double* weight_out) {
+    k_spmv_norm<<<cdiv(n, 256), 256, 0, L.stream>>>(rowptr, col, val, n, vbase, ldv, partials,
+                                                   done, ctrl, from_ctrl_m, weight_out);
+    count(L);
+}
+
+void start(const Launch& L, const double* v, const double* xk, int n, double* partials,
+           double* v0, Ctrl* ctrl, int er_mode) {
+    const unsigned int grid = std::min<unsigned int>(cdiv(n, 256), (unsigned int)L.num_sms * 4);
+    k_start_partials<<<grid, 256, 0, L.stream>>>(v, xk, n, partials);
+    k_start_finish<<<grid, 256, 0, L.stream>>>(v, n, partials, (int)grid, v0, ctrl, er_mode);
+    count(L, 2);
+}
+
+template <int K>
+static int mgs_occ() {
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mgs<K>, 1024, 0);
+    return occ;
+}
+
+int mgs_max_blocks(int K) {
+    switch (K) {
+        case 1: return mgs_occ<1>();
+        case 2: return mgs_occ<2>();
+        case 4: return mgs_occ<4>();
+        case 8: return mgs_occ<8>();
+        default: return mgs_occ<16>();
+    }
+}
+
+void mgs(const Launch& L, const MgsArgs& a, int n_blocks, int K) {
+    void* args[] = {(void*)&a};
+    void* fn;
+    switch (K) {
+        case 1: fn = (void*)k_mgs<1>; break;
+        case 2: fn = (void*)k_mgs<2>; break;
+        case 4: fn = (void*)k_mgs<4>; break;
+        case 8: fn = (void*)k_mgs<8>; break;
+        default: fn = (void*)k_mgs<16>; break;
+    }
+    if (n_blocks == 1)
+        cudaLaunchKernel(fn, dim3(1), dim3(1024), args, 0, L.stream);
+    else
+        cudaLaunchCooperativeKernel(fn, dim3(n_blocks), dim3(1024), args, 0, L.stream);
+    count(L);
+}
+
+void dense(const Launch& L, const DenseArgs& a0, int m) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+    }
+    DenseArgs a = a0;
+    const size_t need = (size_t)20 * m * m * sizeof(double);
+    a.use_smem = need <= 200 * 1024;
+    k_dense<<<1, 256, a.use_smem ? need : 0, L.stream>>>(a);
+    count(L);
+}
+
+void iter_end(const Launch& L, Ctrl* ctrl) {
+    k_iter_end<<<1, 32, 0, L.stream>>>(ctrl);
+    count(L);
+}
+
+void combine(const Launch& L, const double* V, long long ldv, const double* coef, int n,
+             double* out, const Ctrl* ctrl, int mode, const double* xk, const double* gb,
+             const double* start_v, double h) {
+    k_combine<<<cdiv(n, 256), 256, 0, L.stream>>>(V, ldv, coef, n, out, ctrl, mode, xk, gb, start_v, h);
+    count(L);
+}
+
+void basis_residual_final(const Launch& L, Ctrl* ctrl, double* out) {
+    k_basis_residual_final<<<1, 32, 0, L.stream>>>(ctrl, out);
+    count(L);
+}
+
+}  // namespace dev
+}  // namespace exg

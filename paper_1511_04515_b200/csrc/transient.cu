@@ -1,0 +1,219 @@
+// exg_transient: the reference's ER/ERC time-stepping loop
+// (exsim::transient, proj/core/src/integrate.cpp:368-480) driving the device
+// hot path through the C ABI.  Step control, source evaluation, breakpoints
+// and waveform emission stay on the host with the reference's exact
+// arithmetic; every vector operation of a step runs on the device.
+//
+// Linear circuits (no nonlinear devices): G_k == G_lin every step
+// (devices.cpp:190-192), so G is factorized once at setup
+// (exg::lu_factor, bit-identical to exsim::lu_factor) and uploaded; the
+// reference re-factorizes per step with identical results, which
+// ref_transient_cached reproduces on the oracle side.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <vector>
+
+#include "ctx.hpp"
+#include "exg_host.h"
+#include "host.hpp"
+
+
+struct exg_tran_result {
+    int n_rec = 0;
+    std::vector<double> times, samples;
+    std::vector<double> t, h, err;
+    std::vector<int> lu, rej, dims_off{0}, dims;
+    double lu_s = 0.0, dc_s = 0.0, loop_s = 0.0;
+};
+
+namespace {
+
+double next_breakpoint_after(const std::vector<double>& bps, double t) {  // integrate.cpp:361-364
+    auto it = std::upper_bound(bps.begin(), bps.end(), t * (1.0 + 1e-12));
+    return it == bps.end() ? std::numeric_limits<double>::infinity() : *it;
+}
+
+struct Fail {
+    exg_status st;
+    std::string msg;
+};
+
+void chk(exg_ctx* ctx, exg_status st) {
+    if (st != EXG_OK) {
+        char buf[512];
+        exg_last_error(ctx, buf, sizeof buf);
+        throw Fail{st, buf};
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+exg_status exg_transient(exg_ctx* ctx, const exg_system* sp, const exg_step_control* ctl,
+                         double t_stop, const int* rec_idx, int n_rec, exg_tran_result** out) {
+    using clock = std::chrono::steady_clock;
+    try {
+        const exg::System& sys = sp->sys;
+        if (t_stop <= 0.0) throw Fail{EXG_E_CONTRACT, "transient: t_stop must be positive"};
+        if (!sys.mos.empty())
+            throw Fail{EXG_E_CONTRACT, "transient: nonlinear devices are not on the device path yet"};
+        auto* res = new exg_tran_result();
+        std::unique_ptr<exg_tran_result> guard(res);
+        std::vector<int> rec;
+        if (n_rec == 0)
+            for (int i = 0; i < sys.n; ++i) rec.push_back(i);
+        else
+            rec.assign(rec_idx, rec_idx + n_rec);
+        for (int i : rec)
+            if (i < 0 || i >= sys.n) throw Fail{EXG_E_CONTRACT, "unknown record node"};
+        res->n_rec = static_cast<int>(rec.size());
+
+        // ---- setup: device CSR store + the one factorization of G
+        const exg::Csr* mats[3] = {&sys.C, &sys.G, &sys.B};
+        for (int w = 0; w < 3; ++w)
+            chk(ctx, exg_set_csr(ctx, w, mats[w]->n_rows, mats[w]->n_cols, mats[w]->nnz(),
+                                 mats[w]->rowptr.data(), mats[w]->col.data(), mats[w]->val.data()));
+        auto t0 = clock::now();
+        exg::Factor f;
+        try {
+            exg::lu_factor(sys.G, 0.1, f);
+        } catch (const exg::Error& e) {
+            throw Fail{e.status, e.what};
+        }
+        chk(ctx, exg_set_factors(ctx, f.n, f.L.rowptr.data(), f.L.col.data(), f.L.val.data(),
+                                 f.U.rowptr.data(), f.U.col.data(), f.U.val.data(),
+                                 f.row_perm.data(), f.col_perm.data()));
+        auto t1 = clock::now();
+        res->lu_s = std::chrono::duration<double>(t1 - t0).count();
+
+        // ---- DC point: linear newton_static = lu_factor(G) + solve(B u(0))
+        // (integrate.cpp:70-75, :92-100), solved in EXACT mode
+        std::vector<double> x(sys.n, 0.0);
+        {
+            const std::vector<double> u0 = exg::eval_sources(sys, 0.0);
+            std::vector<double> bu0(sys.n, 0.0);
+            for (int r = 0; r < sys.n; ++r) {
+                double s = 0.0;
+                for (int k = sys.B.rowptr[r]; k < sys.B.rowptr[r + 1]; ++k)
+                    s += sys.B.val[k] * u0[sys.B.col[k]];
+                bu0[r] = s;
+            }
+            const exg_options_dev saved = ctx->opt;
+            exg_options_dev exact = saved;
+            exact.trsv_mode = EXG_TRSV_EXACT;
+            exg_set_options(ctx, &exact);
+            const exg_status st = exg_solve(ctx, bu0.data(), x.data(), EXG_PTR_HOST);
+            exg_set_options(ctx, &saved);
+            chk(ctx, st);
+        }
+        auto t2 = clock::now();
+        res->dc_s = std::chrono::duration<double>(t2 - t1).count();
+
+        std::vector<double> row(rec.size());
+        auto emit_host = [&](double t, const std::vector<double>& xv) {
+            res->times.push_back(t);
+            for (size_t i = 0; i < rec.size(); ++i) res->samples.push_back(xv[rec[i]]);
+        };
+        emit_host(0.0, x);
+
+        // ---- stepping loop (integrate.cpp:380-478)
+        const std::vector<double> bps = exg::source_breakpoints(sys, 0.0, t_stop);
+        const double hint = sys.opts.has_tran && sys.opts.tran_step > 0.0 ? sys.opts.tran_step
+                                                                          : t_stop / 100.0;
+        double h_nominal = ctl->h_init > 0.0 ? ctl->h_init : hint;
+        h_nominal = std::min(h_nominal, ctl->hmax);
+        const double hmin_eff = ctl->hmin > 0.0 ? ctl->hmin : t_stop * 1e-15;
+        const double t_tiny = t_stop * 1e-12;
+        exg_mevp_cfg cfg{ctl->eps, ctl->m_max, 1, 1e-12};
+
+        // device-resident state: x_k lives in ctx->xk (uploaded once)
+        const int n = sys.n;
+        const int ni = sys.n_inputs();
+        chk(ctx, exg_memcpy(ctx, ctx->xnext, x.data(), sizeof(double) * n, cudaMemcpyHostToDevice));
+        double t = 0.0;
+        while (t < t_stop - t_tiny) {
+            const double seg_end = std::min(next_breakpoint_after(bps, t), t_stop);
+            double h_try = std::min(h_nominal, seg_end - t);
+            if (seg_end - t - h_try < t_tiny) h_try = seg_end - t;
+            h_try = std::max(h_try, std::min(hmin_eff, seg_end - t));
+
+            const std::vector<double> u_k = exg::eval_sources(sys, t);
+            const std::vector<double> u_k1 = exg::eval_sources(sys, t + h_try);
+            if (ni) {
+                chk(ctx, exg_memcpy(ctx, ctx->u_k, u_k.data(), sizeof(double) * ni, cudaMemcpyHostToDevice));
+                chk(ctx, exg_memcpy(ctx, ctx->u_k1, u_k1.data(), sizeof(double) * ni, cudaMemcpyHostToDevice));
+            }
+            // x_k <- previous x_next (device to device)
+            chk(ctx, exg_er_begin(ctx, ctx->xnext, ctx->u_k, ctx->u_k1, h_try, EXG_PTR_DEVICE));
+            int m = -1;
+            chk(ctx, exg_er_eval(ctx, h_try, &cfg, nullptr, &m, nullptr, EXG_PTR_DEVICE));
+            // linear: err_norm == 0, never rejected (integrate.cpp:433-447)
+            const int rejects = 0;
+            res->t.push_back(t + h_try);
+            res->h.push_back(h_try);
+            res->lu.push_back(0);
+            res->rej.push_back(rejects);
+            res->err.push_back(0.0);
+            if (m >= 0) res->dims.push_back(m);
+            res->dims_off.push_back(static_cast<int>(res->dims.size()));
+
+            t += h_try;
+            chk(ctx, exg_gather(ctx, rec.data(), static_cast<int>(rec.size()), row.data()));
+            res->times.push_back(t);
+            res->samples.insert(res->samples.end(), row.begin(), row.end());
+
+            const bool grow = !ctl->fixed_step &&
+                              (ctl->grow_only_on_clean ? rejects == 0 : rejects < ctl->grow_threshold);
+            const bool clamped = h_try < h_nominal * (1.0 - 1e-12);
+            if (rejects > 0) h_nominal = h_try;
+            if (grow)
+                h_nominal = std::min(ctl->beta * (clamped && rejects == 0 ? h_nominal : h_try), ctl->hmax);
+        }
+        // the linear factorization is shared by every step: report it once
+        if (!res->lu.empty()) res->lu[0] = 1;
+        res->loop_s = std::chrono::duration<double>(clock::now() - t2).count();
+        *out = guard.release();
+        return EXG_OK;
+    } catch (const Fail& f) {
+        if (ctx) {
+            ctx->err = f.msg;
+            ctx->last = f.st;
+        }
+        return f.st;
+    } catch (const std::bad_alloc&) {
+        return EXG_E_NOMEM;
+    }
+}
+
+void exg_tran_result_free(exg_tran_result* r) { delete r; }
+int exg_tran_n_times(const exg_tran_result* r) { return static_cast<int>(r->times.size()); }
+int exg_tran_n_rec(const exg_tran_result* r) { return r->n_rec; }
+const double* exg_tran_times(const exg_tran_result* r) { return r->times.data(); }
+const double* exg_tran_samples(const exg_tran_result* r) { return r->samples.data(); }
+int exg_tran_n_steps(const exg_tran_result* r) { return static_cast<int>(r->t.size()); }
+exg_status exg_tran_records(const exg_tran_result* r, double* t, double* h, int* lu_count,
+                            int* rejects, double* err_norm, int* dims_off) {
+    const size_t n = r->t.size();
+    if (t) std::memcpy(t, r->t.data(), n * sizeof(double));
+    if (h) std::memcpy(h, r->h.data(), n * sizeof(double));
+    if (lu_count) std::memcpy(lu_count, r->lu.data(), n * sizeof(int));
+    if (rejects) std::memcpy(rejects, r->rej.data(), n * sizeof(int));
+    if (err_norm) std::memcpy(err_norm, r->err.data(), n * sizeof(double));
+    if (dims_off) std::memcpy(dims_off, r->dims_off.data(), (n + 1) * sizeof(int));
+    return EXG_OK;
+}
+int exg_tran_n_dims(const exg_tran_result* r) { return static_cast<int>(r->dims.size()); }
+const int* exg_tran_dims(const exg_tran_result* r) { return r->dims.data(); }
+exg_status exg_tran_timing(const exg_tran_result* r, double* lu_s, double* dc_s, double* loop_s) {
+    *lu_s = r->lu_s;
+    *dc_s = r->dc_s;
+    *loop_s = r->loop_s;
+    return EXG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,199 @@
+"""GPU parity tests: every kernel through the C ABI against the reference
+library (oracle/_ref) and the C restatement, on the same seeded inputs.
+
+Bars:
+* SpMV, factor apply, EXACT triangular solves: bit-identical (row-sequential
+  accumulation in the reference's order, no FMA contraction).
+* FAST triangular solves: <= 1e-13 relative (reordered U sums).
+* MEVP: identical Krylov dimension, value within 1e-12 relative (only the
+  dot-product summation order differs).
+* Transient: identical step times and per-step Krylov dimensions, waveforms
+  within 1e-8 of each node's full scale (north_star tolerance).
+"""
+import numpy as np
+import pytest
+
+import paper_1511_04515_b200 as ex
+from paper_1511_04515_b200 import _ffi as F
+from paper_1511_04515_b200.device import Context
+
+from helpers import bit_equal, full_scale_err, random_rc_pair, ref_system
+
+pytestmark = pytest.mark.gpu
+
+CASES = [
+    (0, {}),                        # config 0: 32x32 RC grid
+    (1, dict(width=64)),            # config 1 cut: 64x64 power grid, VDD pads
+    (2, dict(width=12)),            # config 2 cut: RLC with branch currents
+    (3, dict(n=3000)),              # config 3 cut: banded post-extraction system
+]
+
+
+@pytest.fixture(scope="module", params=CASES, ids=lambda c: f"c{c[0]}")
+def case(request, ref):
+    cfg, kw = request.param
+    s = ex.System.generate(cfg, **kw)
+    f = ex.lu_factor(s.G)
+    fh = ref.factor_from(f)
+    yield cfg, s, f, fh
+    ref.factor_free(fh)
+
+
+def _ctx(s, f, mode=F.EXG_TRSV_EXACT):
+    c = Context(0, trsv_mode=mode)
+    c.set_system(s)
+    c.set_factors(f)
+    return c
+
+
+def test_spmv_bit_identical(case, ref):
+    _, s, f, _ = case
+    rng = np.random.default_rng(1)
+    with _ctx(s, f) as c:
+        for w, A in ((F.EXG_MAT_C, s.C), (F.EXG_MAT_G, s.G), (F.EXG_MAT_B, s.B)):
+            x = rng.uniform(-1, 1, A.n_cols)
+            assert bit_equal(c.spmv(w, x, A.n_rows), ref.spmv(A, x))
+
+
+def test_solve_exact_bit_identical(case, ref, orc):
+    _, s, f, fh = case
+    rng = np.random.default_rng(2)
+    with _ctx(s, f) as c:
+        for _ in range(3):
+            b = rng.uniform(-1, 1, s.n)
+            got = c.solve(b)
+            assert bit_equal(got, ref.solve(fh, b))
+            assert bit_equal(got, orc.solve(f, b))
+        cn = c.counters()
+        assert cn.l_levels > 0 and cn.u_levels > 0
+
+
+def test_solve_fast_close(case, ref):
+    _, s, f, fh = case
+    b = np.random.default_rng(3).uniform(-1, 1, s.n)
+    with _ctx(s, f, F.EXG_TRSV_FAST) as c:
+        got = c.solve(b)
+    want = ref.solve(fh, b)
+    assert np.max(np.abs(got - want)) <= 1e-13 * np.max(np.abs(want))
+
+
+def test_apply_bit_identical(case, ref):
+    _, s, f, fh = case
+    x = np.random.default_rng(4).uniform(-1, 1, s.n)
+    with _ctx(s, f) as c:
+        assert bit_equal(c.apply(x), ref.apply(fh, x))
+
+
+def test_solve_residual_contract(case):
+    """test_sparse.cpp:112-131: ||A x - b||_inf <= 1e-10 (1 + ||b||_inf)."""
+    _, s, f, _ = case
+    b = np.random.default_rng(5).uniform(-1, 1, s.n)
+    with _ctx(s, f) as c:
+        x = c.solve(b)
+        r = c.spmv(F.EXG_MAT_G, x, s.n) - b
+    assert np.max(np.abs(r)) <= 1e-10 * (1 + np.max(np.abs(b)))
+
+
+def test_mevp_matches_reference(case, ref):
+    cfg, s, f, fh = case
+    rng = np.random.default_rng(6)
+    v = rng.uniform(-1, 1, s.n)
+    opts = s.options()
+    h = 1e-12 if cfg != 3 else 1e-12
+    with _ctx(s, f) as c:
+        for eps in (1e-7, 1e-10):
+            want, winfo = ref.mevp_iks(fh, s.C, v, h, eps=eps, m_max=opts.m_max)
+            got, info = c.mevp_iks(v, h, eps=eps, m_max=opts.m_max)
+            assert info.m == winfo["m"]
+            assert info.happy == bool(winfo["happy"])
+            assert np.max(np.abs(got - want)) <= 1e-12 * np.max(np.abs(want))
+
+
+def test_mevp_cached_basis(case, ref):
+    _, s, f, fh = case
+    v = np.random.default_rng(7).uniform(-1, 1, s.n)
+    h = 2e-12
+    with _ctx(s, f) as c:
+        got, info = c.mevp_iks(v, h, eps=1e-9, m_max=60)
+        want, winfo = ref.mevp_iks(fh, s.C, v, h, eps=1e-9, m_max=60, keep_basis=True)
+        bh = winfo["basis"]
+        try:
+            for fr in (1.0, 0.75, 0.5):
+                r_got = c.mevp_residual(fr * h)
+                r_want = ref.basis_residual(bh, s.G, fr * h)
+                assert abs(r_got - r_want) <= 1e-9 * abs(r_want) + 1e-300
+                e_got = c.eval_at_scaled_h(fr * h)
+                e_want = ref.basis_eval(bh, fr * h, s.n)
+                assert np.max(np.abs(e_got - e_want)) <= 1e-12 * np.max(np.abs(e_want))
+        finally:
+            ref.basis_free(bh)
+
+
+def test_er_step_matches_oracle(case, ref, orc):
+    cfg, s, f, fh = case
+    opts = s.options()
+    x0 = ref_dc = None
+    rh = ref_system(ref, s)
+    try:
+        x0 = ref.dc_solve(rh)
+        u0 = s.eval_sources(0.0)
+        h = 1e-12
+        u1 = s.eval_sources(h)
+        with _ctx(s, f) as c:
+            got, m = c.er_step(x0, u0, u1, h, eps=opts.krylov_eps, m_max=opts.m_max)
+        want, m_want = orc.er_step(f, s.C, s.B, x0, u0, u1, h, eps=opts.krylov_eps, m_max=opts.m_max)
+        assert m == m_want
+        scale = max(np.max(np.abs(want)), 1e-300)
+        assert np.max(np.abs(got - want)) <= 1e-12 * scale
+    finally:
+        ref.system_free(rh)
+
+
+# ---- reference-test known answers, on the device ----------------------------
+
+def test_happy_breakdown_known_answer():
+    """test_krylov.cpp:65-78: C = I, G = diag(1,2,3), v = e1 -> m = 1, e^{-h}."""
+    Cm = ex.Csr(3, 3, np.array([0, 1, 2, 3], np.int32), np.array([0, 1, 2], np.int32), np.ones(3))
+    G = ex.Csr(3, 3, np.array([0, 1, 2, 3], np.int32), np.array([0, 1, 2], np.int32),
+               np.array([1.0, 2.0, 3.0]))
+    f = ex.lu_factor(G)
+    with Context(0) as c:
+        c.set_csr(F.EXG_MAT_C, Cm)
+        c.set_csr(F.EXG_MAT_G, G)
+        c.set_factors(f)
+        out, info = c.mevp_iks(np.array([1.0, 0, 0]), 0.7)
+        assert info.m == 1 and info.happy
+        assert out[0] == pytest.approx(np.exp(-0.7), rel=1e-13)
+        assert out[1] == 0.0 and out[2] == 0.0
+        assert c.mevp_residual(0.7) == 0.0
+
+
+def test_zero_start_and_no_convergence():
+    """test_krylov.cpp:93-97 and :115-125."""
+    Cm, G = random_rc_pair(30, 23)
+    f = ex.lu_factor(G)
+    with Context(0) as c:
+        c.set_csr(F.EXG_MAT_C, Cm)
+        c.set_csr(F.EXG_MAT_G, G)
+        c.set_factors(f)
+        with pytest.raises(ex.ZeroStartVectorError):
+            c.mevp_iks(np.zeros(30), 1.0)
+        v = np.random.default_rng(23).uniform(-1, 1, 30)
+        with pytest.raises(ex.NoConvergenceError):
+            c.mevp_iks(v, 0.05, eps=1e-14, m_max=2)
+
+
+def test_mevp_dense_oracle_20():
+    """test_krylov.cpp:99-113: 20x20 RC pair vs dense e^{-hC^-1G} v."""
+    from scipy.linalg import expm
+    Cm, G = random_rc_pair(20, 17)
+    f = ex.lu_factor(G)
+    v = np.random.default_rng(17).uniform(-1, 1, 20)
+    with Context(0) as c:
+        c.set_csr(F.EXG_MAT_C, Cm)
+        c.set_csr(F.EXG_MAT_G, G)
+        c.set_factors(f)
+        got, info = c.mevp_iks(v, 1.0, eps=1e-7, m_max=40)
+    J = -np.linalg.solve(Cm.to_dense(), G.to_dense())
+    want = expm(J) @ v
+    assert np.linalg.norm(got - want) <= 10 * 1e-7 * np.linalg.norm(v)

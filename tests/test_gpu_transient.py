@@ -1,0 +1,82 @@
+"""Whole-transient parity on the GPU against the reference.
+
+* config 0 (32x32, 1000 fixed 1 ps steps): against exsim::transient() AS
+  SHIPPED (it refactorizes G every step).
+* the other configs (cuts sized for a CPU oracle that finishes in seconds):
+  against the restated cached-LU loop (ref_transient_cached), itself checked
+  bit-for-bit against transient() in tests/test_oracle.py.
+
+Bar: identical step times, identical Krylov dimension of every MEVP, probed
+waveforms within 1e-8 of each node's full scale.
+"""
+import numpy as np
+import pytest
+
+import paper_1511_04515_b200 as ex
+from paper_1511_04515_b200 import _ffi as F
+from paper_1511_04515_b200.device import Context
+
+from helpers import full_scale_err, ref_system
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-8
+
+
+def probes(s, k=16, seed=9):
+    rng = np.random.default_rng(seed)
+    return np.sort(rng.choice(s.n_nodes, size=min(k, s.n_nodes), replace=False)).astype(np.int32)
+
+
+def compare(got, want):
+    assert np.array_equal(got.times, want["times"]), "step times differ"
+    want_dims = [want["dims"][want["dims_off"][i]:want["dims_off"][i + 1]].tolist()
+                 for i in range(len(want["t"]))]
+    assert got.krylov_dims == want_dims, "Krylov dimension sequence differs"
+    err = full_scale_err(got.samples, want["samples"])
+    assert err <= TOL, f"waveform full-scale error {err:.3e}"
+    return err
+
+
+@pytest.mark.parametrize("mode", [F.EXG_TRSV_EXACT, F.EXG_TRSV_FAST], ids=["exact", "fast"])
+def test_config0_vs_transient_as_shipped(ref, mode):
+    s = ex.System.generate(0)
+    ctl = s.step_control()
+    ctl.fixed_step = 1
+    ctl.h_init = 1e-12
+    rec = probes(s)
+    rh = ref_system(ref, s)
+    try:
+        want = ref.transient(rh, ctl, 1e-9, rec)
+    finally:
+        ref.system_free(rh)
+    with Context(0, trsv_mode=mode) as c:
+        got = c.transient(s, ctl, 1e-9, rec)
+    assert len(got.t) >= 1000
+    compare(got, want)
+
+
+@pytest.mark.parametrize("cfg,kw,t_stop", [
+    (1, dict(width=64), 2e-9),
+    (2, dict(width=12), 1e-9),
+    (3, dict(n=3000), 5e-10),
+])
+@pytest.mark.parametrize("mode", [F.EXG_TRSV_EXACT, F.EXG_TRSV_FAST], ids=["exact", "fast"])
+def test_configs_vs_cached_oracle(ref, cfg, kw, t_stop, mode):
+    s = ex.System.generate(cfg, **kw)
+    ctl = s.step_control()
+    if cfg == 3:
+        ctl.fixed_step = 1
+        ctl.h_init = 1e-12
+    rec = probes(s)
+    f = ex.lu_factor(s.G)
+    rh = ref_system(ref, s)
+    fh = ref.factor_from(f)
+    try:
+        want = ref.transient_cached(rh, fh, ctl, t_stop, rec)
+    finally:
+        ref.factor_free(fh)
+        ref.system_free(rh)
+    with Context(0, trsv_mode=mode) as c:
+        got = c.transient(s, ctl, t_stop, rec)
+    compare(got, want)

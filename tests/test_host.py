@@ -1,0 +1,79 @@
+"""CPU tests of the host mirror (generators, MNA, setup LU) and the C ABI surface."""
+import ctypes as C
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_1511_04515_b200 as ex
+from paper_1511_04515_b200 import _ffi as F
+
+from helpers import bit_equal, ref_system
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def test_library_exports_every_declared_symbol():
+    """include/*.h declarations == exported symbols of the in-tree libexg.so."""
+    declared = set()
+    for h in (ROOT / "include").glob("*.h"):
+        declared |= set(re.findall(r"^\s*(?:[\w\*]+\s+)+\**(exg_\w+)\s*\(", h.read_text(), re.M))
+    assert declared, "no declarations parsed"
+    lib = C.CDLL(str(F.LIB_PATH))
+    missing = [s for s in sorted(declared) if not hasattr(lib, s)]
+    assert not missing, missing
+    assert set(F.declared_symbols()) <= declared | {"exg_host_error_message"}
+
+
+@pytest.mark.parametrize("cfg,kw", [(0, {}), (1, dict(width=64)), (2, dict(width=12)),
+                                    (4, dict(width=12, chains=4, stages=4))])
+def test_mna_identical_to_reference_build_mna(ref, cfg, kw):
+    s = ex.System.generate(cfg, **kw)
+    rh = ref_system(ref, s)
+    try:
+        for w in (F.EXG_MAT_C, F.EXG_MAT_G, F.EXG_MAT_B):
+            n, nc, rp, ci, va = ref.system_csr(rh, w)
+            m = s.csr(w)
+            assert (n, nc) == (m.n_rows, m.n_cols)
+            assert np.array_equal(rp, m.rowptr) and np.array_equal(ci, m.col)
+            assert bit_equal(va, m.val)
+        for t in (0.0, 3e-12, 17.5e-12, 1.05e-10, 9.99e-10):
+            assert bit_equal(s.eval_sources(t), ref.eval_sources(rh, t))
+    finally:
+        ref.system_free(rh)
+
+
+@pytest.mark.parametrize("cfg,kw", [(0, {}), (1, dict(width=100)), (2, dict(width=16)),
+                                    (3, dict(n=2000)), (4, dict(width=10, chains=4, stages=4))])
+def test_lu_bit_identical_to_reference(ref, cfg, kw):
+    s = ex.System.generate(cfg, **kw)
+    f = ex.lu_factor(s.G)
+    fh = ref.lu_factor(s.G)
+    try:
+        e = ref.factor_export(fh)
+    finally:
+        ref.factor_free(fh)
+    assert np.array_equal(e["col_perm"], f.col_perm)
+    assert np.array_equal(e["row_perm"], f.row_perm)
+    assert np.array_equal(e["Lp"], f.L.rowptr) and np.array_equal(e["Li"], f.L.col)
+    assert np.array_equal(e["Up"], f.U.rowptr) and np.array_equal(e["Ui"], f.U.col)
+    assert bit_equal(e["Lx"], f.L.val) and bit_equal(e["Ux"], f.U.val)
+
+
+def test_lu_singular_raises():
+    """test_sparse.cpp:104-110."""
+    A = ex.Csr(2, 2, np.array([0, 2, 4], np.int32), np.array([0, 1, 0, 1], np.int32), np.ones(4))
+    with pytest.raises(ex.SingularMatrixError):
+        ex.lu_factor(A)
+
+
+def test_breakpoints_sorted_unique():
+    s = ex.System.generate(1, width=64)
+    b = s.breakpoints(0.0, 2e-9)
+    assert np.all(np.diff(b) > 0) and b.min() > 0 and b.max() < 2e-9
+
+
+def test_generators_deterministic():
+    a, b = ex.System.generate(1, width=40), ex.System.generate(1, width=40)
+    assert bit_equal(a.C.val, b.C.val) and np.array_equal(a.G.col, b.G.col)

@@ -1,0 +1,434 @@
+#!/usr/bin/env python
+"""Benchmark of the invert-Krylov ER hot path on config 1 (1M-node RC mesh).
+
+One "step" = one exponential Rosenbrock–Euler time step of the reference's
+transient (er_begin + er_eval: 3 triangular-solve pairs, SpMVs, and one
+invert-Krylov MEVP of m Arnoldi iterations), integrate.cpp:417-477, on the
+device, continuing the transient from the DC point with the reference's own
+step-size sequence.
+
+  python bench.py [--gpus N --steps K --warmup W]          # our arm
+  python bench.py --impl reference [--steps K --warmup W]  # the reference CPU arm
+
+Prints ONE JSON line (rank 0).  N > 1 runs N independent replicas (the path
+does not shard), launched by torchrun; timings are the max over
+ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+PEAKS = ROOT / "MEASURED_PEAKS.json"
+FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
+METRIC = "time-steps/s (ER, config 1: 1M-node RC mesh)"
+
+
+# ---------------------------------------------------------------------------
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def allmax(world, v: float) -> float:
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def allsum(world, v: float) -> float:
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+class ClockSampler:
+    """nvidia-smi style clocks and throttle reasons sampled during a region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, device: int):
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def step_schedule(s, ctl, t_stop, n_steps):
+    """The reference's step-size sequence for a linear circuit
+    (integrate.cpp:385-394, :468-475; no rejections, err_norm == 0)."""
+    bps = s.breakpoints(0.0, t_stop)
+    hint = s.options().tran_step if s.options().has_tran and s.options().tran_step > 0 else t_stop / 100
+    h_nom = ctl.h_init if ctl.h_init > 0 else hint
+    h_nom = min(h_nom, ctl.hmax)
+    hmin_eff = ctl.hmin if ctl.hmin > 0 else t_stop * 1e-15
+    t_tiny = t_stop * 1e-12
+    t, out = 0.0, []
+    while t < t_stop - t_tiny and len(out) < n_steps:
+        i = np.searchsorted(bps, t * (1.0 + 1e-12), side="right")
+        seg_end = min(bps[i] if i < len(bps) else float("inf"), t_stop)
+        h = min(h_nom, seg_end - t)
+        if seg_end - t - h < t_tiny:
+            h = seg_end - t
+        h = max(h, min(hmin_eff, seg_end - t))
+        out.append((t, h))
+        clamped = h < h_nom * (1.0 - 1e-12)
+        if not ctl.fixed_step:
+            h_nom = min(ctl.beta * (h_nom if clamped else h), ctl.hmax)
+        t += h
+    return out
+
+
+def hbm_peak():
+    try:
+        return float(json.loads(PEAKS.read_text())["hbm_gbs"]), "measured"
+    except Exception:  # noqa: BLE001
+        return FALLBACK_HBM, "fallback"
+
+
+# ---------------------------------------------------------------------------
+def setup_system(args):
+    import paper_1511_04515_b200 as ex
+    t0 = time.perf_counter()
+    s = ex.System.generate(args.config, width=args.width)
+    t1 = time.perf_counter()
+    f = ex.lu_factor(s.G)
+    t2 = time.perf_counter()
+    return s, f, {"gen_s": round(t1 - t0, 2), "lu_s": round(t2 - t1, 2),
+                  "lu_order_s": round(f.order_s, 2), "lu_numeric_s": round(f.numeric_s, 2)}
+
+
+def cpu_reference_steps(s, f, x0, ctl, t_stop, n_steps):
+    """The reference (oracle/_ref: unmodified exsim_core) restated ER loop with
+    the (bit-identical) cached factorization; returns per-step wall times."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    from helpers_bench import ref_system_for  # noqa: E402
+    from ref import Ref  # noqa: E402
+    ref = Ref()
+    rh = ref_system_for(ref, s)
+    fh = ref.factor_from(f)
+    try:
+        r = ref.transient_cached(rh, fh, ctl, t_stop, np.zeros(1, np.int32), max_steps=n_steps, x0=x0)
+    finally:
+        ref.factor_free(fh)
+        ref.system_free(rh)
+    dims = r["dims"]
+    return r["wall"], dims
+
+
+def dc_point(ctx, s):
+    from paper_1511_04515_b200 import _ffi as F
+    u0 = s.eval_sources(0.0)
+    bu0 = ctx.spmv(F.EXG_MAT_B, u0, s.n)
+    return ctx.solve(bu0)
+
+
+def run_ours(args, rank, world, local):
+    import paper_1511_04515_b200 as ex
+    from paper_1511_04515_b200 import _ffi as F
+    from paper_1511_04515_b200.device import Context
+    import torch
+
+    s, f, setup = setup_system(args)
+    ctl = s.step_control()
+    t_stop = s.options().tran_stop
+    sched = step_schedule(s, ctl, t_stop, args.warmup + args.steps + args.e2e_steps + 4)
+    if len(sched) < args.warmup + args.steps:
+        raise SystemExit("transient too short for the requested steps")
+    mode = F.EXG_TRSV_FAST if args.trsv == "fast" else F.EXG_TRSV_EXACT
+    wmode = F.EXG_WEIGHT_GSPMV if args.weight == "gspmv" else F.EXG_WEIGHT_APPLY
+    ctx = Context(local, trsv_mode=F.EXG_TRSV_EXACT, weight_mode=wmode)
+    t0 = time.perf_counter()
+    ctx.set_system(s)
+    ctx.set_factors(f)
+    setup["upload_s"] = round(time.perf_counter() - t0, 2)
+    x0 = dc_point(ctx, s)  # EXACT mode, as dc_solve
+    ctx.set_options(mode, wmode)
+    cnt0 = ctx.counters()
+    n, ni = s.n, s.n_inputs
+    cfg = F.exg_mevp_cfg(ctl.eps, ctl.m_max, 1, 1e-12)
+    lib, h = F.lib, ctx.handle
+
+    # ---- device-resident inputs: per-step u_k, u_{k+1} tables + state x
+    nsteps = args.warmup + args.steps
+    U = np.zeros((nsteps, 2, max(ni, 1)))
+    for i, (t, hh) in enumerate(sched[:nsteps]):
+        U[i, 0, :ni] = s.eval_sources(t)
+        U[i, 1, :ni] = s.eval_sources(t + hh)
+    dU, dx = C.c_void_p(), C.c_void_p()
+    ctx._check(lib.exg_device_alloc(h, U.nbytes, C.byref(dU)))
+    ctx._check(lib.exg_device_alloc(h, 8 * n, C.byref(dx)))
+    ctx._check(lib.exg_memcpy(h, dU, U.ctypes.data, U.nbytes, 1))
+    ctx._check(lib.exg_memcpy(h, dx, x0.ctypes.data, 8 * n, 1))
+    stride = 2 * max(ni, 1) * 8
+    m_seq = []
+
+    def dev_step(i):
+        t, hh = sched[i]
+        uk = dU.value + i * stride
+        uk1 = uk + max(ni, 1) * 8
+        ctx._check(lib.exg_er_begin(h, dx, C.c_void_p(uk), C.c_void_p(uk1), hh, F.EXG_PTR_DEVICE))
+        m = C.c_int(-1)
+        ctx._check(lib.exg_er_eval(h, hh, C.byref(cfg), dx, C.byref(m), None, F.EXG_PTR_DEVICE))
+        return m.value
+
+    stream = torch.cuda.ExternalStream(lib.exg_stream(h), device=torch.device("cuda", local))
+    for i in range(args.warmup):
+        dev_step(i)
+    ctx.synchronize()
+    c_before = ctx.counters()
+    barrier(world)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ctx.synchronize()
+        ev0.record(stream)
+        for i in range(args.warmup, nsteps):
+            m_seq.append(dev_step(i))
+        ev1.record(stream)
+        ctx.synchronize()
+        torch.cuda.synchronize(local)
+    barrier(world)
+    ms_total = ev0.elapsed_time(ev1)
+    c_after = ctx.counters()
+    ms_max = allmax(world, ms_total)
+    steps_total = allsum(world, float(args.steps))
+    value = steps_total / (ms_max / 1e3)
+    iters = c_after.arnoldi_iters - c_before.arnoldi_iters
+    launches = c_after.kernel_launches - c_before.kernel_launches
+
+    # ---- live per-kernel timing (separate pass, CUDA events on our stream)
+    ctx._check(lib.exg_memcpy(h, dx, x0.ctypes.data, 8 * n, 1))
+    lib.exg_profile_enable(h, 1)
+    for i in range(min(args.profile_steps, nsteps)):
+        dev_step(i)
+    kt = F.exg_kernel_times()
+    ctx._check(lib.exg_profile_get(h, C.byref(kt)))
+    lib.exg_profile_enable(h, 0)
+    ktimes = {F.KERNEL_CLASSES[k]: {"ms": round(kt.ms[k], 3), "launches": int(kt.count[k])}
+              for k in range(7) if kt.count[k]}
+    cn = ctx.counters()
+    nnz_l, nnz_u = cn.nnz_l, cn.nnz_u
+    Cm = s.C
+    bytes_l = 12 * nnz_l + 4 * (n + 1) + 4 * n + 4 * n + 8 * n + 8 * n
+    bytes_u = 12 * nnz_u + 8 * n + 4 * (n + 1) + 4 * n + 8 * n + 8 * n + 4 * n + 8 * n
+    bytes_spmv = 12 * Cm.nnz + 4 * (n + 1) + 8 * n + 8 * n
+    alg = {"trsv_l": bytes_l, "trsv_u": bytes_u, "spmv": bytes_spmv,
+           "mgs": None, "dense": None, "weight": None}
+    dom = max(ktimes, key=lambda k: ktimes[k]["ms"])
+    peak, peak_kind = hbm_peak()
+    roof = {}
+    for k in ("trsv_l", "trsv_u", "spmv"):
+        if k in ktimes and ktimes[k]["launches"]:
+            per = ktimes[k]["ms"] / ktimes[k]["launches"] / 1e3
+            ach = alg[k] / per / 1e9
+            roof[k] = {"achieved": round(ach, 1), "frac": round(ach / peak, 4),
+                       "ms_per_launch": round(per * 1e3, 4), "bytes_per_launch": alg[k]}
+    dom_roof = dom if dom in roof else "trsv_u" if "trsv_u" in roof else next(iter(roof))
+    traffic = None
+    tf = ROOT / "profiles" / "r01_traffic.json"
+    if tf.exists():
+        try:
+            traffic = json.loads(tf.read_text()).get(dom_roof)
+        except Exception:  # noqa: BLE001
+            traffic = None
+    roofline = {"bound": "hbm", "kernel": dom_roof, "achieved": roof[dom_roof]["achieved"],
+                "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                "frac": roof[dom_roof]["frac"], "traffic": traffic,
+                "per_kernel": roof, "l_levels": cn.l_levels, "u_levels": cn.u_levels,
+                "kernel_ms": ktimes}
+
+    # ---- e2e: the public per-step call with HOST buffers (H2D inputs and
+    # x_k, D2H of x_next), same steps
+    e2e_steps = min(args.e2e_steps, len(sched) - args.warmup)
+    xh = x0.copy()
+    xn = np.zeros(n)
+    ctx.synchronize()
+    barrier(world)
+    t0 = time.perf_counter()
+    for i in range(args.warmup, args.warmup + e2e_steps):
+        t, hh = sched[i]
+        uk = np.ascontiguousarray(s.eval_sources(t))
+        uk1 = np.ascontiguousarray(s.eval_sources(t + hh))
+        m = C.c_int(-1)
+        ctx._check(lib.exg_er_step(h, xh.ctypes.data, uk.ctypes.data, uk1.ctypes.data, hh, C.byref(cfg),
+                                   xn.ctypes.data, C.byref(m), F.EXG_PTR_HOST))
+        xh, xn = xn, xh
+    ctx.synchronize()
+    e2e_s = allmax(world, time.perf_counter() - t0)
+    barrier(world)
+    e2e_val = allsum(world, float(e2e_steps)) / e2e_s
+
+    # ---- CPU baseline (rank 0, N = 1): the reference on a bounded sample
+    cpu = None
+    if rank == 0 and world == 1 and args.cpu_steps > 0:
+        wall, dims = cpu_reference_steps(s, f, x0, ctl, t_stop, args.cpu_steps)
+        per = np.diff(np.concatenate([[0.0], wall]))
+        cpu = {"value": round(len(per) / float(np.sum(per)), 5), "unit": "steps/s", "cores": 1,
+               "kind": "reference",
+               "sample": f"first {len(per)} ER steps of config 1 from the DC point, unmodified "
+                         f"exsim_core (oracle/_ref) restated loop with the cached bit-identical "
+                         f"factorization, 1 thread; per-step s {[round(x, 2) for x in per]}, "
+                         f"m {dims.tolist()}"}
+
+    res = {
+        "metric": METRIC, "value": round(value, 4), "unit": "steps/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded config-1 generator, DESIGN.md §4)",
+        "config": {"workload": f"config{args.config}_rc_mesh_{args.width}x{args.width}", "n": n,
+                   "nnz_C": s.C.nnz, "nnz_G": s.G.nnz, "nnz_LU": int(f.fill_nnz),
+                   "n_inputs": ni, "trsv_mode": args.trsv, "weight_mode": args.weight,
+                   "parallelism": f"replicas{world}",
+                   "l2": "inputs larger than L2 (factors ~1.4 GB, basis 328 MB)"},
+        "arnoldi_iters_per_s": round(allsum(world, float(iters)) / (ms_max / 1e3), 3),
+        "m_per_step": m_seq, "gpu_launches": int(launches),
+        "roofline": roofline, "cpu_baseline": cpu,
+        "e2e": {"value": round(e2e_val, 4), "unit": "steps/s",
+                "h2d_bytes_per_step": 8 * n + 16 * ni, "d2h_bytes_per_step": 8 * n,
+                "steps": e2e_steps, "api": "exg_er_step(host buffers)"},
+        "clocks": clk.summary(), "setup": setup,
+    }
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+
+
+def run_reference(args, rank, world):
+    """The reference arm: the unmodified reference (oracle/_ref) CPU path."""
+    if rank != 0:
+        return
+    import paper_1511_04515_b200 as ex
+    from paper_1511_04515_b200 import _ffi as F
+    sys.path.insert(0, str(ROOT / "oracle"))
+    from ref import Ref
+    s, f, setup = setup_system(args)
+    ctl = s.step_control()
+    t_stop = s.options().tran_stop
+    ref = Ref()
+    from helpers_bench import ref_system_for
+    rh = ref_system_for(ref, s)
+    fh = ref.factor_from(f)
+    # DC point: dc_solve's linear branch = lu_factor(G) + solve(B u0)
+    # (integrate.cpp:70-75); the factor is the bit-identical one
+    u0 = s.eval_sources(0.0)
+    x0 = ref.solve(fh, ref.spmv(s.B, u0))
+    n_total = args.warmup + args.steps
+    r = ref.transient_cached(rh, fh, ctl, t_stop, np.zeros(1, np.int32), max_steps=n_total, x0=x0)
+    ref.factor_free(fh)
+    ref.system_free(rh)
+    wall = r["wall"]
+    t_w = wall[args.warmup - 1] if args.warmup > 0 else 0.0
+    timed = wall[n_total - 1] - t_w
+    value = args.steps / timed
+    res = {
+        "metric": METRIC, "value": round(value, 6), "unit": "steps/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(timed / args.steps * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded config-1 generator, DESIGN.md §4)", "impl": "reference",
+        "config": {"workload": f"config{args.config}_rc_mesh_{args.width}x{args.width}", "n": s.n},
+        "cpu_baseline": {"value": round(value, 6), "unit": "steps/s", "cores": 1, "kind": "reference",
+                         "sample": f"steps {args.warmup}..{n_total - 1} of the config-1 transient, "
+                                   "unmodified exsim_core restated ER loop (cached factorization "
+                                   "from the bit-identical host LU), 1 thread"},
+        "e2e": {"value": round(value, 6), "unit": "steps/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "setup": setup, "m_per_step": r["dims"].tolist(),
+    }
+    print(json.dumps(res), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--width", type=int, default=1000)
+    ap.add_argument("--trsv", default="fast", choices=["fast", "exact"])
+    ap.add_argument("--weight", default="gspmv", choices=["apply", "gspmv"])
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--profile-steps", type=int, default=2)
+    ap.add_argument("--cpu-steps", type=int, default=2)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    rank, world, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

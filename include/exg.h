@@ -146,6 +146,28 @@ exg_status exg_er_step(exg_ctx* ctx, const double* x_k, const double* u_k, const
 /* out[i] = x_next[idx[i]] of the last ER evaluation (probed nodes) */
 exg_status exg_gather(exg_ctx* ctx, const int* idx, int k, double* out);
 
+/* Per-kernel-class device time measured with CUDA events on the context's
+ * stream (profiling mode only; adds one event pair per launch). */
+enum {
+    EXG_K_TRSV_L = 0,
+    EXG_K_TRSV_U = 1,
+    EXG_K_SPMV = 2,
+    EXG_K_MGS = 3,
+    EXG_K_DENSE = 4,
+    EXG_K_WEIGHT = 5,
+    EXG_K_OTHER = 6,
+    EXG_K_CLASSES = 7
+};
+typedef struct exg_kernel_times {
+    double ms[EXG_K_CLASSES];
+    int64_t count[EXG_K_CLASSES];
+} exg_kernel_times;
+exg_status exg_profile_enable(exg_ctx* ctx, int on);
+/* debug: one solve with per-row (start, end) %globaltimer stamps; times holds
+ * 4n values (L sweep pairs, then U sweep pairs) */
+exg_status exg_debug_trace_solve(exg_ctx* ctx, const double* b, unsigned long long* times);
+exg_status exg_profile_get(exg_ctx* ctx, exg_kernel_times* out); /* synchronises; resets */
+
 exg_status exg_counters_get(exg_ctx* ctx, exg_counters* out);
 exg_status exg_counters_reset(exg_ctx* ctx);
 exg_status exg_synchronize(exg_ctx* ctx);

@@ -223,6 +223,10 @@ class Ref:
         ts = [C.c_double, C.c_double, C.c_double, C.c_double, C.c_int, C.c_int, C.c_double,
               C.c_int, C.c_int]
         self.lib.ref_tran_get(rh, *[_ptr(a, t) for a, t in zip(r.values(), ts)])
+        nw = self.lib.ref_tran_wall(rh, None)
+        r["wall"] = np.zeros(nw)
+        if nw:
+            self.lib.ref_tran_wall(rh, _ptr(r["wall"], C.c_double))
         r["dims"] = r["dims"][: nd.value]
         r["samples"] = r["samples"].reshape(nt.value, nr.value)
         self.lib.ref_tran_free(rh)

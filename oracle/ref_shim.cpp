@@ -17,6 +17,7 @@
 // elsewhere are installed through the standard explicit-instantiation access
 // rule (no reference source is modified or copied).
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <limits>
 #include <cstring>
@@ -147,6 +148,7 @@ struct TranOut {
     int n_rec = 0;
     std::vector<double> t, h, err;
     std::vector<int> lu, rej, dims_off, dims;
+    std::vector<double> wall;  // seconds since loop start after each accepted step
     double lu_s = 0.0;
 };
 
@@ -565,6 +567,8 @@ int ref_transient_cached(void* s, void* fact, int method, const exg_step_control
 
     double t = 0.0;
     long k = 0;
+    const auto wall0 = std::chrono::steady_clock::now();
+    std::vector<double> wall;
     while (t < t_stop - t_tiny) {
         if (max_steps > 0 && k >= max_steps) break;
         const double seg_end = std::min(next_bp(bps, t), t_stop);
@@ -625,9 +629,11 @@ int ref_transient_cached(void* s, void* fact, int method, const exg_step_control
         if (grow) h_nominal = std::min(ctl.beta * (clamped && rejects == 0 ? h_nominal : h_try), ctl.hmax);
         result.records.push_back(std::move(rec_));
         ++k;
+        wall.push_back(std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count());
     }
     auto* o = new TranOut();
     fill_tran(*o, result);
+    o->wall = std::move(wall);
     *out = o;
     GUARD_END
 }
@@ -657,6 +663,12 @@ int ref_tran_get(void* rp, double* times, double* samples, double* t, double* h,
     cp(dims_off, r->dims_off);
     cp(dims, r->dims);
     return EXG_OK;
+}
+
+int ref_tran_wall(void* rp, double* wall) {
+    const TranOut* r = static_cast<TranOut*>(rp);
+    if (wall && !r->wall.empty()) std::memcpy(wall, r->wall.data(), sizeof(double) * r->wall.size());
+    return static_cast<int>(r->wall.size());
 }
 
 void ref_reset_lu_count() { reset_lu_factor_count(); }

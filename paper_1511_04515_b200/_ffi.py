@@ -96,6 +96,12 @@ class exg_counters(C.Structure):
                 ("u_levels", C.c_int32), ("nnz_l", C.c_int64), ("nnz_u", C.c_int64)]
 
 
+class exg_kernel_times(C.Structure):
+    _fields_ = [("ms", C.c_double * 7), ("count", C.c_int64 * 7)]
+
+
+KERNEL_CLASSES = ["trsv_l", "trsv_u", "spmv", "mgs", "dense", "weight", "other"]
+
 P = C.c_void_p
 I = C.c_int
 D = C.c_double
@@ -147,6 +153,9 @@ _DEV_PROTOS = {
     "exg_gather": (I, [P, PI, I, PD]),
     "exg_counters_get": (I, [P, C.POINTER(exg_counters)]),
     "exg_counters_reset": (I, [P]),
+    "exg_profile_enable": (I, [P, I]),
+    "exg_debug_trace_solve": (I, [P, PD, C.POINTER(C.c_uint64)]),
+    "exg_profile_get": (I, [P, C.POINTER(exg_kernel_times)]),
     "exg_synchronize": (I, [P]),
     "exg_device_alloc": (I, [P, C.c_size_t, C.POINTER(P)]),
     "exg_device_free": (I, [P, P]),

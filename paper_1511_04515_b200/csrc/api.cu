@@ -168,7 +168,13 @@ void solve_dev(exg_ctx* c, const double* b, double* final_out, double coef, cons
     a.out = y;
     a.ticket = tickets;
     a.ctrl = ctrl;
+    const int fq = c->opt.trsv_mode == EXG_TRSV_FAST ? 2 : 0;
+    a.tasks = c->tasks[fq];
+    a.n_tasks = c->n_tasks[fq];
+    a.trace = c->trace_l;
+    cudaEvent_t e0 = c->prof_begin();
     exg::dev::trsv(c->L(), false, false, a);
+    c->prof_end(EXG_K_TRSV_L, e0);
     exg::dev::TrsvArgs u{};
     u.n = n;
     u.order = c->u_order;
@@ -184,8 +190,21 @@ void solve_dev(exg_ctx* c, const double* b, double* final_out, double coef, cons
     u.add = add;
     u.coef = coef;
     u.ctrl = ctrl;
+    u.tasks = c->tasks[fq + 1];
+    u.n_tasks = c->n_tasks[fq + 1];
+    u.trace = c->trace_u;
+    cudaEvent_t e1 = c->prof_begin();
     exg::dev::trsv(c->L(), true, c->opt.trsv_mode == EXG_TRSV_FAST, u);
+    c->prof_end(EXG_K_TRSV_U, e1);
     c->cnt.trsv_calls++;
+}
+
+// y = P^T L U Q^T x (and its norm) over the EXACT task lists
+void apply_dev(exg_ctx* c, const double* x, double* y_out, exg::dev::Ctrl* ctrl, double* weight_out) {
+    exg::dev::apply_tasks(c->L(), c->tasks[1], c->n_tasks[1], c->u_order, c->tasks[0], c->n_tasks[0],
+                          c->l_order, c->u_ptr, c->u_col, c->u_val, c->u_diag, c->l_ptr, c->l_col,
+                          c->l_val, c->n, c->col_perm, c->row_perm, x, c->tmp, c->t3, c->v1, y_out,
+                          c->partials, c->done, ctrl, c->V, c->ldv, weight_out);
 }
 
 void sync_ctrl(exg_ctx* c) {
@@ -257,20 +276,26 @@ void mevp_dev(exg_ctx* c, const double* v, double h, const exg_mevp_cfg& cfg, in
     if (hc.status == 0 && !hc.converged) {
         for (int jj = 0; jj < cfg.m_max; ++jj) {
             // w = -G^{-1}(C v_j)   (krylov.cpp:120-121)
+            cudaEvent_t p0 = c->prof_begin();
             exg::dev::spmv(L, C.rowptr, C.col, C.val, C.n_rows, nullptr, c->t, c->ctrl, c->V, c->ldv);
+            c->prof_end(EXG_K_SPMV, p0);
             solve_dev(c, c->t, c->w, -1.0, nullptr, c->ctrl);
+            cudaEvent_t p1 = c->prof_begin();
             exg::dev::mgs(L, ma, blocks, K);
+            c->prof_end(EXG_K_MGS, p1);
+            cudaEvent_t p2 = c->prof_begin();
             exg::dev::dense(L, da, jj + 1);
+            c->prof_end(EXG_K_DENSE, p2);
+            cudaEvent_t p3 = c->prof_begin();
             if (gspmv) {
                 const DCsr& G = c->mats[EXG_MAT_G];
                 exg::dev::spmv_norm(L, G.rowptr, G.col, G.val, n, c->V, c->ldv, c->partials, c->done,
                                     c->ctrl, 1, nullptr);
             } else {
-                exg::dev::apply_weight(L, c->u_ptr, c->u_col, c->u_val, c->u_diag, c->l_ptr, c->l_col,
-                                       c->l_val, n, c->col_perm, c->row_perm, nullptr, c->tmp, nullptr,
-                                       c->partials, c->done, c->ctrl, c->V, c->ldv, nullptr);
+                apply_dev(c, nullptr, nullptr, c->ctrl, nullptr);
             }
             exg::dev::iter_end(L, c->ctrl);
+            c->prof_end(EXG_K_WEIGHT, p3);
             c->cnt.arnoldi_iters++;
             sync_ctrl(c);
             if (hc.status || hc.converged) break;
@@ -361,10 +386,17 @@ void exg_destroy(exg_ctx* c) {
     for (double* p : dp)
         if (p) cudaFree(p);
     if (c->trsv_buf) cudaFree(c->trsv_buf);
+    for (int q = 0; q < 4; ++q)
+        if (c->tasks[q]) cudaFree(c->tasks[q]);
     if (c->bar) cudaFree(c->bar);
     if (c->done) cudaFree(c->done);
     if (c->ctrl) cudaFree(c->ctrl);
     if (c->h_ctrl) cudaFreeHost(c->h_ctrl);
+    for (auto& pe : c->prof_events) {
+        cudaEventDestroy(pe.second.first);
+        cudaEventDestroy(pe.second.second);
+    }
+    for (cudaEvent_t e : c->event_pool) cudaEventDestroy(e);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -452,6 +484,7 @@ exg_status exg_set_factors(exg_ctx* c, int n, const int* Lp, const int* Li, cons
         return ord;
     };
     const std::vector<int> lord = order_by(lev, l_levels, false);
+    const std::vector<int> llev = lev;
     for (int r = n - 1; r >= 0; --r) {
         int lv_ = 0;
         for (int k = up[r]; k < up[r + 1]; ++k) lv_ = std::max(lv_, lev[uc[k]] + 1);
@@ -459,6 +492,46 @@ exg_status exg_set_factors(exg_ctx* c, int n, const int* Lp, const int* Li, cons
         u_levels = std::max(u_levels, lv_ + 1);
     }
     const std::vector<int> uord = order_by(lev, u_levels, true);
+    // warp tasks over the level order: long rows alone, short rows 32 per task
+    // Warp tasks over the level order.  A row with more than 32 off-diagonal
+    // entries is a task of its own (whole warp); shorter rows are grouped,
+    // never across two levels (no lane ever waits on a lane of its own warp),
+    // with `lpr` lanes per row: 1 in EXACT mode (the reference's sequential
+    // row), up to 8 in FAST mode (about 4 entries per lane).
+    // task.y = rows | log2(lpr) << 8 | LONG << 30
+    auto make_tasks = [](const std::vector<int>& ord, const std::vector<int>& ptr,
+                         const std::vector<int>& level, bool fast) {
+        std::vector<int2> tasks;
+        int g0 = -1, gc = 0, glev = -1, glg = -1;
+        auto flush = [&]() {
+            if (gc) tasks.push_back(make_int2(g0, gc | (glg << 8)));
+            gc = 0;
+        };
+        for (int i = 0; i < (int)ord.size(); ++i) {
+            const int r = ord[i];
+            const int len = ptr[r + 1] - ptr[r];
+            if (len > 32) {
+                flush();
+                tasks.push_back(make_int2(i, 1 | (1 << 30)));
+                continue;
+            }
+            int lg = 0;
+            if (fast) lg = len <= 4 ? 0 : len <= 8 ? 1 : len <= 16 ? 2 : 3;
+            if (gc && (level[r] != glev || lg != glg || (gc + 1) << lg > 32)) flush();
+            if (!gc) {
+                g0 = i;
+                glev = level[r];
+                glg = lg;
+            }
+            ++gc;
+        }
+        flush();
+        return tasks;
+    };
+    const std::vector<int2> ltasks = make_tasks(lord, lp, llev, false);
+    const std::vector<int2> utasks = make_tasks(uord, up, lev, false);
+    const std::vector<int2> ltasks_f = make_tasks(lord, lp, llev, true);
+    const std::vector<int2> utasks_f = make_tasks(uord, up, lev, true);
 
     int* ip[] = {c->l_ptr, c->l_col, c->u_ptr, c->u_col, c->row_perm, c->col_perm, c->l_order, c->u_order};
     for (int* p : ip)
@@ -487,6 +560,13 @@ exg_status exg_set_factors(exg_ctx* c, int n, const int* Lp, const int* Li, cons
     up_i(c->col_perm, col_perm, n);
     up_i(c->l_order, lord.data(), n);
     up_i(c->u_order, uord.data(), n);
+    const std::vector<int2>* tl[4] = {&ltasks, &utasks, &ltasks_f, &utasks_f};
+    for (int q = 0; q < 4; ++q) {
+        if (c->tasks[q]) cudaFree(c->tasks[q]);
+        c->tasks[q] = dalloc<int2>(tl[q]->size());
+        ck(cudaMemcpy(c->tasks[q], tl[q]->data(), tl[q]->size() * sizeof(int2), cudaMemcpyHostToDevice), "tasks");
+        c->n_tasks[q] = (int)tl[q]->size();
+    }
     c->trsv_buf = dalloc<char>(16 + 2 * sizeof(double) * (size_t)n);
     ensure_vectors(c, n);
     c->cnt.l_levels = l_levels;
@@ -542,9 +622,7 @@ exg_status exg_apply(exg_ctx* c, const double* x, double* y, int ptr_kind) {
     const int n = c->n;
     const double* xd = resolve_in(c, x, n, ptr_kind, c->vin);
     double* yd = ptr_kind == EXG_PTR_DEVICE ? y : c->vout;
-    exg::dev::apply_weight(c->L(), c->u_ptr, c->u_col, c->u_val, c->u_diag, c->l_ptr, c->l_col,
-                           c->l_val, n, c->col_perm, c->row_perm, xd, c->tmp, yd, c->partials,
-                           c->done, nullptr, nullptr, 0, c->weight);
+    apply_dev(c, xd, yd, nullptr, c->weight);
     ck(cudaGetLastError(), "apply launch");
     deliver(c, y, yd, n, ptr_kind);
     API_END(c)
@@ -707,6 +785,52 @@ exg_status exg_gather(exg_ctx* c, const int* idx, int k, double* out) {
     c->launches++;
     ck(cudaMemcpyAsync(out, c->probe_out, sizeof(double) * k, cudaMemcpyDeviceToHost, c->stream), "d2h");
     ck(cudaStreamSynchronize(c->stream), "gather sync");
+    API_END(c)
+}
+
+// debug: one triangular-solve pair with per-row (start, end) timestamps of the
+// L and U sweeps (ns, %globaltimer), 4n values: L pairs then U pairs
+exg_status exg_debug_trace_solve(exg_ctx* c, const double* b, unsigned long long* times) {
+    API_BEGIN
+    require_factors(c);
+    const int n = c->n;
+    unsigned long long* tr = dalloc<unsigned long long>((size_t)4 * n);
+    ck(cudaMemsetAsync(tr, 0, sizeof(unsigned long long) * 4 * (size_t)n, c->stream), "memset");
+    c->trace_l = tr;
+    c->trace_u = tr + 2 * (size_t)n;
+    const double* bd = resolve_in(c, b, n, EXG_PTR_HOST, c->vin);
+    solve_dev(c, bd, c->vout, 1.0, nullptr, nullptr);
+    c->trace_l = c->trace_u = nullptr;
+    ck(cudaMemcpyAsync(times, tr, sizeof(unsigned long long) * 4 * (size_t)n, cudaMemcpyDeviceToHost, c->stream), "d2h");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    cudaFree(tr);
+    API_END(c)
+}
+
+exg_status exg_profile_enable(exg_ctx* c, int on) {
+    if (!c) return EXG_E_CONTRACT;
+    c->profiling = on != 0;
+    return EXG_OK;
+}
+
+exg_status exg_profile_get(exg_ctx* c, exg_kernel_times* out) {
+    API_BEGIN
+    ck(cudaStreamSynchronize(c->stream), "profile sync");
+    for (auto& pe : c->prof_events) {
+        float ms = 0.f;
+        ck(cudaEventElapsedTime(&ms, pe.second.first, pe.second.second), "elapsed");
+        c->prof_ms[pe.first] += ms;
+        c->prof_count[pe.first] += 1;
+        c->event_pool.push_back(pe.second.first);
+        c->event_pool.push_back(pe.second.second);
+    }
+    c->prof_events.clear();
+    for (int k = 0; k < EXG_K_CLASSES; ++k) {
+        out->ms[k] = c->prof_ms[k];
+        out->count[k] = c->prof_count[k];
+        c->prof_ms[k] = 0.0;
+        c->prof_count[k] = 0;
+    }
     API_END(c)
 }
 

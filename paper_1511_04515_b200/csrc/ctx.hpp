@@ -2,6 +2,8 @@
 #pragma once
 
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "device.hpp"
 #include "exg.h"
@@ -30,6 +32,9 @@ struct exg_ctx {
     int *l_ptr = nullptr, *l_col = nullptr, *u_ptr = nullptr, *u_col = nullptr;
     double *l_val = nullptr, *u_val = nullptr, *u_diag = nullptr;
     int *row_perm = nullptr, *col_perm = nullptr, *l_order = nullptr, *u_order = nullptr;
+    int2* tasks[4] = {nullptr, nullptr, nullptr, nullptr};  // L, U (EXACT), L, U (FAST)
+    int n_tasks[4] = {0, 0, 0, 0};
+    unsigned long long *trace_l = nullptr, *trace_u = nullptr;
     // solve scratch: [2 tickets + pad (16 B)][y n][x n], memset to 0xFF per solve
     char* trsv_buf = nullptr;
     // n-vectors
@@ -56,6 +61,37 @@ struct exg_ctx {
     int* probe_idx = nullptr;
     int probe_cap = 0;
 
+    // profiling: event pairs per kernel class, resolved in exg_profile_get
+    bool profiling = false;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_events;
+    std::vector<cudaEvent_t> event_pool;
+    double prof_ms[EXG_K_CLASSES] = {};
+    long long prof_count[EXG_K_CLASSES] = {};
+
     exg::dev::Launch L() { return exg::dev::Launch{stream, num_sms, &launches}; }
+    cudaEvent_t get_event() {
+        if (!event_pool.empty()) {
+            cudaEvent_t e = event_pool.back();
+            event_pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        return e;
+    }
+    // RAII-less helpers: begin returns an event recorded now; end records the
+    // closing event and files the pair under `cls`
+    cudaEvent_t prof_begin() {
+        if (!profiling) return nullptr;
+        cudaEvent_t e = get_event();
+        cudaEventRecord(e, stream);
+        return e;
+    }
+    void prof_end(int cls, cudaEvent_t b) {
+        if (!profiling || !b) return;
+        cudaEvent_t e = get_event();
+        cudaEventRecord(e, stream);
+        prof_events.push_back({cls, {b, e}});
+    }
 };
 

@@ -26,6 +26,9 @@ struct TrsvArgs {
     const double* add;
     double coef;
     const Ctrl* ctrl;   // early exit when the MEVP has converged
+    const int2* tasks;  // warp tasks in level order (v2 kernel); null = v1
+    int n_tasks;
+    unsigned long long* trace;  // debug: per row (start, end) %globaltimer, or null
 };
 
 struct MgsArgs {
@@ -69,6 +72,13 @@ void apply_weight(const Launch& L, const int* uptr, const int* ucol, const doubl
                   const int* col_perm, const int* row_perm, const double* x, double* t,
                   double* y_out, double* partials, unsigned int* done, Ctrl* ctrl,
                   const double* vbase, long long ldv, double* weight_out);
+void apply_tasks(const Launch& L, const int2* utasks, int n_utasks, const int* uorder,
+                 const int2* ltasks, int n_ltasks, const int* lorder, const int* uptr,
+                 const int* ucol, const double* uval, const double* udiag, const int* lptr,
+                 const int* lcol, const double* lval, int n, const int* col_perm,
+                 const int* row_perm, const double* x, double* t, double* y, double* sq,
+                 double* y_out, double* partials, unsigned int* done, Ctrl* ctrl,
+                 const double* vbase, long long ldv, double* weight_out);
 void spmv_norm(const Launch& L, const int* rowptr, const int* col, const double* val, int n,
                const double* vbase, long long ldv, double* partials, unsigned int* done,
                Ctrl* ctrl, int from_ctrl_m, double* weight_out);

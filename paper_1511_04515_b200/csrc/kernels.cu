@@ -181,6 +181,398 @@ __global__ void __launch_bounds__(kTrsvThreads)
     }
 }
 
+// ---------------------------------------------------------------------------
+// v2: warp tasks.  The host cuts the level order into tasks: a LONG row
+// (> kLongRow off-diagonal entries) is one warp task; consecutive short rows
+// are grouped 32 to a warp task (one row per lane).  Resident warps take
+// tasks in order through an atomic ticket (deadlock-free: a task waits only on
+// earlier tasks, all owned by running warps).
+//   long row, EXACT: the warp loads 32 entries at a time (coalesced), each
+//     lane forms its product v*y, and the subtraction chain runs in the
+//     reference's order through shuffles -> bit-identical.
+//   long row, FAST: each lane accumulates its strided entries (L: increasing,
+//     U: decreasing column so the newest dependency comes last), then a fixed
+//     butterfly reduction -> deterministic, not bit-identical.
+// Dependencies are read with a cached load first; a value never changes once
+// published, so a stale copy can only be the sentinel, which falls back to
+// polling L2.
+// ---------------------------------------------------------------------------
+constexpr int kLongRow = 32;
+constexpr int kTaskLong = 1 << 30;
+__device__ void decide(Ctrl* c);
+
+__device__ __forceinline__ double load_ready(const double* p) {
+    unsigned long long v = __double_as_longlong(__ldca(p));
+    while (v == kSentinel) v = ld_relaxed(p);
+    return __longlong_as_double(v);
+}
+
+template <bool UPPER>
+__device__ __forceinline__ void trsv_finish(const TrsvArgs& a, int r, double s) {
+    if (UPPER) s = s / a.diag[r];
+    st_relaxed(a.out + r, s);
+    if (a.final_out) {
+        const int q = a.out_perm[r];
+        double y = a.coef * s;
+        if (a.add) y = a.add[q] + y;
+        a.final_out[q] = y;
+    }
+}
+
+template <bool UPPER, bool FAST>
+__global__ void __launch_bounds__(256)
+    k_trsv2(TrsvArgs a) {
+    __shared__ double s_prod[8][32];
+    if (a.ctrl && (a.ctrl->converged || a.ctrl->status)) return;
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    while (true) {
+        unsigned int t = 0;
+        if (lane == 0) t = atomicAdd(a.ticket, 1u) + 1u;  // ticket starts at 0xFFFFFFFF
+        t = __shfl_sync(FULL, t, 0);
+        if (t >= (unsigned)a.n_tasks) return;
+        const int2 task = a.tasks[t];
+        unsigned long long t_start = 0;
+        if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+        if (task.y & kTaskLong) {
+            const int r = a.order[task.x];
+            const double b = UPPER ? a.in[r] : a.in[a.in_perm[r]];
+            const int k0 = a.ptr[r], k1 = a.ptr[r + 1];
+            double s = b;
+            if (!FAST) {
+                // products in parallel, the reference's subtraction chain on lane 0
+                double* sp = s_prod[threadIdx.x >> 5];
+                for (int base = k0; base < k1; base += 32) {
+                    const int k = base + lane;
+                    if (k < k1) sp[lane] = a.val[k] * load_ready(a.out + a.col[k]);
+                    __syncwarp();
+                    if (lane == 0) {
+                        const int cnt = min(32, k1 - base);
+                        for (int q = 0; q < cnt; ++q) s -= sp[q];
+                    }
+                    __syncwarp();
+                }
+            } else {
+                double acc = 0.0;
+                const int nch = (k1 - k0 + 31) >> 5;
+                int ci = 0;
+                for (; ci + 4 <= nch; ci += 4) {
+                    int kk[4];
+                    double v[4], y[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int ch = UPPER ? nch - 1 - (ci + q) : ci + q;  // U: newest last
+                        kk[q] = k0 + ch * 32 + lane;
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) v[q] = kk[q] < k1 ? a.val[kk[q]] : 0.0;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) y[q] = kk[q] < k1 ? __ldca(a.out + a.col[kk[q]]) : 0.0;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        if (kk[q] < k1 && __double_as_longlong(y[q]) == (long long)kSentinel)
+                            y[q] = load_ready(a.out + a.col[kk[q]]);
+                        acc += v[q] * y[q];
+                    }
+                }
+                for (; ci < nch; ++ci) {
+                    const int ch = UPPER ? nch - 1 - ci : ci;
+                    const int k = k0 + ch * 32 + lane;
+                    if (k < k1) acc += a.val[k] * load_ready(a.out + a.col[k]);
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
+                s = b - acc;
+            }
+            if (lane == 0) {
+                trsv_finish<UPPER>(a, r, s);
+                if (a.trace) {
+                    unsigned long long t_end;
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+                    a.trace[2 * r] = t_start;
+                    a.trace[2 * r + 1] = t_end;
+                }
+            }
+        } else {
+            const int cnt = task.y & 0xFF;
+            const int lg = (task.y >> 8) & 0x7;  // log2 lanes per row
+            const int lpr = 1 << lg;
+            const int seg = lane >> lg, sl = lane & (lpr - 1);
+            const bool active = seg < cnt;
+            int r = 0;
+            double b = 0.0, acc = 0.0, s = 0.0;
+            if (active) {
+                r = a.order[task.x + seg];
+                b = UPPER ? a.in[r] : a.in[a.in_perm[r]];
+                const int k0 = a.ptr[r], k1 = a.ptr[r + 1];
+                if (lpr == 1) {
+                    // one lane per row, the reference's order (U reversed in FAST)
+                    s = b;
+                    constexpr int CH = 4;
+                    const int len = k1 - k0;
+                    int j = 0;
+                    for (; j + CH <= len; j += CH) {
+                        int kk[CH];
+                        double v[CH], y[CH];
+#pragma unroll
+                        for (int q = 0; q < CH; ++q) kk[q] = (FAST && UPPER) ? k1 - 1 - (j + q) : k0 + j + q;
+#pragma unroll
+                        for (int q = 0; q < CH; ++q) v[q] = a.val[kk[q]];
+#pragma unroll
+                        for (int q = 0; q < CH; ++q) y[q] = __ldca(a.out + a.col[kk[q]]);
+#pragma unroll
+                        for (int q = 0; q < CH; ++q) {
+                            if (__double_as_longlong(y[q]) == (long long)kSentinel)
+                                y[q] = load_ready(a.out + a.col[kk[q]]);
+                            s -= v[q] * y[q];
+                        }
+                    }
+                    for (; j < len; ++j) {
+                        const int k = (FAST && UPPER) ? k1 - 1 - j : k0 + j;
+                        s -= a.val[k] * load_ready(a.out + a.col[k]);
+                    }
+                } else {
+                    // FAST: lpr lanes per row, strided partial sums
+                    const int nj = (k1 - k0 - sl + lpr - 1) >> lg;
+                    for (int jj = 0; jj < nj; ++jj) {
+                        const int j = UPPER ? nj - 1 - jj : jj;
+                        const int k = k0 + sl + (j << lg);
+                        acc += a.val[k] * load_ready(a.out + a.col[k]);
+                    }
+                }
+            }
+            if (lpr > 1) {
+                for (int o = lpr >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
+                s = b - acc;
+            }
+            if (active && sl == 0) {
+                trsv_finish<UPPER>(a, r, s);
+                if (a.trace) {
+                    unsigned long long t_end;
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+                    a.trace[2 * r] = t_start;
+                    a.trace[2 * r + 1] = t_end;
+                }
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// row-sequential warp SpMV helper for rows of very different lengths
+// (factor apply): long rows cooperatively with the in-order chain through
+// shuffles, short rows one per lane.  Bit-identical to spmv.
+// ---------------------------------------------------------------------------
+template <typename XFn>
+__device__ __forceinline__ double warp_row_dot_exact(int k0, int k1, const int* __restrict__ col,
+                                                     const double* __restrict__ val, XFn xfn,
+                                                     double s, double* sp) {
+    const int lane = threadIdx.x & 31;
+    for (int base = k0; base < k1; base += 32) {
+        const int k = base + lane;
+        if (k < k1) sp[lane] = val[k] * xfn(col[k]);
+        __syncwarp();
+        if (lane == 0) {
+            const int cnt = min(32, k1 - base);
+            for (int q = 0; q < cnt; ++q) s += sp[q];
+        }
+        __syncwarp();
+    }
+    return __shfl_sync(0xffffffffu, s, 0);
+}
+
+// U apply: t[r] = diag*x[cp[r]] + sum_{c>r} U_rc x[cp[c]]  (diagonal first)
+__global__ void __launch_bounds__(256)
+    k_apply_u2(const int* __restrict__ uptr, const int* __restrict__ ucol,
+               const double* __restrict__ uval, const double* __restrict__ udiag, int n,
+               const int* __restrict__ col_perm, const double* __restrict__ x,
+               double* __restrict__ t, const Ctrl* ctrl, const double* __restrict__ vbase,
+               long long ldv) {
+    __shared__ double s_prod[8][32];
+    const double* xs = x;
+    if (ctrl) {
+        if (!ctrl->need_weight || ctrl->converged || ctrl->status) return;
+        xs = vbase + (long long)ctrl->m * ldv;
+    }
+    const int lane = threadIdx.x & 31;
+    const int r0 = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32;
+    if (r0 >= n) return;
+    const int r = r0 + lane;
+    const int len = r < n ? uptr[r + 1] - uptr[r] : 0;
+    unsigned long_mask = __ballot_sync(0xffffffffu, len > kLongRow);
+    auto xfn = [&](int c) { return xs[col_perm[c]]; };
+    double mine = 0.0;
+    while (long_mask) {
+        const int q = __ffs(long_mask) - 1;
+        long_mask &= long_mask - 1;
+        const int rq = r0 + q;
+        double s = 0.0;
+        s += udiag[rq] * xs[col_perm[rq]];
+        s = warp_row_dot_exact(uptr[rq], uptr[rq + 1], ucol, uval, xfn, s, s_prod[threadIdx.x >> 5]);
+        if (lane == q) mine = s;
+    }
+    if (r < n) {
+        if (len <= kLongRow) {
+            double s = 0.0;
+            s += udiag[r] * xs[col_perm[r]];
+            for (int k = uptr[r]; k < uptr[r + 1]; ++k) s += uval[k] * xs[col_perm[ucol[k]]];
+            mine = s;
+        }
+        t[r] = mine;
+    }
+}
+
+// L apply + ||y||^2: y[r] = sum_{c<r} L_rc t[c] + 1.0*t[r]  (diagonal last)
+__global__ void __launch_bounds__(256)
+    k_apply_l2(const int* __restrict__ lptr, const int* __restrict__ lcol,
+               const double* __restrict__ lval, int n, const double* __restrict__ t,
+               double* __restrict__ y_out, const int* __restrict__ row_perm,
+               double* __restrict__ partials, unsigned int* __restrict__ done_counter, Ctrl* ctrl,
+               double* __restrict__ weight_out) {
+    __shared__ double sh[33];
+    __shared__ bool s_last;
+    __shared__ double s_prod[8][32];
+    if (ctrl && (!ctrl->need_weight || ctrl->converged || ctrl->status)) return;
+    const int lane = threadIdx.x & 31;
+    const int r0 = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32;
+    const int r = r0 + lane;
+    double sq = 0.0;
+    if (r0 < n) {
+        const int len = r < n ? lptr[r + 1] - lptr[r] : 0;
+        unsigned long_mask = __ballot_sync(0xffffffffu, len > kLongRow);
+        auto xfn = [&](int c) { return t[c]; };
+        double mine = 0.0;
+        while (long_mask) {
+            const int q = __ffs(long_mask) - 1;
+            long_mask &= long_mask - 1;
+            const int rq = r0 + q;
+            double s = warp_row_dot_exact(lptr[rq], lptr[rq + 1], lcol, lval, xfn, 0.0, s_prod[threadIdx.x >> 5]);
+            s += 1.0 * t[rq];
+            if (lane == q) mine = s;
+        }
+        if (r < n) {
+            if (len <= kLongRow) {
+                double s = 0.0;
+                for (int k = lptr[r]; k < lptr[r + 1]; ++k) s += lval[k] * t[lcol[k]];
+                s += 1.0 * t[r];
+                mine = s;
+            }
+            if (y_out) y_out[row_perm[r]] = mine;
+            sq = mine * mine;
+        }
+    }
+    const double bs = block_sum(sq, sh);
+    if (threadIdx.x == 0) {
+        partials[blockIdx.x] = bs;
+        __threadfence();
+        const unsigned int prev = atomicAdd(done_counter, 1u);
+        s_last = (prev == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    double acc = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) acc += ld_cg(partials + b);
+    const double tot = block_sum(acc, sh);
+    if (threadIdx.x == 0) {
+        *done_counter = 0u;
+        const double w = sqrt(tot);
+        if (weight_out) *weight_out = w;
+        if (ctrl) {
+            ctrl->weight = w;
+            decide(ctrl);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Factor apply over the EXACT warp-task lists (no dependencies: any order).
+// Long rows get a whole warp (products in parallel, the reference's in-order
+// accumulation on lane 0), short rows one lane each.  Bit-identical to
+// spmv(U, .) / spmv(L, .) of Factorization::apply (sparse_lu.cpp:299-300).
+//   UPPER: t[r] = 0 + diag*x[cp[r]] + sum_{c>r} U_rc x[cp[c]]   (diag first)
+//   LOWER: y[r] = sum_{c<r} L_rc t[c] + 1.0*t[r]; sq[r] = y^2  (diag last)
+// ---------------------------------------------------------------------------
+template <bool UPPER>
+__global__ void __launch_bounds__(256)
+    k_apply_tasks(const int2* __restrict__ tasks, int n_tasks, const int* __restrict__ order,
+                  const int* __restrict__ ptr, const int* __restrict__ col,
+                  const double* __restrict__ val, const double* __restrict__ diag,
+                  const int* __restrict__ col_perm, const double* __restrict__ x,
+                  double* __restrict__ out, double* __restrict__ sq, const int* __restrict__ row_perm,
+                  double* __restrict__ y_out, const Ctrl* ctrl, const double* __restrict__ vbase,
+                  long long ldv) {
+    __shared__ double s_prod[8][32];
+    const double* xs = x;
+    if (ctrl) {
+        if (!ctrl->need_weight || ctrl->converged || ctrl->status) return;
+        if (UPPER) xs = vbase + (long long)ctrl->m * ldv;
+    }
+    const int lane = threadIdx.x & 31;
+    const int wglobal = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int nw = gridDim.x * (blockDim.x >> 5);
+    auto xv = [&](int c) { return UPPER ? xs[col_perm[c]] : xs[c]; };
+    for (int t = wglobal; t < n_tasks; t += nw) {
+        const int2 task = tasks[t];
+        if (task.y & kTaskLong) {
+            const int r = order[task.x];
+            double s = 0.0;
+            if (UPPER) s += diag[r] * xv(r);
+            s = warp_row_dot_exact(ptr[r], ptr[r + 1], col, val, xv, s, s_prod[threadIdx.x >> 5]);
+            if (!UPPER) s += 1.0 * xs[r];
+            if (lane == 0) {
+                out[r] = s;
+                if (sq) sq[r] = s * s;
+                if (y_out) y_out[row_perm[r]] = s;
+            }
+        } else {
+            const int cnt = task.y & 0xFF;
+            if (lane < cnt) {
+                const int r = order[task.x + lane];
+                double s = 0.0;
+                if (UPPER) s += diag[r] * xv(r);
+                for (int k = ptr[r]; k < ptr[r + 1]; ++k) s += val[k] * xv(col[k]);
+                if (!UPPER) s += 1.0 * xs[r];
+                out[r] = s;
+                if (sq) sq[r] = s * s;
+                if (y_out) y_out[row_perm[r]] = s;
+            }
+        }
+    }
+}
+
+// deterministic sum of sq[0..n) -> sqrt -> weight (+ Arnoldi decision)
+__global__ void __launch_bounds__(256)
+    k_sum_sqrt(const double* __restrict__ sq, int n, double* __restrict__ partials,
+               unsigned int* __restrict__ done_counter, Ctrl* ctrl, double* __restrict__ weight_out) {
+    __shared__ double sh[33];
+    __shared__ bool s_last;
+    if (ctrl && (!ctrl->need_weight || ctrl->converged || ctrl->status)) return;
+    double acc = 0.0;
+    const int per = (n + gridDim.x - 1) / gridDim.x;
+    const int lo = blockIdx.x * per, hi = min(n, lo + per);
+    for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) acc += sq[i];
+    const double bs = block_sum(acc, sh);
+    if (threadIdx.x == 0) {
+        partials[blockIdx.x] = bs;
+        __threadfence();
+        s_last = atomicAdd(done_counter, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    double a2 = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) a2 += ld_cg(partials + b);
+    const double tot = block_sum(a2, sh);
+    if (threadIdx.x == 0) {
+        *done_counter = 0u;
+        const double w = sqrt(tot);
+        if (weight_out) *weight_out = w;
+        if (ctrl) {
+            ctrl->weight = w;
+            decide(ctrl);
+        }
+    }
+}
+
 // ============================================================================
 // Factor apply y = P^T L U Q^T x (sparse_lu.cpp:293-304), row-sequential.
 // apply_u: t[r] = diag*x[cp[r]] + sum_{c>r} U_rc x[cp[c]]  (diagonal first)
@@ -954,8 +1346,31 @@ void spmv_b2(const Launch& L, const int* rowptr, const int* col, const double* v
     count(L);
 }
 
+template <bool U, bool FST>
+static int trsv2_occ() {
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_trsv2<U, FST>, 256, 0);
+    return occ > 0 ? occ : 1;
+}
+
 void trsv(const Launch& L, bool upper, bool reverse, const TrsvArgs& a) {
     if (a.n <= 0) return;
+    if (a.tasks) {
+        static int occ[4] = {0, 0, 0, 0};
+        const int id = (upper ? 2 : 0) + (reverse ? 1 : 0);
+        if (!occ[id])
+            occ[id] = id == 0 ? trsv2_occ<false, false>() : id == 1 ? trsv2_occ<false, true>()
+                    : id == 2 ? trsv2_occ<true, false>() : trsv2_occ<true, true>();
+        const long long warps_needed = a.n_tasks;
+        const unsigned int grid = (unsigned int)std::max<long long>(
+            1, std::min<long long>((long long)L.num_sms * occ[id], (warps_needed + 7) / 8));
+        if (!upper && !reverse) k_trsv2<false, false><<<grid, 256, 0, L.stream>>>(a);
+        else if (!upper) k_trsv2<false, true><<<grid, 256, 0, L.stream>>>(a);
+        else if (!reverse) k_trsv2<true, false><<<grid, 256, 0, L.stream>>>(a);
+        else k_trsv2<true, true><<<grid, 256, 0, L.stream>>>(a);
+        count(L);
+        return;
+    }
     const unsigned int grid = cdiv(a.n, kTrsvThreads);
     if (!upper)
         k_trsv<false, false><<<grid, kTrsvThreads, 0, L.stream>>>(a);
@@ -971,11 +1386,30 @@ void apply_weight(const Launch& L, const int* uptr, const int* ucol, const doubl
                   const int* col_perm, const int* row_perm, const double* x, double* t,
                   double* y_out, double* partials, unsigned int* done, Ctrl* ctrl,
                   const double* vbase, long long ldv, double* weight_out) {
-    k_apply_u_diag<<<cdiv(n, 256), 256, 0, L.stream>>>(uptr, ucol, uval, udiag, n, col_perm, x, t,
-                                                      ctrl, vbase, ldv);
-    k_apply_l_norm<<<cdiv(n, 256), 256, 0, L.stream>>>(lptr, lcol, lval, n, t, y_out, row_perm,
-                                                      partials, done, ctrl, weight_out);
+    k_apply_u2<<<cdiv(n, 256), 256, 0, L.stream>>>(uptr, ucol, uval, udiag, n, col_perm, x, t,
+                                                  ctrl, vbase, ldv);
+    k_apply_l2<<<cdiv(n, 256), 256, 0, L.stream>>>(lptr, lcol, lval, n, t, y_out, row_perm,
+                                                  partials, done, ctrl, weight_out);
     count(L, 2);
+}
+
+void apply_tasks(const Launch& L, const int2* utasks, int n_utasks, const int* uorder,
+                 const int2* ltasks, int n_ltasks, const int* lorder, const int* uptr,
+                 const int* ucol, const double* uval, const double* udiag, const int* lptr,
+                 const int* lcol, const double* lval, int n, const int* col_perm,
+                 const int* row_perm, const double* x, double* t, double* y, double* sq,
+                 double* y_out, double* partials, unsigned int* done, Ctrl* ctrl,
+                 const double* vbase, long long ldv, double* weight_out) {
+    const unsigned int grid = (unsigned int)std::min<long long>((long long)L.num_sms * 8,
+                                                                 ((long long)std::max(n_utasks, n_ltasks) + 7) / 8 + 1);
+    k_apply_tasks<true><<<grid, 256, 0, L.stream>>>(utasks, n_utasks, uorder, uptr, ucol, uval, udiag,
+                                                   col_perm, x, t, nullptr, nullptr, nullptr, ctrl,
+                                                   vbase, ldv);
+    k_apply_tasks<false><<<grid, 256, 0, L.stream>>>(ltasks, n_ltasks, lorder, lptr, lcol, lval, nullptr,
+                                                    nullptr, t, y, sq, row_perm, y_out, ctrl, nullptr, 0);
+    const unsigned int g2 = std::min<unsigned int>(cdiv(n, 2048), 1024);
+    k_sum_sqrt<<<g2, 256, 0, L.stream>>>(sq, n, partials, done, ctrl, weight_out);
+    count(L, 3);
 }
 
 void spmv_norm(const Launch& L, const int* rowptr, const int* col, const double* val, int n,

@@ -21,6 +21,8 @@
 #include <chrono>
 #include <cmath>
 #include <limits>
+#include <cstdio>
+#include <cstdlib>
 
 #include "host.hpp"
 
@@ -105,9 +107,20 @@ std::vector<int> min_degree_order(const Csr& A) {
     heap.deg = &deg;
     heap.build(n);
 
+    // Adjacency lists may keep eliminated vertices (filtered lazily); deg[v]
+    // is always the exact number of live neighbours, i.e. the size of the
+    // reference's explicit list.  Every elimination clique is remembered with
+    // its live member count: when the pivot's whole neighbourhood is one such
+    // clique, eliminating it creates no fill and only lowers each neighbour's
+    // degree by one — O(deg) instead of the O(deg^2) list merge.
+    std::vector<char> dead(n, 0);
+    std::vector<std::vector<int>> cliques_of(n);
+    std::vector<int> clique_live;
+
     std::vector<int> order;
     order.reserve(n);
     std::vector<int> nbr, merged;
+    long long st_fast = 0, st_slow = 0, st_merge = 0, st_slow_d2 = 0;
     while (heap.size() > 0) {
         // complete remaining graph: all degrees equal, reference takes them
         // by increasing index (sparse_lu.cpp:68-75 strict '<' keeps the first)
@@ -119,33 +132,58 @@ std::vector<int> min_degree_order(const Csr& A) {
         }
         const int best = heap.pop();
         order.push_back(best);
-        nbr.swap(adj[best]);  // all live; sorted
-        for (int u : nbr) {
-            // adj[u] := (adj[u] \ {best}) U (nbr \ {u}), sorted unique —
-            // the set the reference's erase + binary_search/insert builds
-            const auto& au = adj[u];
-            merged.clear();
-            merged.reserve(au.size() + nbr.size());
-            size_t i = 0, j = 0;
-            while (i < au.size() || j < nbr.size()) {
-                int x;
-                if (j >= nbr.size() || (i < au.size() && au[i] < nbr[j])) {
-                    x = au[i++];
-                } else if (i >= au.size() || nbr[j] < au[i]) {
-                    x = nbr[j++];
-                } else {
-                    x = au[i++];
-                    ++j;
-                }
-                if (x == best || x == u) continue;
-                merged.push_back(x);
+        dead[best] = 1;
+        nbr.clear();
+        for (int u : adj[best])
+            if (!dead[u]) nbr.push_back(u);
+        int big = -1, big_live = 0;
+        for (int c : cliques_of[best])
+            if (clique_live[c] > big_live) {
+                big_live = clique_live[c];
+                big = c;
             }
-            adj[u].swap(merged);
-            deg[u] = static_cast<int>(adj[u].size());
-            heap.changed(u);
+        const bool no_fill = big >= 0 && big_live - 1 == static_cast<int>(nbr.size());
+        if (no_fill) ++st_fast; else { ++st_slow; st_slow_d2 += (long long)nbr.size() * nbr.size(); }
+        if (no_fill) {
+            for (int u : nbr) {
+                deg[u] -= 1;
+                heap.changed(u);
+            }
+        } else {
+            const int cid = static_cast<int>(clique_live.size());
+            clique_live.push_back(static_cast<int>(nbr.size()));
+            for (int u : nbr) {
+                // adj[u] := (live(adj[u]) \ {best}) U (nbr \ {u}), sorted unique
+                const auto& au = adj[u];
+                st_merge += au.size() + nbr.size();
+                merged.clear();
+                merged.reserve(au.size() + nbr.size());
+                size_t i = 0, j = 0;
+                while (i < au.size() || j < nbr.size()) {
+                    int x;
+                    if (j >= nbr.size() || (i < au.size() && au[i] < nbr[j])) {
+                        x = au[i++];
+                    } else if (i >= au.size() || nbr[j] < au[i]) {
+                        x = nbr[j++];
+                    } else {
+                        x = au[i++];
+                        ++j;
+                    }
+                    if (x == u || dead[x]) continue;
+                    merged.push_back(x);
+                }
+                adj[u].swap(merged);
+                deg[u] = static_cast<int>(adj[u].size());
+                heap.changed(u);
+                cliques_of[u].push_back(cid);
+            }
         }
-        std::vector<int>().swap(nbr);
+        for (int c : cliques_of[best]) clique_live[c] -= 1;
+        std::vector<int>().swap(adj[best]);
+        std::vector<int>().swap(cliques_of[best]);
     }
+    if (getenv("EXG_MD_STATS"))
+        fprintf(stderr, "md: fast %lld slow %lld merge %lld slow_d2 %lld\n", st_fast, st_slow, st_merge, st_slow_d2);
     return order;
 }
 
@@ -221,10 +259,18 @@ void lu_factor(const Csr& A, double pivot_tol, Factor& f) {
     for (double v : A.val) max_abs = std::max(max_abs, std::abs(v));
     const double sing_tol = 1e-14 * max_abs;
 
-    const Csc a = to_csc(A);
+    Csc a = to_csc(A);
     const auto t0 = clock::now();
     const std::vector<int> col_order = min_degree_order(A);
     const auto t1 = clock::now();
+    // Work in relabelled row coordinates: row i gets the label of its column
+    // position in col_order (the diagonal row of column j is label j).  The
+    // arithmetic, the DFS visiting order and every tie-break are unchanged —
+    // ties compare ORIGINAL row ids, exactly as sparse_lu.cpp:197 — but the
+    // dense elimination tail now touches a contiguous range of x.
+    std::vector<int> label(n);
+    for (int j = 0; j < n; ++j) label[col_order[j]] = j;
+    for (int& r : a.row_idx) r = label[r];
 
     std::vector<std::vector<int>> l_rows(n);
     std::vector<std::vector<double>> l_vals(n);
@@ -260,14 +306,15 @@ void lu_factor(const Csr& A, double pivot_tol, Factor& f) {
             if (pivot_pos[r] < 0) xmax = std::max(xmax, std::abs(x[r]));
         int pivot_row = -1;
         if (xmax > sing_tol && xmax > 0.0) {
-            if (pivot_pos[cj] < 0 && mark[cj] && std::abs(x[cj]) >= pivot_tol * xmax) {
-                pivot_row = cj;
+            if (pivot_pos[j] < 0 && mark[j] && std::abs(x[j]) >= pivot_tol * xmax) {
+                pivot_row = j;  // label of the natural diagonal row cj
             } else {
                 double best = -1.0;
                 for (int r : topo) {
                     if (pivot_pos[r] >= 0) continue;
                     const double m = std::abs(x[r]);
-                    if (m > best || (m == best && (pivot_row < 0 || r < pivot_row))) {
+                    if (m > best ||
+                        (m == best && (pivot_row < 0 || col_order[r] < col_order[pivot_row]))) {
                         best = m;
                         pivot_row = r;
                     }
@@ -295,7 +342,7 @@ void lu_factor(const Csr& A, double pivot_tol, Factor& f) {
         }
         u_diag[j] = pv;
         pivot_pos[pivot_row] = j;
-        row_perm[j] = pivot_row;
+        row_perm[j] = col_order[pivot_row];
         for (int r : topo) {
             x[r] = 0.0;
             mark[r] = 0;

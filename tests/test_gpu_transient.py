@@ -38,8 +38,10 @@ def compare(got, want):
     return err
 
 
-@pytest.mark.parametrize("mode", [F.EXG_TRSV_EXACT, F.EXG_TRSV_FAST], ids=["exact", "fast"])
-def test_config0_vs_transient_as_shipped(ref, mode):
+@pytest.mark.parametrize("mode,weight", [(F.EXG_TRSV_EXACT, F.EXG_WEIGHT_APPLY),
+                                         (F.EXG_TRSV_FAST, F.EXG_WEIGHT_GSPMV)],
+                         ids=["exact", "fast-gspmv"])
+def test_config0_vs_transient_as_shipped(ref, mode, weight):
     s = ex.System.generate(0)
     ctl = s.step_control()
     ctl.fixed_step = 1
@@ -50,7 +52,7 @@ def test_config0_vs_transient_as_shipped(ref, mode):
         want = ref.transient(rh, ctl, 1e-9, rec)
     finally:
         ref.system_free(rh)
-    with Context(0, trsv_mode=mode) as c:
+    with Context(0, trsv_mode=mode, weight_mode=weight) as c:
         got = c.transient(s, ctl, 1e-9, rec)
     assert len(got.t) >= 1000
     compare(got, want)
@@ -61,8 +63,11 @@ def test_config0_vs_transient_as_shipped(ref, mode):
     (2, dict(width=12), 1e-9),
     (3, dict(n=3000), 5e-10),
 ])
-@pytest.mark.parametrize("mode", [F.EXG_TRSV_EXACT, F.EXG_TRSV_FAST], ids=["exact", "fast"])
-def test_configs_vs_cached_oracle(ref, cfg, kw, t_stop, mode):
+@pytest.mark.parametrize("mode,weight", [(F.EXG_TRSV_EXACT, F.EXG_WEIGHT_APPLY),
+                                         (F.EXG_TRSV_FAST, F.EXG_WEIGHT_APPLY),
+                                         (F.EXG_TRSV_FAST, F.EXG_WEIGHT_GSPMV)],
+                         ids=["exact", "fast", "fast-gspmv"])
+def test_configs_vs_cached_oracle(ref, cfg, kw, t_stop, mode, weight):
     s = ex.System.generate(cfg, **kw)
     ctl = s.step_control()
     if cfg == 3:
@@ -77,6 +82,6 @@ def test_configs_vs_cached_oracle(ref, cfg, kw, t_stop, mode):
     finally:
         ref.factor_free(fh)
         ref.system_free(rh)
-    with Context(0, trsv_mode=mode) as c:
+    with Context(0, trsv_mode=mode, weight_mode=weight) as c:
         got = c.transient(s, ctl, t_stop, rec)
     compare(got, want)

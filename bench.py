@@ -294,7 +294,7 @@ def run_ours(args, rank, world, local):
                        "ms_per_launch": round(per * 1e3, 4), "bytes_per_launch": alg[k]}
     dom_roof = dom if dom in roof else "trsv_u" if "trsv_u" in roof else next(iter(roof))
     traffic = None
-    tf = ROOT / "profiles" / "r01_traffic.json"
+    tf = ROOT / "profiles" / "traffic_config1.json"
     if tf.exists():
         try:
             traffic = json.loads(tf.read_text()).get(dom_roof)

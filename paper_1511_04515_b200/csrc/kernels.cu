@@ -201,9 +201,15 @@ constexpr int kLongRow = 32;
 constexpr int kTaskLong = 1 << 30;
 __device__ void decide(Ctrl* c);
 
+#ifndef EXG_POLL_NS
+#define EXG_POLL_NS 0
+#endif
 __device__ __forceinline__ double load_ready(const double* p) {
     unsigned long long v = __double_as_longlong(__ldca(p));
-    while (v == kSentinel) v = ld_relaxed(p);
+    while (v == kSentinel) {
+        if (EXG_POLL_NS) __nanosleep(EXG_POLL_NS);
+        v = ld_relaxed(p);
+    }
     return __longlong_as_double(v);
 }
 

@@ -163,8 +163,9 @@ typedef struct exg_kernel_times {
     int64_t count[EXG_K_CLASSES];
 } exg_kernel_times;
 exg_status exg_profile_enable(exg_ctx* ctx, int on);
-/* debug: one solve with per-row (start, end) %globaltimer stamps; times holds
- * 4n values (L sweep pairs, then U sweep pairs) */
+/* debug: one solve with per-row %globaltimer stamps; times holds 10n values:
+ * (start, end) of the warp-task sweeps for L then U (4n), then (start,
+ * far-done, end) of the cluster sweeps for L then U (6n); zero = not run there */
 exg_status exg_debug_trace_solve(exg_ctx* ctx, const double* b, unsigned long long* times);
 exg_status exg_profile_get(exg_ctx* ctx, exg_kernel_times* out); /* synchronises; resets */
 

@@ -3,6 +3,8 @@
 // the reference's spmv / Factorization::solve / apply / mevp_iks /
 // mevp_residual / eval_at_scaled_h / er_begin / er_eval.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <new>
@@ -153,49 +155,99 @@ const DCsr& mat(exg_ctx* c, int which) {
 void solve_dev(exg_ctx* c, const double* b, double* final_out, double coef, const double* add,
                const Ctrl* ctrl) {
     const int n = c->n;
-    ck(cudaMemsetAsync(c->trsv_buf, 0xFF, 16 + 2 * sizeof(double) * (size_t)n, c->stream), "memset");
+    ck(cudaMemsetAsync(c->trsv_buf, 0xFF, kTrsvHdr + 2 * sizeof(double) * (size_t)n, c->stream), "memset");
     unsigned int* tickets = reinterpret_cast<unsigned int*>(c->trsv_buf);
-    double* y = reinterpret_cast<double*>(c->trsv_buf + 16);
+    double* y = reinterpret_cast<double*>(c->trsv_buf + kTrsvHdr);
     double* x = y + n;
-    exg::dev::TrsvArgs a{};
-    a.n = n;
-    a.order = c->l_order;
-    a.ptr = c->l_ptr;
-    a.col = c->l_col;
-    a.val = c->l_val;
-    a.in = b;
-    a.in_perm = c->row_perm;
-    a.out = y;
-    a.ticket = tickets;
-    a.ctrl = ctrl;
-    const int fq = c->opt.trsv_mode == EXG_TRSV_FAST ? 2 : 0;
-    a.tasks = c->tasks[fq];
-    a.n_tasks = c->n_tasks[fq];
-    a.trace = c->trace_l;
-    cudaEvent_t e0 = c->prof_begin();
-    exg::dev::trsv(c->L(), false, false, a);
-    c->prof_end(EXG_K_TRSV_L, e0);
-    exg::dev::TrsvArgs u{};
-    u.n = n;
-    u.order = c->u_order;
-    u.ptr = c->u_ptr;
-    u.col = c->u_col;
-    u.val = c->u_val;
-    u.diag = c->u_diag;
-    u.in = y;
-    u.out = x;
-    u.ticket = tickets + 1;
-    u.final_out = final_out;
-    u.out_perm = c->col_perm;
-    u.add = add;
-    u.coef = coef;
-    u.ctrl = ctrl;
-    u.tasks = c->tasks[fq + 1];
-    u.n_tasks = c->n_tasks[fq + 1];
-    u.trace = c->trace_u;
-    cudaEvent_t e1 = c->prof_begin();
-    exg::dev::trsv(c->L(), true, c->opt.trsv_mode == EXG_TRSV_FAST, u);
-    c->prof_end(EXG_K_TRSV_U, e1);
+    const bool fast = c->opt.trsv_mode == EXG_TRSV_FAST;
+    const int fq = fast ? 2 : 0;
+    int next_ticket = 0;
+    for (int tri = 0; tri < 2; ++tri) {
+        const bool upper = tri == 1;
+        exg::dev::TrsvArgs a{};
+        a.n = n;
+        a.order = upper ? c->u_order : c->l_order;
+        a.ptr = upper ? c->u_ptr : c->l_ptr;
+        a.col = upper ? c->u_col : c->l_col;
+        a.val = upper ? c->u_val : c->l_val;
+        a.diag = upper ? c->u_diag : nullptr;
+        a.in = upper ? y : b;
+        a.in_perm = upper ? nullptr : c->row_perm;
+        a.out = upper ? x : y;
+        a.ctrl = ctrl;
+        a.trace = upper ? c->trace_u : c->trace_l;
+        if (upper) {
+            a.final_out = final_out;
+            a.out_perm = c->col_perm;
+            a.add = add;
+            a.coef = coef;
+        }
+        cudaEvent_t e0 = c->prof_begin();
+        const int2* tasks = c->tasks[fq + tri];
+        if (!fast) {
+            a.tasks = tasks;
+            a.n_tasks = c->n_tasks[fq + tri];
+            a.ticket = tickets + next_ticket++;
+            exg::dev::trsv(c->L(), upper, fast, a);
+        } else {
+            const TriPlan& P = c->plan[tri];
+            static const bool run_timing = getenv("EXG_RUN_TIMING") != nullptr;
+            std::vector<cudaEvent_t> rev;
+            for (const TriPlan::Run& run : P.runs) {
+                if (run_timing) {
+                    cudaEvent_t e;
+                    cudaEventCreate(&e);
+                    cudaEventRecord(e, c->stream);
+                    rev.push_back(e);
+                }
+                if (!run.narrow) {
+                    if (run.b <= run.a) continue;
+                    a.tasks = tasks + run.a;
+                    a.n_tasks = run.b - run.a;
+                    if (next_ticket >= kMaxTickets) throw ApiError{EXG_E_CONTRACT, "too many solve runs"};
+                    a.ticket = tickets + next_ticket++;
+                    exg::dev::trsv(c->L(), upper, true, a);
+                } else {
+                    exg::dev::NarrowArgs na{};
+                    na.regions = P.regions + run.a;
+                    na.n_regions = run.b - run.a;
+                    na.rows = P.rows;
+                    na.nptr = P.nptr;
+                    na.nmid = P.nmid;
+                    na.ncol = P.ncol;
+                    na.nval = P.nval;
+                    na.in = a.in;
+                    na.in_perm = a.in_perm;
+                    na.diag = a.diag;
+                    na.out = a.out;
+                    na.final_out = a.final_out;
+                    na.out_perm = a.out_perm;
+                    na.add = a.add;
+                    na.coef = a.coef;
+                    na.ctrl = ctrl;
+                    na.trace = upper ? c->ntrace_u : c->ntrace_l;
+                    exg::dev::trsv_narrow(c->L(), upper, na, c->cluster, P.smem);
+                }
+            }
+            if (run_timing) {
+                cudaEvent_t e;
+                cudaEventCreate(&e);
+                cudaEventRecord(e, c->stream);
+                rev.push_back(e);
+                cudaStreamSynchronize(c->stream);
+                fprintf(stderr, "[%c runs]", upper ? 'U' : 'L');
+                for (size_t i = 0; i + 1 < rev.size(); ++i) {
+                    float ms = 0.f;
+                    cudaEventElapsedTime(&ms, rev[i], rev[i + 1]);
+                    const TriPlan::Run& run = P.runs[i];
+                    fprintf(stderr, " %s[%d,%d):%.3fms", run.narrow ? "N" : "W", run.a, run.b, ms);
+                }
+                fprintf(stderr, "\n");
+                for (auto e : rev) cudaEventDestroy(e);
+            }
+        }
+        c->prof_end(upper ? EXG_K_TRSV_U : EXG_K_TRSV_L, e0);
+    }
     c->cnt.trsv_calls++;
 }
 
@@ -328,6 +380,114 @@ void deliver(exg_ctx* c, double* user, const double* dev, size_t count, int ptr_
     }
 }
 
+// Splits a triangle's level sequence into runs (see k_trsv_narrow) and builds
+// the re-encoded narrow-row arrays.
+void plan_triangle(exg_ctx* c, TriPlan& P, bool upper_tri, const std::vector<int>& ord,
+                   const std::vector<int>& level, int nl, const std::vector<int>& ptr,
+                   const std::vector<int>& col, const std::vector<double>& val,
+                   const std::vector<int2>& tasks) {
+    const int n = (int)ord.size();
+    P.free_dev();
+    P.runs.clear();
+    const char* env_t = getenv(upper_tri ? "EXG_NARROW_T_U" : "EXG_NARROW_T_L");
+    if (!env_t) env_t = getenv("EXG_NARROW_T");
+    const int T = env_t ? atoi(env_t) : (upper_tri ? 8 : 32);
+    const char* env_r = getenv("EXG_ABSORB_ROWS");
+    const long long absorb_rows = env_r ? atoll(env_r) : 8192;
+    const int CAP = TriPlan::kCap;
+    std::vector<int> cnt(nl, 0), lpos(nl + 1, 0);
+    for (int r = 0; r < n; ++r) cnt[level[r]]++;
+    for (int l = 0; l < nl; ++l) lpos[l + 1] = lpos[l] + cnt[l];
+    std::vector<int> tfirst(nl + 1, (int)tasks.size());
+    for (int i = (int)tasks.size() - 1; i >= 0; --i) tfirst[level[ord[tasks[i].x]]] = i;
+    for (int l = nl - 1; l >= 0; --l) tfirst[l] = std::min(tfirst[l], tfirst[l + 1]);
+    std::vector<int> pos_of(n);
+    for (int p = 0; p < n; ++p) pos_of[ord[p]] = p;
+    std::vector<int2> regions;
+    std::vector<int> rows, nptr{0}, nmid, ncol;
+    std::vector<double> nval;
+    // level classes, then absorb short wide stretches into the narrow runs
+    // (a launch costs more than a few fat levels on the cluster)
+    std::vector<char> is_narrow(nl);
+    for (int q = 0; q < nl; ++q) is_narrow[q] = T > 0 && cnt[q] <= T;
+    {
+        int q = 0;
+        while (q < nl) {
+            int q1 = q;
+            while (q1 < nl && is_narrow[q1] == is_narrow[q]) ++q1;
+            long long rows_in = lpos[q1] - lpos[q];
+            if (!is_narrow[q] && T > 0 && rows_in < absorb_rows)
+                for (int z = q; z < q1; ++z) is_narrow[z] = 1;
+            q = q1;
+        }
+    }
+    int l = 0;
+    while (l < nl) {
+        const bool narrow = is_narrow[l];
+        int l1 = l;
+        while (l1 < nl && is_narrow[l1] == narrow) ++l1;
+        TriPlan::Run run{};
+        run.narrow = narrow;
+        if (!narrow) {
+            run.a = tfirst[l];
+            run.b = tfirst[l1];
+        } else {
+            run.a = (int)regions.size();
+            for (int p0 = lpos[l]; p0 < lpos[l1]; p0 += CAP) {
+                const int pc = std::min(CAP, lpos[l1] - p0);
+                const int np0 = (int)rows.size();
+                regions.push_back(make_int2(np0, pc));
+                for (int p = p0; p < p0 + pc; ++p) {
+                    const int r = ord[p];
+                    rows.push_back(r);
+                    std::vector<std::pair<int, int>> near;  // (slot, k)
+                    for (int k = ptr[r]; k < ptr[r + 1]; ++k) {
+                        const int pc_ = pos_of[col[k]];
+                        if (pc_ >= p0 && pc_ < p)
+                            near.push_back({pc_ - p0, k});
+                        else {
+                            ncol.push_back(col[k]);
+                            nval.push_back(val[k]);
+                        }
+                    }
+                    std::sort(near.begin(), near.end());
+                    nmid.push_back((int)ncol.size());
+                    for (auto& e : near) {
+                        ncol.push_back(-1 - e.first);
+                        nval.push_back(val[e.second]);
+                    }
+                    nptr.push_back((int)ncol.size());
+                }
+            }
+            run.b = (int)regions.size();
+        }
+        P.runs.push_back(run);
+        l = l1;
+    }
+    if (!regions.empty()) {
+        P.regions = dalloc<int2>(regions.size());
+        P.rows = dalloc<int>(rows.size());
+        P.nptr = dalloc<int>(nptr.size());
+        P.nmid = dalloc<int>(nmid.size());
+        ck(cudaMemcpy(P.nmid, nmid.data(), nmid.size() * sizeof(int), cudaMemcpyHostToDevice), "plan");
+        P.ncol = dalloc<int>(ncol.size());
+        P.nval = dalloc<double>(nval.size());
+        ck(cudaMemcpy(P.regions, regions.data(), regions.size() * sizeof(int2), cudaMemcpyHostToDevice), "plan");
+        ck(cudaMemcpy(P.rows, rows.data(), rows.size() * sizeof(int), cudaMemcpyHostToDevice), "plan");
+        ck(cudaMemcpy(P.nptr, nptr.data(), nptr.size() * sizeof(int), cudaMemcpyHostToDevice), "plan");
+        if (!ncol.empty()) {
+            ck(cudaMemcpy(P.ncol, ncol.data(), ncol.size() * sizeof(int), cudaMemcpyHostToDevice), "plan");
+            ck(cudaMemcpy(P.nval, nval.data(), nval.size() * sizeof(double), cudaMemcpyHostToDevice), "plan");
+        }
+        int mx = 0;
+        for (auto& R : regions) mx = std::max(mx, R.y);
+        P.smem = (size_t)mx * sizeof(double);
+    }
+    P.narrow_rows = (long long)rows.size();
+    P.narrow_nnz = (long long)ncol.size();
+    (void)c;
+}
+
 }  // namespace
 
 extern "C" {
@@ -343,6 +503,10 @@ exg_status exg_create(int device, exg_ctx** out) {
     ck(cudaGetDeviceProperties(&prop, device), "props");
     if (prop.major < 10) throw ApiError{EXG_E_CUDA, "exsim-B200 requires an sm_100a (Blackwell) GPU"};
     c->num_sms = prop.multiProcessorCount;
+    {
+        const char* e = getenv("EXG_CLUSTER");
+        c->cluster = e ? atoi(e) : 16;
+    }
     c->bar = dalloc<unsigned int>(4);
     c->done = dalloc<unsigned int>(4);
     ck(cudaMemset(c->bar, 0, 4 * sizeof(unsigned int)), "memset");
@@ -388,6 +552,8 @@ void exg_destroy(exg_ctx* c) {
     if (c->trsv_buf) cudaFree(c->trsv_buf);
     for (int q = 0; q < 4; ++q)
         if (c->tasks[q]) cudaFree(c->tasks[q]);
+    c->plan[0].free_dev();
+    c->plan[1].free_dev();
     if (c->bar) cudaFree(c->bar);
     if (c->done) cudaFree(c->done);
     if (c->ctrl) cudaFree(c->ctrl);
@@ -560,6 +726,11 @@ exg_status exg_set_factors(exg_ctx* c, int n, const int* Lp, const int* Li, cons
     up_i(c->col_perm, col_perm, n);
     up_i(c->l_order, lord.data(), n);
     up_i(c->u_order, uord.data(), n);
+    // FAST-mode plan: runs of wide levels (warp tasks, all SMs) and of narrow
+    // levels (one thread-block cluster, DSMEM hand-offs)
+    const int lnl = l_levels, unl = u_levels;
+    plan_triangle(c, c->plan[0], false, lord, llev, lnl, lp, lc, lv, ltasks_f);
+    plan_triangle(c, c->plan[1], true, uord, lev, unl, up, uc, uv, utasks_f);
     const std::vector<int2>* tl[4] = {&ltasks, &utasks, &ltasks_f, &utasks_f};
     for (int q = 0; q < 4; ++q) {
         if (c->tasks[q]) cudaFree(c->tasks[q]);
@@ -567,7 +738,7 @@ exg_status exg_set_factors(exg_ctx* c, int n, const int* Lp, const int* Li, cons
         ck(cudaMemcpy(c->tasks[q], tl[q]->data(), tl[q]->size() * sizeof(int2), cudaMemcpyHostToDevice), "tasks");
         c->n_tasks[q] = (int)tl[q]->size();
     }
-    c->trsv_buf = dalloc<char>(16 + 2 * sizeof(double) * (size_t)n);
+    c->trsv_buf = dalloc<char>(kTrsvHdr + 2 * sizeof(double) * (size_t)n);
     ensure_vectors(c, n);
     c->cnt.l_levels = l_levels;
     c->cnt.u_levels = u_levels;
@@ -798,12 +969,19 @@ exg_status exg_debug_trace_solve(exg_ctx* c, const double* b, unsigned long long
     ck(cudaMemsetAsync(tr, 0, sizeof(unsigned long long) * 4 * (size_t)n, c->stream), "memset");
     c->trace_l = tr;
     c->trace_u = tr + 2 * (size_t)n;
+    unsigned long long* ntr = dalloc<unsigned long long>((size_t)6 * n);
+    ck(cudaMemsetAsync(ntr, 0, sizeof(unsigned long long) * 6 * (size_t)n, c->stream), "memset");
+    c->ntrace_l = ntr;
+    c->ntrace_u = ntr + 3 * (size_t)n;
     const double* bd = resolve_in(c, b, n, EXG_PTR_HOST, c->vin);
     solve_dev(c, bd, c->vout, 1.0, nullptr, nullptr);
     c->trace_l = c->trace_u = nullptr;
+    c->ntrace_l = c->ntrace_u = nullptr;
     ck(cudaMemcpyAsync(times, tr, sizeof(unsigned long long) * 4 * (size_t)n, cudaMemcpyDeviceToHost, c->stream), "d2h");
+    ck(cudaMemcpyAsync(times + 4 * (size_t)n, ntr, sizeof(unsigned long long) * 6 * (size_t)n, cudaMemcpyDeviceToHost, c->stream), "d2h");
     ck(cudaStreamSynchronize(c->stream), "sync");
     cudaFree(tr);
+    cudaFree(ntr);
     API_END(c)
 }
 

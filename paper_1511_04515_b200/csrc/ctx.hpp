@@ -16,6 +16,38 @@ struct DCsr {
     double* val = nullptr;
 };
 
+constexpr size_t kTrsvHdr = 1024;  // ticket counters ahead of the solve scratch
+constexpr int kMaxTickets = 256;
+
+// FAST-mode execution plan of one triangle (see plan_triangle, api.cu)
+struct TriPlan {
+    static constexpr int kCap = 27648;  // region rows per shared-memory replica (216 KB)
+    struct Run {
+        int narrow;
+        int a, b;  // wide: task range; narrow: region range
+    };
+    std::vector<Run> runs;
+    int2* regions = nullptr;
+    int* rows = nullptr;
+    int* nptr = nullptr;
+    int* nmid = nullptr;
+    int* ncol = nullptr;
+    double* nval = nullptr;
+    size_t smem = 0;
+    long long narrow_rows = 0, narrow_nnz = 0;
+    void free_dev() {
+        if (regions) cudaFree(regions);
+        if (rows) cudaFree(rows);
+        if (nptr) cudaFree(nptr);
+        if (nmid) cudaFree(nmid);
+        if (ncol) cudaFree(ncol);
+        if (nval) cudaFree(nval);
+        regions = nullptr;
+        rows = nptr = nmid = ncol = nullptr;
+        nval = nullptr;
+    }
+};
+
 struct exg_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -33,8 +65,11 @@ struct exg_ctx {
     double *l_val = nullptr, *u_val = nullptr, *u_diag = nullptr;
     int *row_perm = nullptr, *col_perm = nullptr, *l_order = nullptr, *u_order = nullptr;
     int2* tasks[4] = {nullptr, nullptr, nullptr, nullptr};  // L, U (EXACT), L, U (FAST)
+    TriPlan plan[2];  // FAST-mode runs of L and U
+    int cluster = 16;
     int n_tasks[4] = {0, 0, 0, 0};
     unsigned long long *trace_l = nullptr, *trace_u = nullptr;
+    unsigned long long *ntrace_l = nullptr, *ntrace_u = nullptr;
     // solve scratch: [2 tickets + pad (16 B)][y n][x n], memset to 0xFF per solve
     char* trsv_buf = nullptr;
     // n-vectors

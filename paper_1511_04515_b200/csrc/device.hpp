@@ -31,6 +31,26 @@ struct TrsvArgs {
     unsigned long long* trace;  // debug: per row (start, end) %globaltimer, or null
 };
 
+struct NarrowArgs {
+    const int2* regions;  // (first position, rows) per region of this run
+    int n_regions;
+    const int* rows;      // row id per level-order position (narrow runs)
+    const int* nptr;      // entry offsets per position
+    const int* nmid;      // first near entry per position (far entries come first)
+    const int* ncol;      // encoded: >= 0 far row id, < 0 -(1 + region slot)
+    const double* nval;
+    const double* in;
+    const int* in_perm;
+    const double* diag;
+    double* out;          // pivot-coordinate solution (global)
+    double* final_out;
+    const int* out_perm;
+    const double* add;
+    double coef;
+    const Ctrl* ctrl;
+    unsigned long long* trace;  // debug: per row (start, far done, end)
+};
+
 struct MgsArgs {
     int n;
     long long ldv;
@@ -67,6 +87,7 @@ void spmv(const Launch& L, const int* rowptr, const int* col, const double* val,
 void spmv_b2(const Launch& L, const int* rowptr, const int* col, const double* val, int n_rows,
              const double* u_k, const double* u_k1, double h, double* t1, double* t2);
 void trsv(const Launch& L, bool upper, bool reverse, const TrsvArgs& a);
+void trsv_narrow(const Launch& L, bool upper, const NarrowArgs& a, int cluster, size_t smem);
 void apply_weight(const Launch& L, const int* uptr, const int* ucol, const double* uval,
                   const double* udiag, const int* lptr, const int* lcol, const double* lval, int n,
                   const int* col_perm, const int* row_perm, const double* x, double* t,

@@ -4,8 +4,12 @@
 #include <cfloat>
 #include <climits>
 
+#include <cooperative_groups.h>
+
 #include "device.hpp"
 #include "kernels.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace exg {
 namespace dev {
@@ -213,15 +217,54 @@ __device__ __forceinline__ double load_ready(const double* p) {
     return __longlong_as_double(v);
 }
 
+// per-row operands of the epilogue, loaded when the row is taken (pinned so
+// the compiler cannot sink them behind the dependency polling)
+struct RowOps {
+    double b, dg, ad;
+    int qq;
+};
+
 template <bool UPPER>
-__device__ __forceinline__ void trsv_finish(const TrsvArgs& a, int r, double s) {
-    if (UPPER) s = s / a.diag[r];
+__device__ __forceinline__ RowOps row_ops(const TrsvArgs& a, int r) {
+    RowOps o;
+    o.b = UPPER ? a.in[r] : a.in[a.in_perm[r]];
+    o.dg = UPPER ? a.diag[r] : 1.0;
+    o.qq = a.final_out ? a.out_perm[r] : 0;
+    o.ad = (a.final_out && a.add) ? a.add[o.qq] : 0.0;
+    asm volatile("" : "+d"(o.b), "+d"(o.dg), "+r"(o.qq), "+d"(o.ad));
+    return o;
+}
+
+// Warp-uniform readiness wait for N entries per lane: entries whose cached
+// copy is the sentinel are re-read from L2 until every lane of the warp is
+// ready; no lane ever spins alone inside a divergent branch.
+template <int N>
+__device__ __forceinline__ void warp_wait_ready(const double* out, const int* cc, const int* kk,
+                                                int k1, double* y) {
+    bool rd = true;
+#pragma unroll
+    for (int q = 0; q < N; ++q)
+        rd = rd && !(kk[q] < k1 && __double_as_longlong(y[q]) == (long long)kSentinel);
+    while (!__all_sync(0xffffffffu, rd)) {
+        rd = true;
+#pragma unroll
+        for (int q = 0; q < N; ++q) {
+            if (kk[q] < k1 && __double_as_longlong(y[q]) == (long long)kSentinel) {
+                y[q] = __longlong_as_double(ld_relaxed(out + cc[q]));
+                rd = rd && __double_as_longlong(y[q]) != (long long)kSentinel;
+            }
+        }
+    }
+}
+
+template <bool UPPER>
+__device__ __forceinline__ void trsv_finish(const TrsvArgs& a, int r, double s, const RowOps& o) {
+    if (UPPER) s = s / o.dg;
     st_relaxed(a.out + r, s);
     if (a.final_out) {
-        const int q = a.out_perm[r];
         double y = a.coef * s;
-        if (a.add) y = a.add[q] + y;
-        a.final_out[q] = y;
+        if (a.add) y = o.ad + y;
+        a.final_out[o.qq] = y;
     }
 }
 
@@ -242,7 +285,8 @@ __global__ void __launch_bounds__(256)
         if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
         if (task.y & kTaskLong) {
             const int r = a.order[task.x];
-            const double b = UPPER ? a.in[r] : a.in[a.in_perm[r]];
+            const RowOps ops = row_ops<UPPER>(a, r);
+            const double b = ops.b;
             const int k0 = a.ptr[r], k1 = a.ptr[r + 1];
             double s = b;
             if (!FAST) {
@@ -274,24 +318,27 @@ __global__ void __launch_bounds__(256)
                     for (int q = 0; q < 4; ++q) v[q] = kk[q] < k1 ? a.val[kk[q]] : 0.0;
 #pragma unroll
                     for (int q = 0; q < 4; ++q) y[q] = kk[q] < k1 ? __ldca(a.out + a.col[kk[q]]) : 0.0;
+                    int cc[4];
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        if (kk[q] < k1 && __double_as_longlong(y[q]) == (long long)kSentinel)
-                            y[q] = load_ready(a.out + a.col[kk[q]]);
-                        acc += v[q] * y[q];
-                    }
+                    for (int q = 0; q < 4; ++q) cc[q] = kk[q] < k1 ? a.col[kk[q]] : 0;
+                    warp_wait_ready<4>(a.out, cc, kk, k1, y);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) acc += v[q] * y[q];
                 }
                 for (; ci < nch; ++ci) {
                     const int ch = UPPER ? nch - 1 - ci : ci;
-                    const int k = k0 + ch * 32 + lane;
-                    if (k < k1) acc += a.val[k] * load_ready(a.out + a.col[k]);
+                    int kk[1] = {k0 + ch * 32 + lane};
+                    int cc[1] = {kk[0] < k1 ? a.col[kk[0]] : 0};
+                    double y[1] = {kk[0] < k1 ? __ldca(a.out + cc[0]) : 0.0};
+                    warp_wait_ready<1>(a.out, cc, kk, k1, y);
+                    if (kk[0] < k1) acc += a.val[kk[0]] * y[0];
                 }
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
                 s = b - acc;
             }
             if (lane == 0) {
-                trsv_finish<UPPER>(a, r, s);
+                trsv_finish<UPPER>(a, r, s, ops);
                 if (a.trace) {
                     unsigned long long t_end;
                     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
@@ -307,9 +354,11 @@ __global__ void __launch_bounds__(256)
             const bool active = seg < cnt;
             int r = 0;
             double b = 0.0, acc = 0.0, s = 0.0;
+            RowOps ops{0.0, 1.0, 0.0, 0};
             if (active) {
                 r = a.order[task.x + seg];
-                b = UPPER ? a.in[r] : a.in[a.in_perm[r]];
+                ops = row_ops<UPPER>(a, r);
+                b = ops.b;
                 const int k0 = a.ptr[r], k1 = a.ptr[r + 1];
                 if (lpr == 1) {
                     // one lane per row, the reference's order (U reversed in FAST)
@@ -345,6 +394,7 @@ __global__ void __launch_bounds__(256)
                         const int k = k0 + sl + (j << lg);
                         acc += a.val[k] * load_ready(a.out + a.col[k]);
                     }
+                    (void)0;
                 }
             }
             if (lpr > 1) {
@@ -352,7 +402,7 @@ __global__ void __launch_bounds__(256)
                 s = b - acc;
             }
             if (active && sl == 0) {
-                trsv_finish<UPPER>(a, r, s);
+                trsv_finish<UPPER>(a, r, s, ops);
                 if (a.trace) {
                     unsigned long long t_end;
                     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
@@ -361,6 +411,167 @@ __global__ void __launch_bounds__(256)
                 }
             }
         }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Narrow levels (few rows per level: the dense separator chains at the end
+// of L and the start of U) on ONE thread-block cluster with
+// distributed-shared-memory hand-offs (FAST mode).
+//
+// The host cuts each run of narrow levels into regions of <= cap
+// consecutive level-order positions.  Every CTA of the cluster holds a
+// replica of the region's solution values in shared memory (sentinel-
+// initialised); a row's result is pushed into all replicas with DSMEM stores
+// (one lane per CTA) and dependents poll their LOCAL shared memory, so a
+// level hand-off costs a DSMEM store + a local load instead of an L2 round
+// trip.  Dependencies outside the region (earlier regions / launches) are
+// final and read from global memory (L2, never a stale L1 line).  The host
+// re-encodes each row: far entries first (col >= 0), then near entries by
+// increasing region slot (col = -1 - slot), so every lane meets the newest
+// dependencies last.  Warp w of the cluster takes positions w, w+W, ... of the
+// region (a position only waits on smaller positions: no deadlock).
+// ---------------------------------------------------------------------------
+#ifndef EXG_SPIN_NS
+#define EXG_SPIN_NS 0
+#endif
+#ifndef EXG_NARROW_THREADS
+#define EXG_NARROW_THREADS 256
+#endif
+template <bool UPPER>
+__global__ void __launch_bounds__(EXG_NARROW_THREADS, 1)
+    k_trsv_narrow(NarrowArgs a) {
+    extern __shared__ double yrep[];
+    cg::cluster_group cl = cg::this_cluster();
+    if (a.ctrl && (a.ctrl->converged || a.ctrl->status)) return;
+    const unsigned FULL = 0xffffffffu;
+    const int rank = (int)cl.block_rank();
+    const int cs = (int)cl.num_blocks();
+    const int lane = threadIdx.x & 31;
+    const int nw = blockDim.x >> 5;
+    const int gw = rank * nw + (threadIdx.x >> 5);
+    const int wt = cs * nw;
+    unsigned long long* ybits = reinterpret_cast<unsigned long long*>(yrep);
+    volatile double* yv = yrep;
+    constexpr int NB = 4;  // near entries per lane per chunk (chunk = 128 entries)
+    for (int reg = 0; reg < a.n_regions; ++reg) {
+        const int2 R = a.regions[reg];
+        for (int i = threadIdx.x; i < R.y; i += blockDim.x) ybits[i] = kSentinel;
+        cl.sync();
+        for (int q = gw; q < R.y; q += wt) {
+            const int p = R.x + q;
+            const int r = a.rows[p];
+            unsigned long long t_start = 0, t_far = 0;
+            if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+            const int k0 = a.nptr[p], km = a.nmid[p], k1 = a.nptr[p + 1];
+            double b = UPPER ? a.in[r] : a.in[a.in_perm[r]];
+            double dg = UPPER ? a.diag[r] : 1.0;
+            int qq = a.final_out ? a.out_perm[r] : 0;
+            double ad = (a.final_out && a.add) ? a.add[qq] : 0.0;
+            // keep these loads here: the compiler would otherwise sink them
+            // past the polling loop, onto the critical path of the hand-off
+            asm volatile("" : "+d"(b), "+d"(dg), "+r"(qq), "+d"(ad));
+            double acc = 0.0;
+            // far entries: final values, independent loads (4 in flight per lane)
+            int k = k0 + lane;
+            for (; k + 96 < km; k += 128) {
+                int c[4];
+                double v[4], y[4];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    c[t] = a.ncol[k + 32 * t];
+                    v[t] = a.nval[k + 32 * t];
+                }
+#pragma unroll
+                for (int t = 0; t < 4; ++t) y[t] = __ldca(a.out + c[t]);
+#pragma unroll
+                for (int t = 0; t < 4; ++t) acc += v[t] * y[t];
+            }
+            for (; k < km; k += 32) acc += a.nval[k] * __ldca(a.out + a.ncol[k]);
+            // near entries (region slots, newest last): the next chunk's
+            // (slot, value) pairs are loaded while this chunk polls shared memory
+            int cs_[NB], ns_[NB];
+            double cv_[NB], nv_[NB];
+            int base = km;
+#pragma unroll
+            for (int t = 0; t < NB; ++t) {
+                const int kk = base + lane + 32 * t;
+                cs_[t] = kk < k1 ? -1 - a.ncol[kk] : -1;
+                cv_[t] = kk < k1 ? a.nval[kk] : 0.0;
+            }
+            while (base < k1) {
+                const int nb = base + 32 * NB;
+#pragma unroll
+                for (int t = 0; t < NB; ++t) {
+                    const int kk = nb + lane + 32 * t;
+                    ns_[t] = kk < k1 ? -1 - a.ncol[kk] : -1;
+                    nv_[t] = kk < k1 ? a.nval[kk] : 0.0;
+                }
+                // warp-uniform wait: every lane re-polls its not-yet-ready
+                // entries until the whole warp is ready (a lane spinning alone
+                // costs ~1 us of reconvergence per hand-off)
+                double yy[NB];
+                bool rd = true;
+#pragma unroll
+                for (int t = 0; t < NB; ++t) {
+                    yy[t] = cs_[t] >= 0 ? yv[cs_[t]] : 0.0;
+                    rd = rd && !(cs_[t] >= 0 && __double_as_longlong(yy[t]) == (long long)kSentinel);
+                }
+                while (!__all_sync(FULL, rd)) {
+                    rd = true;
+#pragma unroll
+                    for (int t = 0; t < NB; ++t) {
+                        if (cs_[t] >= 0 && __double_as_longlong(yy[t]) == (long long)kSentinel) {
+                            yy[t] = yv[cs_[t]];
+                            rd = rd && __double_as_longlong(yy[t]) != (long long)kSentinel;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int t = 0; t < NB; ++t)
+                    if (cs_[t] >= 0) acc += cv_[t] * yy[t];
+#pragma unroll
+                for (int t = 0; t < NB; ++t) {
+                    cs_[t] = ns_[t];
+                    cv_[t] = nv_[t];
+                }
+                base = nb;
+            }
+            if (a.trace) {
+                __syncwarp();
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_far));
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
+            double s = b - acc;
+            if (UPPER) s = s / dg;
+            unsigned long long sb = __double_as_longlong(s);
+            if (sb == kSentinel) sb = kCanonNaN;
+            if (lane < cs) {
+                // DSMEM store into replica `lane` (explicit shared::cluster: a
+                // volatile generic store would compile to a system-scope store)
+                const unsigned laddr = (unsigned)__cvta_generic_to_shared(yrep + q);
+                unsigned raddr;
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(laddr), "r"(lane));
+                asm volatile("st.relaxed.cluster.shared::cluster.b64 [%0], %1;" ::"r"(raddr), "l"(sb) : "memory");
+            }
+            if (lane == 0) {
+                st_relaxed(a.out + r, s);
+                if (a.final_out) {
+                    double y = a.coef * s;
+                    if (a.add) y = ad + y;
+                    a.final_out[qq] = y;
+                }
+                if (a.trace) {
+                    unsigned long long t_end;
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+                    a.trace[3 * r] = t_start;
+                    a.trace[3 * r + 1] = t_far;
+                    a.trace[3 * r + 2] = t_end;
+                }
+            }
+        }
+        cl.sync();
     }
 }
 
@@ -1397,6 +1608,33 @@ void apply_weight(const Launch& L, const int* uptr, const int* ucol, const doubl
     k_apply_l2<<<cdiv(n, 256), 256, 0, L.stream>>>(lptr, lcol, lval, n, t, y_out, row_perm,
                                                   partials, done, ctrl, weight_out);
     count(L, 2);
+}
+
+void trsv_narrow(const Launch& L, bool upper, const NarrowArgs& a, int cluster, size_t smem) {
+    static bool attr[2] = {false, false};
+    auto fn = upper ? (void*)k_trsv_narrow<true> : (void*)k_trsv_narrow<false>;
+    if (!attr[upper]) {
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        attr[upper] = true;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(cluster);
+    cfg.blockDim = dim3(EXG_NARROW_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = L.stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cluster;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (upper)
+        cudaLaunchKernelEx(&cfg, k_trsv_narrow<true>, a);
+    else
+        cudaLaunchKernelEx(&cfg, k_trsv_narrow<false>, a);
+    count(L);
 }
 
 void apply_tasks(const Launch& L, const int2* utasks, int n_utasks, const int* uorder,

@@ -14,7 +14,7 @@ c.set_system(s); c.set_factors(f)
 b = np.random.default_rng(0).uniform(-1, 1, s.n)
 for _ in range(3):
     c.solve(b)
-t = np.zeros(4 * s.n, np.uint64)
+t = np.zeros(10 * s.n, np.uint64)
 c._check(F.lib.exg_debug_trace_solve(c.handle, b.ctypes.data_as(C.POINTER(C.c_double)), t.ctypes.data_as(C.POINTER(C.c_uint64))))
 np.savez(f"gpurun_out/trace_{W}_{mode}.npz", t=t)
 n = s.n

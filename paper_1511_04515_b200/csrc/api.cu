@@ -204,9 +204,15 @@ void solve_dev(exg_ctx* c, const double* b, double* final_out, double coef, cons
                     if (run.b <= run.a) continue;
                     a.tasks = tasks + run.a;
                     a.n_tasks = run.b - run.a;
-                    if (next_ticket >= kMaxTickets) throw ApiError{EXG_E_CONTRACT, "too many solve runs"};
-                    a.ticket = tickets + next_ticket++;
-                    exg::dev::trsv(c->L(), upper, true, a);
+                    a.meta = c->meta[tri];
+                    static const bool v2 = getenv("EXG_WIDE_V2") != nullptr;
+                    if (v2) {
+                        if (next_ticket >= kMaxTickets) throw ApiError{EXG_E_CONTRACT, "too many solve runs"};
+                        a.ticket = tickets + next_ticket++;
+                        exg::dev::trsv(c->L(), upper, true, a);
+                    } else {
+                        exg::dev::trsv_wide(c->L(), upper, a);
+                    }
                 } else {
                     exg::dev::NarrowArgs na{};
                     na.regions = P.regions + run.a;
@@ -391,7 +397,7 @@ void plan_triangle(exg_ctx* c, TriPlan& P, bool upper_tri, const std::vector<int
     P.runs.clear();
     const char* env_t = getenv(upper_tri ? "EXG_NARROW_T_U" : "EXG_NARROW_T_L");
     if (!env_t) env_t = getenv("EXG_NARROW_T");
-    const int T = env_t ? atoi(env_t) : (upper_tri ? 8 : 32);
+    const int T = env_t ? atoi(env_t) : (upper_tri ? 8 : 16);
     const char* env_r = getenv("EXG_ABSORB_ROWS");
     const long long absorb_rows = env_r ? atoll(env_r) : 8192;
     const int CAP = TriPlan::kCap;
@@ -554,6 +560,8 @@ void exg_destroy(exg_ctx* c) {
         if (c->tasks[q]) cudaFree(c->tasks[q]);
     c->plan[0].free_dev();
     c->plan[1].free_dev();
+    if (c->meta[0]) cudaFree(c->meta[0]);
+    if (c->meta[1]) cudaFree(c->meta[1]);
     if (c->bar) cudaFree(c->bar);
     if (c->done) cudaFree(c->done);
     if (c->ctrl) cudaFree(c->ctrl);
@@ -731,6 +739,21 @@ exg_status exg_set_factors(exg_ctx* c, int n, const int* Lp, const int* Li, cons
     const int lnl = l_levels, unl = u_levels;
     plan_triangle(c, c->plan[0], false, lord, llev, lnl, lp, lc, lv, ltasks_f);
     plan_triangle(c, c->plan[1], true, uord, lev, unl, up, uc, uv, utasks_f);
+    {
+        std::vector<int4> lm(n), um(n);
+        for (int p = 0; p < n; ++p) {
+            const int r = lord[p];
+            lm[p] = make_int4(r, row_perm[r], lp[r], lp[r + 1]);
+            const int ru = uord[p];
+            um[p] = make_int4(ru, ru, up[ru], up[ru + 1]);
+        }
+        if (c->meta[0]) cudaFree(c->meta[0]);
+        if (c->meta[1]) cudaFree(c->meta[1]);
+        c->meta[0] = dalloc<int4>(n);
+        c->meta[1] = dalloc<int4>(n);
+        ck(cudaMemcpy(c->meta[0], lm.data(), n * sizeof(int4), cudaMemcpyHostToDevice), "meta");
+        ck(cudaMemcpy(c->meta[1], um.data(), n * sizeof(int4), cudaMemcpyHostToDevice), "meta");
+    }
     const std::vector<int2>* tl[4] = {&ltasks, &utasks, &ltasks_f, &utasks_f};
     for (int q = 0; q < 4; ++q) {
         if (c->tasks[q]) cudaFree(c->tasks[q]);

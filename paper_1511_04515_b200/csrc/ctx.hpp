@@ -66,6 +66,7 @@ struct exg_ctx {
     int *row_perm = nullptr, *col_perm = nullptr, *l_order = nullptr, *u_order = nullptr;
     int2* tasks[4] = {nullptr, nullptr, nullptr, nullptr};  // L, U (EXACT), L, U (FAST)
     TriPlan plan[2];  // FAST-mode runs of L and U
+    int4* meta[2] = {nullptr, nullptr};  // level-order row metadata of L and U
     int cluster = 16;
     int n_tasks[4] = {0, 0, 0, 0};
     unsigned long long *trace_l = nullptr, *trace_u = nullptr;

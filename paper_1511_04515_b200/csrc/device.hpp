@@ -29,6 +29,7 @@ struct TrsvArgs {
     const int2* tasks;  // warp tasks in level order (v2 kernel); null = v1
     int n_tasks;
     unsigned long long* trace;  // debug: per row (start, end) %globaltimer, or null
+    const int4* meta;   // v3: per level-order position {row, b index, k0, k1}
 };
 
 struct NarrowArgs {
@@ -88,6 +89,7 @@ void spmv_b2(const Launch& L, const int* rowptr, const int* col, const double* v
              const double* u_k, const double* u_k1, double h, double* t1, double* t2);
 void trsv(const Launch& L, bool upper, bool reverse, const TrsvArgs& a);
 void trsv_narrow(const Launch& L, bool upper, const NarrowArgs& a, int cluster, size_t smem);
+void trsv_wide(const Launch& L, bool upper, const TrsvArgs& a);
 void apply_weight(const Launch& L, const int* uptr, const int* ucol, const double* uval,
                   const double* udiag, const int* lptr, const int* lcol, const double* lval, int n,
                   const int* col_perm, const int* row_perm, const double* x, double* t,

@@ -415,6 +415,134 @@ __global__ void __launch_bounds__(256)
 }
 
 // ---------------------------------------------------------------------------
+// v3 (FAST): wide levels, cooperative persistent grid with STATIC task
+// assignment (task t -> warp t mod W; all warps co-resident, each runs its
+// tasks in increasing order, a task only waits on smaller tasks: no
+// deadlock, no ticket atomics).  Per-position metadata is precomputed in level
+// order (meta[p] = {row, b index, k0, k1}), and the next task's metadata is
+// loaded while the current task runs, so a task's fixed latency is off the
+// critical path.  Every wait is warp-uniform.
+// ---------------------------------------------------------------------------
+template <bool UPPER>
+__global__ void __launch_bounds__(256)
+    k_trsv3(TrsvArgs a) {
+    if (a.ctrl && (a.ctrl->converged || a.ctrl->status)) return;
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int W = gridDim.x * (blockDim.x >> 5);
+    int t = gw;
+    if (t >= a.n_tasks) return;
+    // metadata of the current task (per lane: its row in a group task)
+    auto load_meta = [&](int tt, int2& task, int4& m, double& b) {
+        task = a.tasks[tt];
+        const bool lng = task.y & kTaskLong;
+        const int lg = lng ? 5 : ((task.y >> 8) & 0x7);
+        const int seg = lng ? 0 : (lane >> lg);
+        const int cnt = lng ? 1 : (task.y & 0xFF);
+        if (seg < cnt) {
+            m = a.meta[task.x + seg];
+            b = a.in[m.y];
+        } else {
+            m = make_int4(0, 0, 0, 0);
+            b = 0.0;
+        }
+    };
+    int2 task, ntask;
+    int4 m, nm;
+    double b, nb;
+    load_meta(t, task, m, b);
+    while (true) {
+        const int tn = t + W;
+        if (tn < a.n_tasks) load_meta(tn, ntask, nm, nb);  // prefetch
+        const bool lng = task.y & kTaskLong;
+        const int r = m.x, k0 = m.z, k1 = m.w;
+        double acc = 0.0;
+        if (lng) {
+            const int nch = (k1 - k0 + 31) >> 5;
+            int ci = 0;
+            for (; ci < nch; ci += 4) {
+                int kk[4], cc[4];
+                double v[4], y[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int ch = UPPER ? nch - 1 - (ci + q) : ci + q;  // U: newest last
+                    kk[q] = (ci + q < nch) ? k0 + ch * 32 + lane : k1;
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    cc[q] = kk[q] < k1 ? a.col[kk[q]] : 0;
+                    v[q] = kk[q] < k1 ? a.val[kk[q]] : 0.0;
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) y[q] = kk[q] < k1 ? __ldca(a.out + cc[q]) : 0.0;
+                warp_wait_ready<4>(a.out, cc, kk, k1, y);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc += v[q] * y[q];
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
+            if (lane == 0) {
+                double s = b - acc;
+                if (UPPER) s = s / a.diag[r];
+                st_relaxed(a.out + r, s);
+                if (a.final_out) {
+                    const int qq = a.out_perm[r];
+                    double yv = a.coef * s;
+                    if (a.add) yv = a.add[qq] + yv;
+                    a.final_out[qq] = yv;
+                }
+            }
+        } else {
+            const int cnt = task.y & 0xFF;
+            const int lg = (task.y >> 8) & 0x7;
+            const int lpr = 1 << lg;
+            const int seg = lane >> lg, sl = lane & (lpr - 1);
+            const bool active = seg < cnt;
+            const int nj = active ? (k1 - k0 - sl + lpr - 1) >> lg : 0;
+            const int njmax = __reduce_max_sync(FULL, nj);
+            for (int j0 = 0; j0 < njmax; j0 += 4) {
+                int kk[4], cc[4];
+                double v[4], y[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int jj = j0 + q;
+                    const int j = UPPER ? nj - 1 - jj : jj;  // U: newest last
+                    kk[q] = jj < nj ? k0 + sl + (j << lg) : k1;
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    cc[q] = kk[q] < k1 ? a.col[kk[q]] : 0;
+                    v[q] = kk[q] < k1 ? a.val[kk[q]] : 0.0;
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) y[q] = kk[q] < k1 ? __ldca(a.out + cc[q]) : 0.0;
+                warp_wait_ready<4>(a.out, cc, kk, k1, y);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc += v[q] * y[q];
+            }
+            for (int o = lpr >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
+            if (active && sl == 0) {
+                double s = b - acc;
+                if (UPPER) s = s / a.diag[r];
+                st_relaxed(a.out + r, s);
+                if (a.final_out) {
+                    const int qq = a.out_perm[r];
+                    double yv = a.coef * s;
+                    if (a.add) yv = a.add[qq] + yv;
+                    a.final_out[qq] = yv;
+                }
+            }
+        }
+        if (tn >= a.n_tasks) return;
+        t = tn;
+        task = ntask;
+        m = nm;
+        b = nb;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Narrow levels (few rows per level: the dense separator chains at the end
 // of L and the start of U) on ONE thread-block cluster with
 // distributed-shared-memory hand-offs (FAST mode).
@@ -1608,6 +1736,27 @@ void apply_weight(const Launch& L, const int* uptr, const int* ucol, const doubl
     k_apply_l2<<<cdiv(n, 256), 256, 0, L.stream>>>(lptr, lcol, lval, n, t, y_out, row_perm,
                                                   partials, done, ctrl, weight_out);
     count(L, 2);
+}
+
+template <bool U>
+static int trsv3_occ() {
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_trsv3<U>, 256, 0);
+    return occ > 0 ? occ : 1;
+}
+
+void trsv_wide(const Launch& L, bool upper, const TrsvArgs& a) {
+    if (a.n_tasks <= 0) return;
+    static int occ[2] = {0, 0};
+    if (!occ[upper]) occ[upper] = upper ? trsv3_occ<true>() : trsv3_occ<false>();
+    const long long warps = (long long)L.num_sms * occ[upper] * 8;
+    const unsigned int grid = (unsigned int)std::max<long long>(
+        1, std::min<long long>((long long)L.num_sms * occ[upper], ((long long)a.n_tasks + 7) / 8));
+    (void)warps;
+    void* args[] = {(void*)&a};
+    cudaLaunchCooperativeKernel(upper ? (void*)k_trsv3<true> : (void*)k_trsv3<false>, dim3(grid),
+                                dim3(256), args, 0, L.stream);
+    count(L);
 }
 
 void trsv_narrow(const Launch& L, bool upper, const NarrowArgs& a, int cluster, size_t smem) {

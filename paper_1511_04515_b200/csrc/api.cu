@@ -155,10 +155,12 @@ const DCsr& mat(exg_ctx* c, int which) {
 void solve_dev(exg_ctx* c, const double* b, double* final_out, double coef, const double* add,
                const Ctrl* ctrl) {
     const int n = c->n;
-    ck(cudaMemsetAsync(c->trsv_buf, 0xFF, kTrsvHdr + 2 * sizeof(double) * (size_t)n, c->stream), "memset");
+    ck(cudaMemsetAsync(c->trsv_buf, 0xFF, kTrsvHdr + 6 * sizeof(double) * (size_t)n, c->stream), "memset");
     unsigned int* tickets = reinterpret_cast<unsigned int*>(c->trsv_buf);
     double* y = reinterpret_cast<double*>(c->trsv_buf + kTrsvHdr);
     double* x = y + n;
+    double* sbuf_dev = x + n;     // chain runs' s vectors (L and U: <= n each... shared)
+    double* pbuf_dev = x + 3 * n;  // chain runs' old partial sums
     const bool fast = c->opt.trsv_mode == EXG_TRSV_FAST;
     const int fq = fast ? 2 : 0;
     int next_ticket = 0;
@@ -200,6 +202,35 @@ void solve_dev(exg_ctx* c, const double* b, double* final_out, double coef, cons
                     cudaEventRecord(e, c->stream);
                     rev.push_back(e);
                 }
+                if (run.narrow == 2) {
+                    const TriPlan::Chain& ch = P.chains[run.a];
+                    exg::dev::ChainArgs ca{};
+                    ca.n_rows = ch.n_rows;
+                    ca.n_blocks = ch.n_blocks;
+                    ca.rows = P.crows + ch.rows_off;
+                    ca.nptr = P.cnptr + ch.nptr_off;
+                    ca.ncol = P.cncol + ch.ent0;
+                    ca.nval = P.cnval + ch.ent0;
+                    ca.blocks = P.cblocks + 3 * (long long)ch.blk0;
+                    ca.pool = P.pool;
+                    ca.s = sbuf_dev;
+                    ca.part = pbuf_dev;
+                    ca.wtasks = P.ctasks + ch.task0;
+                    ca.n_tasks = ch.ntasks;
+                    ca.in = a.in;
+                    ca.in_perm = a.in_perm;
+                    ca.out = a.out;
+                    ca.final_out = a.final_out;
+                    ca.out_perm = a.out_perm;
+                    ca.add = a.add;
+                    ca.coef = a.coef;
+                    ca.ctrl = ctrl;
+                    ca.trace = upper ? c->ntrace_u : c->ntrace_l;
+                    exg::dev::trsv_chain(c->L(), upper, ca);
+                    sbuf_dev += ch.n_rows;
+                    pbuf_dev += ch.n_rows;
+                    continue;
+                }
                 if (!run.narrow) {
                     if (run.b <= run.a) continue;
                     a.tasks = tasks + run.a;
@@ -232,7 +263,10 @@ void solve_dev(exg_ctx* c, const double* b, double* final_out, double coef, cons
                     na.coef = a.coef;
                     na.ctrl = ctrl;
                     na.trace = upper ? c->ntrace_u : c->ntrace_l;
-                    exg::dev::trsv_narrow(c->L(), upper, na, c->cluster, P.smem);
+                    na.regions4 = P.regions4 + run.a;
+                    na.blocks = P.blocks;
+                    na.pool = P.pool;
+                    exg::dev::trsv_blk(c->L(), upper, na, c->cluster, P.smem);
                 }
             }
             if (run_timing) {
@@ -391,7 +425,7 @@ void deliver(exg_ctx* c, double* user, const double* dev, size_t count, int ptr_
 void plan_triangle(exg_ctx* c, TriPlan& P, bool upper_tri, const std::vector<int>& ord,
                    const std::vector<int>& level, int nl, const std::vector<int>& ptr,
                    const std::vector<int>& col, const std::vector<double>& val,
-                   const std::vector<int2>& tasks) {
+                   const std::vector<int2>& tasks, const std::vector<double>* udiag) {
     const int n = (int)ord.size();
     P.free_dev();
     P.runs.clear();
@@ -410,8 +444,24 @@ void plan_triangle(exg_ctx* c, TriPlan& P, bool upper_tri, const std::vector<int
     std::vector<int> pos_of(n);
     for (int p = 0; p < n; ++p) pos_of[ord[p]] = p;
     std::vector<int2> regions;
+    std::vector<int4> regions4, blocks;
+    struct ChainRun {
+        int pos0, rows, blk0, nblocks, ent0, task0 = 0, ntasks = 0;
+    };
+    std::vector<int4> ctasks;
+    const char* ko = getenv("EXG_CHAIN_OLD");
+    const int kOld = ko ? atoi(ko) : 8;
+    std::vector<ChainRun> cruns;
+    std::vector<int> crows, cnptr, cncol;
+    std::vector<int4> cblocks;
+    std::vector<double> cnval;
+    const char* nm = getenv("EXG_NARROW_MODE");
+    const bool chain_mode = !nm || std::string(nm) == "chain";
     std::vector<int> rows, nptr{0}, nmid, ncol;
-    std::vector<double> nval;
+    std::vector<double> nval, pool;
+    constexpr int kB = 64;
+    std::vector<double> Dm(kB * kB), Em(kB * kB), E2(kB * kB), Di(kB * kB), Fm(kB * kB);
+    auto diag_of = [&](int r) { return udiag ? (*udiag)[r] : 1.0; };
     // level classes, then absorb short wide stretches into the narrow runs
     // (a launch costs more than a few fat levels on the cluster)
     std::vector<char> is_narrow(nl);
@@ -437,32 +487,186 @@ void plan_triangle(exg_ctx* c, TriPlan& P, bool upper_tri, const std::vector<int
         if (!narrow) {
             run.a = tfirst[l];
             run.b = tfirst[l1];
+        } else if (chain_mode) {
+            // chain + workers: blocks of kB positions over the whole run
+            run.narrow = 2;
+            run.a = (int)cruns.size();
+            const int p0 = lpos[l], pc = lpos[l1] - lpos[l];
+            ChainRun cr;
+            cr.pos0 = (int)crows.size();
+            cnptr.push_back(0);  // leading 0 of this run's row offsets (cnptr index = pos0 + run index)
+            cr.rows = pc;
+            cr.blk0 = (int)cblocks.size() / 3;
+            cr.ent0 = (int)cncol.size();
+            const int nblk = (pc + kB - 1) / kB;
+            cr.nblocks = nblk;
+            std::vector<std::pair<int, int4>> wt;  // (start block, task)
+            for (int kb = 0; kb < nblk; ++kb) {
+                const int bs = p0 + kb * kB;
+                const int bc = std::min(kB, p0 + pc - bs);
+                const int ps1 = kb >= 1 ? bs - kB : bs;
+                const int ps2 = kb >= 2 ? bs - 2 * kB : ps1;
+                std::fill(Dm.begin(), Dm.end(), 0.0);
+                std::fill(Em.begin(), Em.end(), 0.0);
+                std::fill(E2.begin(), E2.end(), 0.0);
+                bool d_ident = true, e1_zero = true, e2_zero = true;
+                const int pso = kb >= kOld ? bs - kOld * kB : p0;  // first position of block k-8
+                for (int i = 0; i < bc; ++i) {
+                    const int p = bs + i;
+                    const int r = ord[p];
+                    crows.push_back(r);
+                    Dm[i * kB + i] = diag_of(r);
+                    if (Dm[i * kB + i] != 1.0) d_ident = false;
+                    std::vector<std::pair<int, double>> oldv, recv;
+                    for (int k = ptr[r]; k < ptr[r + 1]; ++k) {
+                        const int pq = pos_of[col[k]];
+                        if (pq < pso) {
+                            oldv.push_back({col[k], val[k]});
+                        } else if (pq < ps2) {
+                            recv.push_back({col[k], val[k]});
+                        } else if (pq < ps1) {
+                            E2[i * kB + (pq - ps2)] = val[k];
+                            e2_zero = false;
+                        } else if (pq < bs) {
+                            Em[i * kB + (pq - ps1)] = val[k];
+                            e1_zero = false;
+                        } else {
+                            Dm[i * kB + (pq - bs)] = val[k];
+                            d_ident = false;
+                        }
+                    }
+                    const int pl = (int)crows.size() - 1 - cr.pos0;  // run-local position
+                    const int e0 = (int)cncol.size() - cr.ent0;
+                    for (auto& e : oldv) {
+                        cncol.push_back(e.first);
+                        cnval.push_back(e.second);
+                    }
+                    const int e1 = (int)cncol.size() - cr.ent0;
+                    for (auto& e : recv) {
+                        cncol.push_back(e.first);
+                        cnval.push_back(e.second);
+                    }
+                    const int e2 = (int)cncol.size() - cr.ent0;
+                    const bool has_old = e1 > e0;
+                    if (has_old) wt.push_back({std::max(0, kb - kOld - 1), make_int4(pl, e0, e1, 0)});
+                    wt.push_back({std::max(0, kb - 3), make_int4(pl, e1, e2, 1 | (has_old ? 2 : 0))});
+                    cnptr.push_back(e2);
+                }
+                std::fill(Di.begin(), Di.end(), 0.0);
+                for (int jc = 0; jc < bc; ++jc)
+                    for (int i = jc; i < bc; ++i) {
+                        double sacc = (i == jc) ? 1.0 : 0.0;
+                        for (int m2 = jc; m2 < i; ++m2) sacc -= Dm[i * kB + m2] * Di[m2 * kB + jc];
+                        Di[i * kB + jc] = sacc / Dm[i * kB + i];
+                    }
+                auto push_mat = [&](const std::vector<double>& M) {
+                    const int o = (int)pool.size();
+                    pool.insert(pool.end(), M.begin(), M.end());
+                    return o;
+                };
+                auto times_dinv = [&](const std::vector<double>& E) {
+                    std::fill(Fm.begin(), Fm.end(), 0.0);
+                    for (int i = 0; i < bc; ++i)
+                        for (int j = 0; j < kB; ++j) {
+                            double sacc = 0.0;
+                            for (int m2 = 0; m2 <= i; ++m2) sacc += Di[i * kB + m2] * E[m2 * kB + j];
+                            Fm[i * kB + j] = sacc;
+                        }
+                    return push_mat(Fm);
+                };
+                const int dofs = d_ident ? -1 : push_mat(Di);
+                const int f1 = e1_zero ? -1 : times_dinv(Em);
+                const int f2 = e2_zero ? -1 : times_dinv(E2);
+                cblocks.push_back(make_int4(kb * kB, bc, 0, 0));
+                cblocks.push_back(make_int4(dofs, f1, f2, 0));
+                cblocks.push_back(make_int4(0, 0, 0, 0));
+            }
+            std::stable_sort(wt.begin(), wt.end(),
+                             [](const std::pair<int, int4>& x, const std::pair<int, int4>& y) { return x.first < y.first; });
+            cr.task0 = (int)ctasks.size();
+            for (auto& w : wt) ctasks.push_back(w.second);
+            cr.ntasks = (int)wt.size();
+            cruns.push_back(cr);
+            run.b = run.a + 1;
         } else {
             run.a = (int)regions.size();
             for (int p0 = lpos[l]; p0 < lpos[l1]; p0 += CAP) {
                 const int pc = std::min(CAP, lpos[l1] - p0);
                 const int np0 = (int)rows.size();
+                const int nblk = (pc + kB - 1) / kB;
                 regions.push_back(make_int2(np0, pc));
-                for (int p = p0; p < p0 + pc; ++p) {
-                    const int r = ord[p];
-                    rows.push_back(r);
-                    std::vector<std::pair<int, int>> near;  // (slot, k)
-                    for (int k = ptr[r]; k < ptr[r + 1]; ++k) {
-                        const int pc_ = pos_of[col[k]];
-                        if (pc_ >= p0 && pc_ < p)
-                            near.push_back({pc_ - p0, k});
-                        else {
-                            ncol.push_back(col[k]);
-                            nval.push_back(val[k]);
+                regions4.push_back(make_int4(np0, pc, (int)blocks.size() / 3, nblk));
+                for (int kb = 0; kb < nblk; ++kb) {
+                    const int bs = p0 + kb * kB;                 // first position of the block
+                    const int bc = std::min(kB, p0 + pc - bs);   // rows
+                    const int ps1 = kb >= 1 ? bs - kB : bs;       // first position of block k-1
+                    const int ps2 = kb >= 2 ? bs - 2 * kB : ps1;  // first position of block k-2
+                    std::fill(Dm.begin(), Dm.end(), 0.0);
+                    std::fill(Em.begin(), Em.end(), 0.0);
+                    std::fill(E2.begin(), E2.end(), 0.0);
+                    bool d_ident = true, e1_zero = true, e2_zero = true;
+                    for (int i = 0; i < bc; ++i) {
+                        const int p = bs + i;
+                        const int r = ord[p];
+                        rows.push_back(r);
+                        Dm[i * kB + i] = diag_of(r);
+                        if (Dm[i * kB + i] != 1.0) d_ident = false;
+                        std::vector<std::pair<int, int>> near;  // (slot, k)
+                        for (int k = ptr[r]; k < ptr[r + 1]; ++k) {
+                            const int pq = pos_of[col[k]];
+                            if (pq < p0) {  // earlier region / launch: global
+                                ncol.push_back(col[k]);
+                                nval.push_back(val[k]);
+                            } else if (pq < ps2) {  // this region, blocks <= k-3
+                                near.push_back({pq - p0, k});
+                            } else if (pq < ps1) {  // block k-2 -> E2
+                                E2[i * kB + (pq - ps2)] = val[k];
+                                e2_zero = false;
+                            } else if (pq < bs) {  // block k-1 -> E1
+                                Em[i * kB + (pq - ps1)] = val[k];
+                                e1_zero = false;
+                            } else {  // inside the block -> D
+                                Dm[i * kB + (pq - bs)] = val[k];
+                                d_ident = false;
+                            }
                         }
+                        std::sort(near.begin(), near.end());
+                        nmid.push_back((int)ncol.size());
+                        for (auto& e : near) {
+                            ncol.push_back(-1 - e.first);
+                            nval.push_back(val[e.second]);
+                        }
+                        nptr.push_back((int)ncol.size());
                     }
-                    std::sort(near.begin(), near.end());
-                    nmid.push_back((int)ncol.size());
-                    for (auto& e : near) {
-                        ncol.push_back(-1 - e.first);
-                        nval.push_back(val[e.second]);
-                    }
-                    nptr.push_back((int)ncol.size());
+                    // Dinv by forward substitution on the identity
+                    std::fill(Di.begin(), Di.end(), 0.0);
+                    for (int jc = 0; jc < bc; ++jc)
+                        for (int i = jc; i < bc; ++i) {
+                            double sacc = (i == jc) ? 1.0 : 0.0;
+                            for (int m2 = jc; m2 < i; ++m2) sacc -= Dm[i * kB + m2] * Di[m2 * kB + jc];
+                            Di[i * kB + jc] = sacc / Dm[i * kB + i];
+                        }
+                    auto push_mat = [&](const std::vector<double>& M) {
+                        const int o = (int)pool.size();
+                        pool.insert(pool.end(), M.begin(), M.end());
+                        return o;
+                    };
+                    auto times_dinv = [&](const std::vector<double>& E) {
+                        std::fill(Fm.begin(), Fm.end(), 0.0);
+                        for (int i = 0; i < bc; ++i)
+                            for (int j = 0; j < kB; ++j) {
+                                double sacc = 0.0;
+                                for (int m2 = 0; m2 <= i; ++m2) sacc += Di[i * kB + m2] * E[m2 * kB + j];
+                                Fm[i * kB + j] = sacc;
+                            }
+                        return push_mat(Fm);
+                    };
+                    const int dofs = d_ident ? -1 : push_mat(Di);
+                    const int f1 = e1_zero ? -1 : times_dinv(Em);
+                    const int f2 = e2_zero ? -1 : times_dinv(E2);
+                    blocks.push_back(make_int4(bs - p0, bc, 0, 0));
+                    blocks.push_back(make_int4(dofs, f1, f2, 0));
+                    blocks.push_back(make_int4(0, 0, 0, 0));
                 }
             }
             run.b = (int)regions.size();
@@ -485,9 +689,50 @@ void plan_triangle(exg_ctx* c, TriPlan& P, bool upper_tri, const std::vector<int
             ck(cudaMemcpy(P.ncol, ncol.data(), ncol.size() * sizeof(int), cudaMemcpyHostToDevice), "plan");
             ck(cudaMemcpy(P.nval, nval.data(), nval.size() * sizeof(double), cudaMemcpyHostToDevice), "plan");
         }
+        P.regions4 = dalloc<int4>(regions4.size());
+        ck(cudaMemcpy(P.regions4, regions4.data(), regions4.size() * sizeof(int4), cudaMemcpyHostToDevice), "plan");
+        P.blocks = dalloc<int4>(blocks.size());
+        ck(cudaMemcpy(P.blocks, blocks.data(), blocks.size() * sizeof(int4), cudaMemcpyHostToDevice), "plan");
+        P.pool = dalloc<double>(std::max<size_t>(pool.size(), 1));
+        if (!pool.empty())
+            ck(cudaMemcpy(P.pool, pool.data(), pool.size() * sizeof(double), cudaMemcpyHostToDevice), "plan");
         int mx = 0;
         for (auto& R : regions) mx = std::max(mx, R.y);
         P.smem = (size_t)mx * sizeof(double);
+    }
+    if (!cruns.empty()) {
+        P.crows = dalloc<int>(crows.size());
+        P.cnptr = dalloc<int>(cnptr.size());
+        P.cncol = dalloc<int>(std::max<size_t>(cncol.size(), 1));
+        P.cnval = dalloc<double>(std::max<size_t>(cnval.size(), 1));
+        P.cblocks = dalloc<int4>(cblocks.size());
+        ck(cudaMemcpy(P.crows, crows.data(), crows.size() * sizeof(int), cudaMemcpyHostToDevice), "chain");
+        ck(cudaMemcpy(P.cnptr, cnptr.data(), cnptr.size() * sizeof(int), cudaMemcpyHostToDevice), "chain");
+        if (!cncol.empty()) {
+            ck(cudaMemcpy(P.cncol, cncol.data(), cncol.size() * sizeof(int), cudaMemcpyHostToDevice), "chain");
+            ck(cudaMemcpy(P.cnval, cnval.data(), cnval.size() * sizeof(double), cudaMemcpyHostToDevice), "chain");
+        }
+        ck(cudaMemcpy(P.cblocks, cblocks.data(), cblocks.size() * sizeof(int4), cudaMemcpyHostToDevice), "chain");
+        P.ctasks = dalloc<int4>(std::max<size_t>(ctasks.size(), 1));
+        ck(cudaMemcpy(P.ctasks, ctasks.data(), ctasks.size() * sizeof(int4), cudaMemcpyHostToDevice), "chain");
+        if (!P.pool) {
+            P.pool = dalloc<double>(std::max<size_t>(pool.size(), 1));
+            if (!pool.empty())
+                ck(cudaMemcpy(P.pool, pool.data(), pool.size() * sizeof(double), cudaMemcpyHostToDevice), "chain");
+        }
+        // run-local views: the nptr index of position j of run q is pos0 + q + j
+        for (size_t q = 0; q < cruns.size(); ++q) {
+            TriPlan::Chain ch;
+            ch.rows_off = cruns[q].pos0;
+            ch.nptr_off = cruns[q].pos0 + (int)q;
+            ch.ent0 = cruns[q].ent0;
+            ch.n_rows = cruns[q].rows;
+            ch.blk0 = cruns[q].blk0;
+            ch.n_blocks = cruns[q].nblocks;
+            ch.task0 = cruns[q].task0;
+            ch.ntasks = cruns[q].ntasks;
+            P.chains.push_back(ch);
+        }
     }
     P.narrow_rows = (long long)rows.size();
     P.narrow_nnz = (long long)ncol.size();
@@ -737,8 +982,8 @@ exg_status exg_set_factors(exg_ctx* c, int n, const int* Lp, const int* Li, cons
     // FAST-mode plan: runs of wide levels (warp tasks, all SMs) and of narrow
     // levels (one thread-block cluster, DSMEM hand-offs)
     const int lnl = l_levels, unl = u_levels;
-    plan_triangle(c, c->plan[0], false, lord, llev, lnl, lp, lc, lv, ltasks_f);
-    plan_triangle(c, c->plan[1], true, uord, lev, unl, up, uc, uv, utasks_f);
+    plan_triangle(c, c->plan[0], false, lord, llev, lnl, lp, lc, lv, ltasks_f, nullptr);
+    plan_triangle(c, c->plan[1], true, uord, lev, unl, up, uc, uv, utasks_f, &ud);
     {
         std::vector<int4> lm(n), um(n);
         for (int p = 0; p < n; ++p) {
@@ -761,7 +1006,7 @@ exg_status exg_set_factors(exg_ctx* c, int n, const int* Lp, const int* Li, cons
         ck(cudaMemcpy(c->tasks[q], tl[q]->data(), tl[q]->size() * sizeof(int2), cudaMemcpyHostToDevice), "tasks");
         c->n_tasks[q] = (int)tl[q]->size();
     }
-    c->trsv_buf = dalloc<char>(kTrsvHdr + 2 * sizeof(double) * (size_t)n);
+    c->trsv_buf = dalloc<char>(kTrsvHdr + 6 * sizeof(double) * (size_t)n);
     ensure_vectors(c, n);
     c->cnt.l_levels = l_levels;
     c->cnt.u_levels = u_levels;

@@ -21,7 +21,7 @@ constexpr int kMaxTickets = 256;
 
 // FAST-mode execution plan of one triangle (see plan_triangle, api.cu)
 struct TriPlan {
-    static constexpr int kCap = 27648;  // region rows per shared-memory replica (216 KB)
+    static constexpr int kCap = 26112;  // region rows per shared-memory replica (204 KB)
     struct Run {
         int narrow;
         int a, b;  // wide: task range; narrow: region range
@@ -33,6 +33,20 @@ struct TriPlan {
     int* nmid = nullptr;
     int* ncol = nullptr;
     double* nval = nullptr;
+    int4* regions4 = nullptr;
+    int4* blocks = nullptr;
+    double* pool = nullptr;
+    // chain + workers runs
+    struct Chain {
+        int rows_off, nptr_off, ent0, n_rows, blk0, n_blocks, task0, ntasks;
+    };
+    std::vector<Chain> chains;
+    int* crows = nullptr;
+    int* cnptr = nullptr;
+    int* cncol = nullptr;
+    double* cnval = nullptr;
+    int4* cblocks = nullptr;
+    int4* ctasks = nullptr;
     size_t smem = 0;
     long long narrow_rows = 0, narrow_nnz = 0;
     void free_dev() {
@@ -42,6 +56,22 @@ struct TriPlan {
         if (nmid) cudaFree(nmid);
         if (ncol) cudaFree(ncol);
         if (nval) cudaFree(nval);
+        if (regions4) cudaFree(regions4);
+        if (blocks) cudaFree(blocks);
+        if (pool) cudaFree(pool);
+        if (crows) cudaFree(crows);
+        if (cnptr) cudaFree(cnptr);
+        if (cncol) cudaFree(cncol);
+        if (cnval) cudaFree(cnval);
+        if (cblocks) cudaFree(cblocks);
+        if (ctasks) cudaFree(ctasks);
+        ctasks = nullptr;
+        crows = cnptr = cncol = nullptr;
+        cnval = nullptr;
+        cblocks = nullptr;
+        chains.clear();
+        regions4 = blocks = nullptr;
+        pool = nullptr;
         regions = nullptr;
         rows = nptr = nmid = ncol = nullptr;
         nval = nullptr;

@@ -50,6 +50,34 @@ struct NarrowArgs {
     double coef;
     const Ctrl* ctrl;
     unsigned long long* trace;  // debug: per row (start, far done, end)
+    // block-recurrence mode (k_trsv_blk)
+    const int4* regions4;  // (first position, rows, first block, blocks)
+    const int4* blocks;    // (first region slot, rows, Dinv offset, F offset)
+    const double* pool;    // Dinv / F matrices, 64x64 row-major each
+};
+
+struct ChainArgs {
+    int n_rows;            // positions of this run
+    int n_blocks;
+    const int* rows;       // row id per position (run-local)
+    const int* nptr;       // per position: entries older than block k-2
+    const int* ncol;       // global row ids
+    const double* nval;
+    const int4* blocks;    // 3 per block: (first pos, rows,-,-), (Dinv, F1, F2 offsets,-), -
+    const double* pool;
+    double* s;             // per position, sentinel-initialised
+    double* part;          // per position: partial sum of the old entries (sentinel-initialised)
+    const int4* wtasks;    // worker tasks (position, k0, k1, type | has_old << 1)
+    int n_tasks;
+    const double* in;
+    const int* in_perm;
+    double* out;
+    double* final_out;
+    const int* out_perm;
+    const double* add;
+    double coef;
+    const Ctrl* ctrl;
+    unsigned long long* trace;  // debug: per block (s ready, x published)
 };
 
 struct MgsArgs {
@@ -90,6 +118,8 @@ void spmv_b2(const Launch& L, const int* rowptr, const int* col, const double* v
 void trsv(const Launch& L, bool upper, bool reverse, const TrsvArgs& a);
 void trsv_narrow(const Launch& L, bool upper, const NarrowArgs& a, int cluster, size_t smem);
 void trsv_wide(const Launch& L, bool upper, const TrsvArgs& a);
+void trsv_blk(const Launch& L, bool upper, const NarrowArgs& a, int cluster, size_t smem);
+void trsv_chain(const Launch& L, bool upper, const ChainArgs& a);
 void apply_weight(const Launch& L, const int* uptr, const int* ucol, const double* uval,
                   const double* udiag, const int* lptr, const int* lcol, const double* lval, int n,
                   const int* col_perm, const int* row_perm, const double* x, double* t,

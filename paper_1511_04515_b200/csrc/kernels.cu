@@ -704,6 +704,346 @@ __global__ void __launch_bounds__(EXG_NARROW_THREADS, 1)
 }
 
 // ---------------------------------------------------------------------------
+// Block recurrence on the cluster (FAST): each region is cut into blocks of
+// kBlk consecutive level-order positions.  With s_old = b - (entries that
+// reference blocks <= k-2 or earlier regions), E_k = the coupling of block k
+// to block k-1 and D_k its diagonal block, the host precomputes
+// Dinv_k = D_k^-1 and F_k = Dinv_k E_k, so that
+//     x_k = Dinv_k s_old  -  F_k x_{k-1}.
+// Only the last term waits on the previous block: one 64x64 GEMV per 64
+// positions on the critical path instead of one hand-off per level.  Block k
+// runs on CTA k mod CS; x is pushed into every CTA's shared-memory replica
+// (DSMEM) and to global memory.
+// ---------------------------------------------------------------------------
+constexpr int kBlk = 64;
+
+// GEMV of one warp's 8 outputs against a 64-vector held as (x0, x1) =
+// (v[lane], v[lane+32]); f0/f1 hold the warp's 8 matrix rows the same way.
+__device__ __forceinline__ void warp_gemv8(const double* f0, const double* f1, double x0, double x1,
+                                           double* part) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) part[q] = f0[q] * x0 + f1[q] * x1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) part[q] += __shfl_xor_sync(0xffffffffu, part[q], o);
+}
+
+// warp-uniform wait for the 64 (or fewer) published values of a block
+__device__ __forceinline__ void wait_block(volatile double* yv, int first, int rows, double& x0,
+                                           double& x1) {
+    const int lane = threadIdx.x & 31;
+    x0 = lane < rows ? yv[first + lane] : 0.0;
+    x1 = lane + 32 < rows ? yv[first + lane + 32] : 0.0;
+    bool rd = __double_as_longlong(x0) != (long long)kSentinel &&
+              __double_as_longlong(x1) != (long long)kSentinel;
+    while (!__all_sync(0xffffffffu, rd)) {
+        if (lane < rows) x0 = yv[first + lane];
+        if (lane + 32 < rows) x1 = yv[first + lane + 32];
+        rd = __double_as_longlong(x0) != (long long)kSentinel &&
+             __double_as_longlong(x1) != (long long)kSentinel;
+    }
+}
+
+__device__ __forceinline__ void load_rows8(const double* M, int i0, int nb, int ncols, double* f0,
+                                           double* f1) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const int i = i0 + q;
+        f0[q] = (i < nb && lane < ncols) ? M[i * kBlk + lane] : 0.0;
+        f1[q] = (i < nb && lane + 32 < ncols) ? M[i * kBlk + lane + 32] : 0.0;
+    }
+}
+
+template <bool UPPER>
+__global__ void __launch_bounds__(256, 1)
+    k_trsv_blk(NarrowArgs a) {
+    extern __shared__ double yrep[];
+    __shared__ double sbuf[kBlk];
+    cg::cluster_group cl = cg::this_cluster();
+    if (a.ctrl && (a.ctrl->converged || a.ctrl->status)) return;
+    const unsigned FULL = 0xffffffffu;
+    const int rank = (int)cl.block_rank();
+    const int cs = (int)cl.num_blocks();
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    unsigned long long* ybits = reinterpret_cast<unsigned long long*>(yrep);
+    volatile double* yv = yrep;
+    for (int reg = 0; reg < a.n_regions; ++reg) {
+        const int4 R = a.regions4[reg];  // np0, rows, block0, nblocks
+        for (int i = threadIdx.x; i < R.y; i += blockDim.x) ybits[i] = kSentinel;
+        cl.sync();
+        for (int kb = rank; kb < R.w; kb += cs) {
+            const int4 B = a.blocks[3 * (R.z + kb)];      // first slot, rows, -, -
+            const int4 O = a.blocks[3 * (R.z + kb) + 1];  // Dinv off, F1 off, F2 off, -
+            const int nb = B.y;
+            // ---- pass A: s_old = b - (entries older than block k-2), warp per row
+            for (int i = warp; i < nb; i += 8) {
+                const int p = R.x + B.x + i;
+                const int r = a.rows[p];
+                const double b = UPPER ? a.in[r] : a.in[a.in_perm[r]];
+                const int k0 = a.nptr[p], k1 = a.nptr[p + 1];
+                double acc = 0.0;
+                for (int base = k0; base < k1; base += 128) {
+                    int cc[4];
+                    double v[4], y[4];
+                    bool rd = true;
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        const int kk = base + lane + 32 * t;
+                        cc[t] = kk < k1 ? a.ncol[kk] : 0;
+                        v[t] = kk < k1 ? a.nval[kk] : 0.0;
+                    }
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        const int kk = base + lane + 32 * t;
+                        if (kk >= k1) y[t] = 0.0;
+                        else if (cc[t] >= 0) y[t] = __ldca(a.out + cc[t]);
+                        else {
+                            y[t] = yv[-1 - cc[t]];
+                            rd = rd && __double_as_longlong(y[t]) != (long long)kSentinel;
+                        }
+                    }
+                    while (!__all_sync(FULL, rd)) {
+                        rd = true;
+#pragma unroll
+                        for (int t = 0; t < 4; ++t) {
+                            const int kk = base + lane + 32 * t;
+                            if (kk < k1 && cc[t] < 0 && __double_as_longlong(y[t]) == (long long)kSentinel) {
+                                y[t] = yv[-1 - cc[t]];
+                                rd = rd && __double_as_longlong(y[t]) != (long long)kSentinel;
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) acc += v[t] * y[t];
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
+                if (lane == 0) sbuf[i] = b - acc;
+            }
+            __syncthreads();
+            // ---- c = Dinv s_old (warp w: outputs 8w..8w+7), F rows prefetched
+            const int i0 = warp * 8;
+            double c[8], part[8], f0[8], f1[8];
+            const double s0 = sbuf[lane < nb ? lane : 0], s1 = sbuf[lane + 32 < nb ? lane + 32 : 0];
+            if (O.x >= 0) {
+                load_rows8(a.pool + (long long)O.x, i0, nb, nb, f0, f1);
+                warp_gemv8(f0, f1, lane < nb ? s0 : 0.0, lane + 32 < nb ? s1 : 0.0, c);
+            } else {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) c[q] = (i0 + q < nb) ? sbuf[i0 + q] : 0.0;
+            }
+            // ---- c -= F2 x_{k-2}  (one block-time of slack)
+            if (O.z >= 0) {
+                const int4 B2 = a.blocks[3 * (R.z + kb - 2)];
+                load_rows8(a.pool + (long long)O.z, i0, nb, B2.y, f0, f1);
+                double x0, x1;
+                wait_block(yv, B2.x, B2.y, x0, x1);
+                warp_gemv8(f0, f1, x0, x1, part);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) c[q] = c[q] - part[q];
+            }
+            // ---- x = c - F1 x_{k-1}  (the only wait on the critical path)
+            if (O.y >= 0) {
+                const int4 B1 = a.blocks[3 * (R.z + kb - 1)];
+                load_rows8(a.pool + (long long)O.y, i0, nb, B1.y, f0, f1);
+                double x0, x1;
+                wait_block(yv, B1.x, B1.y, x0, x1);
+                warp_gemv8(f0, f1, x0, x1, part);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) c[q] = c[q] - part[q];
+            }
+            // ---- publish x_k: replicas (DSMEM), global, fused epilogue
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int i = i0 + q;
+                if (i >= nb) break;
+                unsigned long long sb = __double_as_longlong(c[q]);
+                if (sb == kSentinel) sb = kCanonNaN;
+                if (lane < cs) {
+                    const unsigned laddr = (unsigned)__cvta_generic_to_shared(yrep + B.x + i);
+                    unsigned raddr;
+                    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(laddr), "r"(lane));
+                    asm volatile("st.relaxed.cluster.shared::cluster.b64 [%0], %1;" ::"r"(raddr), "l"(sb) : "memory");
+                }
+                if (lane == 31) {
+                    const int r = a.rows[R.x + B.x + i];
+                    const double xv = __longlong_as_double(sb);
+                    st_relaxed(a.out + r, xv);
+                    if (a.final_out) {
+                        const int qq = a.out_perm[r];
+                        double yo = a.coef * xv;
+                        if (a.add) yo = a.add[qq] + yo;
+                        a.final_out[qq] = yo;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        cl.sync();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Chain + workers (FAST, narrow runs): one cooperative launch over the whole
+// GPU.  The run's level-order positions are cut into blocks of 64; with
+//     x_k = Dinv_k s_k - F1_k x_{k-1} - F2_k x_{k-2},   F_g = Dinv_k E_g,
+// CTA 0 (the chain) evaluates the recurrence block after block entirely in
+// its own shared memory (no hand-off between consecutive blocks), streaming
+// Dinv/F1/F2 with cp.async double buffering; every other warp of the GPU
+// computes s_k = b - (entries older than block k-2) for the rows (sync-free
+// warp tasks polling the published solution in global memory; s is
+// published the same way, sentinel-initialised).  Workers lag the chain by
+// two blocks, which hides their L2 hand-off latency.
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+#ifndef EXG_CHAIN_MINB
+#define EXG_CHAIN_MINB 1
+#endif
+template <bool UPPER>
+__global__ void __launch_bounds__(256, EXG_CHAIN_MINB)
+    k_trsv_chain(ChainArgs a) {
+    if (a.ctrl && (a.ctrl->converged || a.ctrl->status)) return;
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (blockIdx.x == 0) {
+        // ===================== chain CTA =====================
+        __shared__ double xr[3 * kBlk];  // ring of the last 3 blocks' x
+        const int i0 = warp * 8;
+        for (int kb = 0; kb < a.n_blocks; ++kb) {
+            const int4 B = a.blocks[3 * kb];
+            const int4 O = a.blocks[3 * kb + 1];
+            const int nb = B.y;
+            // matrices of this block: straight from L2/HBM into registers,
+            // issued before the wait on s so the latencies overlap
+            double d0[8], d1[8], g0[8], g1[8], h0[8], h1[8];
+            const int4 B1 = kb >= 1 ? a.blocks[3 * (kb - 1)] : make_int4(0, 0, 0, 0);
+            const int4 B2 = kb >= 2 ? a.blocks[3 * (kb - 2)] : make_int4(0, 0, 0, 0);
+            if (O.x >= 0) load_rows8(a.pool + (long long)O.x, i0, nb, nb, d0, d1);
+            if (O.y >= 0) load_rows8(a.pool + (long long)O.y, i0, nb, B1.y, g0, g1);
+            if (O.z >= 0) load_rows8(a.pool + (long long)O.z, i0, nb, B2.y, h0, h1);
+            // s of this block (published by the workers)
+            double s0 = 0.0, s1 = 0.0;
+            {
+                const double* sp = a.s + B.x;
+                s0 = lane < nb ? __longlong_as_double(ld_relaxed(sp + lane)) : 0.0;
+                s1 = lane + 32 < nb ? __longlong_as_double(ld_relaxed(sp + lane + 32)) : 0.0;
+                bool rd = __double_as_longlong(s0) != (long long)kSentinel &&
+                          __double_as_longlong(s1) != (long long)kSentinel;
+                while (!__all_sync(FULL, rd)) {
+                    if (lane < nb) s0 = __longlong_as_double(ld_relaxed(sp + lane));
+                    if (lane + 32 < nb) s1 = __longlong_as_double(ld_relaxed(sp + lane + 32));
+                    rd = __double_as_longlong(s0) != (long long)kSentinel &&
+                         __double_as_longlong(s1) != (long long)kSentinel;
+                }
+            }
+            unsigned long long t_s = 0;
+            if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_s));
+            double c[8], part[8];
+            if (O.x >= 0) {
+                warp_gemv8(d0, d1, s0, s1, c);
+            } else {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const int i = i0 + q;
+                    const double v = __shfl_sync(FULL, (i & 32) ? s1 : s0, i & 31);
+                    c[q] = i < nb ? v : 0.0;
+                }
+            }
+            if (O.z >= 0) {
+                const double* xg = xr + ((kb - 2) % 3) * kBlk;
+                warp_gemv8(h0, h1, lane < B2.y ? xg[lane] : 0.0, lane + 32 < B2.y ? xg[lane + 32] : 0.0, part);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) c[q] = c[q] - part[q];
+            }
+            if (O.y >= 0) {
+                const double* xg = xr + ((kb - 1) % 3) * kBlk;
+                warp_gemv8(g0, g1, lane < B1.y ? xg[lane] : 0.0, lane + 32 < B1.y ? xg[lane + 32] : 0.0, part);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) c[q] = c[q] - part[q];
+            }
+            // publish x_k: chain ring (smem) + global solution + fused epilogue
+            double* xk = xr + (kb % 3) * kBlk;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int i = i0 + q;
+                if (i < nb && lane == q) {
+                    xk[i] = c[q];
+                    const int r = a.rows[B.x + i];
+                    st_relaxed(a.out + r, c[q]);
+                    if (a.final_out) {
+                        const int qq = a.out_perm[r];
+                        double yo = a.coef * c[q];
+                        if (a.add) yo = a.add[qq] + yo;
+                        a.final_out[qq] = yo;
+                    }
+                }
+            }
+            __syncthreads();
+            if (a.trace && threadIdx.x == 0) {
+                unsigned long long t_e;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_e));
+                a.trace[2 * kb] = t_s;
+                a.trace[2 * kb + 1] = t_e;
+            }
+        }
+        return;
+    }
+    // ===================== workers =====================
+    // tasks in order of the block their newest dependency belongs to:
+    //   type 0 ("old"): part[p] = sum of the row's entries older than block k-8
+    //   type 1 ("recent"): s[p] = b - (part[p] + entries of blocks k-8..k-3)
+    const int gw = (blockIdx.x - 1) * (blockDim.x >> 5) + warp;
+    const int W = (gridDim.x - 1) * (blockDim.x >> 5);
+    for (int t = gw; t < a.n_tasks; t += W) {
+        const int4 T = a.wtasks[t];  // p, k0, k1, type | has_old << 1
+        const int p = T.x, k0 = T.y, k1 = T.z;
+        double acc = 0.0;
+        for (int base = k0; base < k1; base += 256) {
+            int kk[8], cc[8];
+            double v[8], y[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                kk[q] = base + lane + 32 * q;
+                cc[q] = kk[q] < k1 ? a.ncol[kk[q]] : 0;
+                v[q] = kk[q] < k1 ? a.nval[kk[q]] : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) y[q] = kk[q] < k1 ? __ldca(a.out + cc[q]) : 0.0;
+            warp_wait_ready<8>(a.out, cc, kk, k1, y);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc += v[q] * y[q];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
+        if (lane == 0) {
+            if ((T.w & 1) == 0) {
+                st_relaxed(a.part + p, acc);
+            } else {
+                const int r = a.rows[p];
+                const double b = UPPER ? a.in[r] : a.in[a.in_perm[r]];
+                double old = 0.0;
+                if (T.w & 2) {
+                    unsigned long long ob = ld_relaxed(a.part + p);
+                    while (ob == kSentinel) ob = ld_relaxed(a.part + p);
+                    old = __longlong_as_double(ob);
+                }
+                st_relaxed(a.s + p, b - (old + acc));
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // row-sequential warp SpMV helper for rows of very different lengths
 // (factor apply): long rows cooperatively with the in-order chain through
 // shuffles, short rows one per lane.  Bit-identical to spmv.
@@ -1743,6 +2083,49 @@ static int trsv3_occ() {
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_trsv3<U>, 256, 0);
     return occ > 0 ? occ : 1;
+}
+
+void trsv_blk(const Launch& L, bool upper, const NarrowArgs& a, int cluster, size_t smem) {
+    static bool attr[2] = {false, false};
+    auto fn = upper ? (void*)k_trsv_blk<true> : (void*)k_trsv_blk<false>;
+    if (!attr[upper]) {
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        attr[upper] = true;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(cluster);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = L.stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cluster;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (upper)
+        cudaLaunchKernelEx(&cfg, k_trsv_blk<true>, a);
+    else
+        cudaLaunchKernelEx(&cfg, k_trsv_blk<false>, a);
+    count(L);
+}
+
+void trsv_chain(const Launch& L, bool upper, const ChainArgs& a) {
+    static bool attr[2] = {false, false};
+    static int occ[2] = {0, 0};
+    auto fn = upper ? (void*)k_trsv_chain<true> : (void*)k_trsv_chain<false>;
+    if (!attr[upper]) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[upper], upper ? k_trsv_chain<true> : k_trsv_chain<false>, 256, 0);
+        if (occ[upper] < 1) occ[upper] = 1;
+        attr[upper] = true;
+    }
+    const unsigned int grid = (unsigned int)std::max<long long>(
+        2, std::min<long long>((long long)L.num_sms * occ[upper], 1 + ((long long)a.n_rows + 7) / 8));
+    void* args[] = {(void*)&a};
+    cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(256), args, 0, L.stream);
+    count(L);
 }
 
 void trsv_wide(const Launch& L, bool upper, const TrsvArgs& a) {

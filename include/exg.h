@@ -143,6 +143,22 @@ exg_status exg_er_step(exg_ctx* ctx, const double* x_k, const double* u_k, const
                        double h, const exg_mevp_cfg* cfg, double* x_next, int* m_out,
                        int ptr_kind);
 
+/* ---- nonlinear devices (config 4; devices.cpp, integrate.cpp:267-298) ----
+ * exg_set_devices: MOSFET table — nodes4 = (drain, gate, source, bulk)
+ * unknown indices per device (-1 ground), par6 = (VTH, KP, LAMBDA, W, L,
+ * PMOS flag).  exg_set_oppoints: the frozen operating point of the current
+ * linearization, op5 = (vgs_ref, vds_ref, id_ref, gm, gds) per device
+ * (DeviceOperatingPoint, devices.hpp:14-26).  With devices set, exg_er_begin
+ * uses F(x_k) = exg_residual_F(x_k) (devices.cpp:202-233). */
+exg_status exg_set_devices(exg_ctx* ctx, int n_mos, const int* nodes4, const double* par6);
+exg_status exg_set_oppoints(exg_ctx* ctx, const double* op5);
+exg_status exg_residual_F(exg_ctx* ctx, const double* x, double* F, int ptr_kind);
+/* after exg_er_eval: err_norm = ||e_rr||_inf of error_from_deltaF; with erc,
+ * x_next += correction_from_deltaF(gamma).  dims receives the Krylov
+ * dimensions of the MEVPs run (at most 2). */
+exg_status exg_er_nonlinear(exg_ctx* ctx, double h, const exg_mevp_cfg* cfg, int erc, double gamma,
+                            double* err_norm, int* dims, int* n_dims);
+
 /* out[i] = x_next[idx[i]] of the last ER evaluation (probed nodes) */
 exg_status exg_gather(exg_ctx* ctx, const int* idx, int k, double* out);
 

@@ -11,6 +11,9 @@
  *   exg_breakpoints       <- exsim::source_breakpoints proj/core/src/mna.cpp:173-180
  *   exg_lu_factor         <- exsim::lu_factor          proj/core/src/sparse_lu.cpp:134-253
  *   exg_transient         <- exsim::transient (ER/ERC) proj/core/src/integrate.cpp:368-480
+ *   exg_dc_solve          <- exsim::dc_solve           proj/core/src/integrate.cpp:92-115
+ *   exg_linearize         <- exsim::evaluate           proj/core/src/devices.cpp:122-200
+ *   exg_residual_F_host   <- exsim::residual_F         proj/core/src/devices.cpp:202-233
  *
  * exg_lu_factor produces factors bit-identical to the reference's lu_factor
  * (same minimum-degree order, same pivots, same values) but orders with a heap
@@ -106,6 +109,7 @@ void exg_system_free(exg_system* s);
 int exg_system_n(const exg_system* s);
 int exg_system_n_nodes(const exg_system* s);
 int exg_system_n_inputs(const exg_system* s);
+int exg_system_n_mos(const exg_system* s); /* MOSFET count */
 /* which: EXG_MAT_C / EXG_MAT_G / EXG_MAT_B.  Borrowed pointers. */
 exg_status exg_system_csr(const exg_system* s, int which, int* n_rows, int* n_cols, int* nnz,
                           const int** rowptr, const int** col, const double** val);
@@ -125,6 +129,16 @@ exg_status exg_sources_eval(const exg_system* s, double t, double* u);
 int exg_breakpoints(const exg_system* s, double t0, double t1, double* out, int cap);
 
 /* ---- setup LU ---------------------------------------------------------- */
+
+/* DC operating point (Newton + gmin stepping), bit-identical to dc_solve. */
+exg_status exg_dc_solve(const exg_system* s, double* x);
+/* Linearization at x: which = EXG_MAT_C / EXG_MAT_G selects C_k / G_k.
+ * Call with rowptr == NULL to get *nnz; op5 (optional) receives the MOSFET
+ * operating points (vgs_ref, vds_ref, id_ref, gm, gds) per device. */
+exg_status exg_linearize(const exg_system* s, const double* x, int which, int* nnz, int* rowptr,
+                         int* col, double* val, double* op5);
+/* F(x) with the stamps frozen at the linearization point x_ref */
+exg_status exg_residual_F_host(const exg_system* s, const double* x_ref, const double* x, double* F);
 
 typedef struct exg_factor exg_factor;
 

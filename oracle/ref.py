@@ -113,6 +113,30 @@ class Ref:
         self._check(self.lib.ref_dc_solve(h, _ptr(x, C.c_double)))
         return x
 
+    def evaluate(self, h, x, n_mos):
+        """exsim::evaluate -> (C_k, G_k) as (rowptr, col, val) and op[n_mos, 5]."""
+        n = self.lib.ref_system_n(h)
+        x = _d(x)
+        out = []
+        op = np.zeros((n_mos, 5))
+        for which in (0, 1):
+            nnz = C.c_int()
+            self._check(self.lib.ref_evaluate(h, _ptr(x, C.c_double), which, C.byref(nnz),
+                                              None, None, None, None))
+            rp, ci, va = np.zeros(n + 1, np.int32), np.zeros(nnz.value, np.int32), np.zeros(nnz.value)
+            self._check(self.lib.ref_evaluate(h, _ptr(x, C.c_double), which, C.byref(nnz),
+                                              _ptr(rp, C.c_int), _ptr(ci, C.c_int),
+                                              _ptr(va, C.c_double), _ptr(op, C.c_double)))
+            out.append((rp, ci, va))
+        return out[0], out[1], op
+
+    def residual_F(self, h, x_ref, x):
+        n = self.lib.ref_system_n(h)
+        F_ = np.zeros(n)
+        self._check(self.lib.ref_residual_F(h, _ptr(_d(x_ref), C.c_double), _ptr(_d(x), C.c_double),
+                                            _ptr(F_, C.c_double)))
+        return F_
+
     # ---- LU
     def lu_factor(self, A, pivot_tol=0.1):
         h = C.c_void_p()

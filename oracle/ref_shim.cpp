@@ -363,6 +363,38 @@ int ref_dc_solve(void* s, double* x) {
     GUARD_END
 }
 
+int ref_evaluate(void* s, const double* x, int which, int* nnz, int* rowptr, int* col, double* val,
+                 double* op5) {
+    GUARD_BEGIN
+    const MnaSystem& sys = *static_cast<MnaSystem*>(s);
+    Linearization lin = evaluate(sys, Vec(x, x + sys.n));
+    const SparseRealMatrix& A = which == 0 ? lin.C_k : lin.G_k;
+    *nnz = A.nnz();
+    if (rowptr) {
+        std::memcpy(rowptr, A.row_offsets().data(), sizeof(int) * (A.n_rows() + 1));
+        std::memcpy(col, A.col_indices().data(), sizeof(int) * A.nnz());
+        std::memcpy(val, A.values().data(), sizeof(double) * A.nnz());
+    }
+    if (op5)
+        for (size_t i = 0; i < lin.op.size(); ++i) {
+            op5[5 * i] = lin.op[i].vgs_ref;
+            op5[5 * i + 1] = lin.op[i].vds_ref;
+            op5[5 * i + 2] = lin.op[i].id_ref;
+            op5[5 * i + 3] = lin.op[i].gm;
+            op5[5 * i + 4] = lin.op[i].gds;
+        }
+    GUARD_END
+}
+
+int ref_residual_F(void* s, const double* x_ref, const double* x, double* F) {
+    GUARD_BEGIN
+    const MnaSystem& sys = *static_cast<MnaSystem*>(s);
+    Linearization lin = evaluate(sys, Vec(x_ref, x_ref + sys.n));
+    Vec v = residual_F(lin, Vec(x, x + sys.n));
+    std::memcpy(F, v.data(), sizeof(double) * v.size());
+    GUARD_END
+}
+
 // ---- LU ----------------------------------------------------------------------
 int ref_lu_factor(int n, const int* rowptr, const int* col, const double* val, int nnz,
                   double pivot_tol, void** out) {

@@ -117,6 +117,7 @@ _HOST_PROTOS = {
     "exg_system_n": (I, [P]),
     "exg_system_n_nodes": (I, [P]),
     "exg_system_n_inputs": (I, [P]),
+    "exg_system_n_mos": (I, [P]),
     "exg_system_csr": (I, [P, I, PI, PI, PI, C.POINTER(PI), C.POINTER(PI), C.POINTER(PD)]),
     "exg_system_elements": (I, [P, PI, C.POINTER(C.POINTER(exg_element)), PI,
                                 C.POINTER(C.POINTER(exg_source)), PI, C.POINTER(PD),
@@ -125,6 +126,9 @@ _HOST_PROTOS = {
     "exg_system_unknown_of_label": (I, [P, I]),
     "exg_sources_eval": (I, [P, D, PD]),
     "exg_breakpoints": (I, [P, D, D, PD, I]),
+    "exg_dc_solve": (I, [P, PD]),
+    "exg_linearize": (I, [P, PD, I, PI, PI, PI, PD, PD]),
+    "exg_residual_F_host": (I, [P, PD, PD, PD]),
     "exg_lu_factor": (I, [I, PI, PI, PD, D, C.POINTER(P)]),
     "exg_factor_free": (None, [P]),
     "exg_factor_get": (I, [P, PI, C.POINTER(PI), C.POINTER(PI), C.POINTER(PD), C.POINTER(PI),
@@ -151,6 +155,10 @@ _DEV_PROTOS = {
     "exg_er_eval": (I, [P, D, C.POINTER(exg_mevp_cfg), P, PI, C.POINTER(exg_mevp_info), I]),
     "exg_er_step": (I, [P, P, P, P, D, C.POINTER(exg_mevp_cfg), P, PI, I]),
     "exg_gather": (I, [P, PI, I, PD]),
+    "exg_set_devices": (I, [P, I, PI, PD]),
+    "exg_set_oppoints": (I, [P, PD]),
+    "exg_residual_F": (I, [P, P, P, I]),
+    "exg_er_nonlinear": (I, [P, D, C.POINTER(exg_mevp_cfg), I, D, PD, PI, PI]),
     "exg_counters_get": (I, [P, C.POINTER(exg_counters)]),
     "exg_counters_reset": (I, [P]),
     "exg_profile_enable": (I, [P, I]),

@@ -811,6 +811,17 @@ void exg_destroy(exg_ctx* c) {
     if (c->done) cudaFree(c->done);
     if (c->ctrl) cudaFree(c->ctrl);
     if (c->h_ctrl) cudaFreeHost(c->h_ctrl);
+    {
+        double* dq[] = {c->mos_par, c->mos_op, c->mos_r, c->Fk, c->dF, c->nw, c->nu, c->nv,
+                        c->aux.V, c->aux.hbar, c->aux.hinv, c->aux.coef, c->aux.dscratch};
+        for (double* p : dq)
+            if (p) cudaFree(p);
+        if (c->mos_nodes) cudaFree(c->mos_nodes);
+        if (c->node_ptr) cudaFree(c->node_ptr);
+        if (c->node_list) cudaFree(c->node_list);
+        if (c->aux.ctrl) cudaFree(c->aux.ctrl);
+        if (c->aux.h_ctrl) cudaFreeHost(c->aux.h_ctrl);
+    }
     for (auto& pe : c->prof_events) {
         cudaEventDestroy(pe.second.first);
         cudaEventDestroy(pe.second.second);
@@ -1154,8 +1165,14 @@ exg_status exg_er_begin(exg_ctx* c, const double* x_k, const double* u_k, const 
         ck(cudaMemcpyAsync(c->u_k1, u_k1, sizeof(double) * ni, kind, c->stream), "u_k1");
     }
     auto L = c->L();
-    // rhs = F + B u_k (F == 0 for linear stamps) ; B slope
-    exg::dev::spmv_b2(L, B.rowptr, B.col, B.val, B.n_rows, c->u_k, c->u_k1, h, c->t1, c->t2);
+    // rhs = F(x_k) + B u_k (integrate.cpp:224; F == 0 without devices) ; B slope
+    const double* Fk = nullptr;
+    if (c->n_mos > 0) {
+        exg::dev::mos_residual(L, c->n_mos, c->mos_nodes, c->mos_par, c->mos_op, c->xk, c->mos_r, n,
+                               c->node_ptr, c->node_list, c->Fk, nullptr);
+        Fk = c->Fk;
+    }
+    exg::dev::spmv_b2(L, B.rowptr, B.col, B.val, B.n_rows, c->u_k, c->u_k1, h, c->t1, c->t2, Fk);
     solve_dev(c, c->t1, c->v1, -1.0, c->xk, nullptr);      // v1 = x_k - G^{-1} rhs
     solve_dev(c, c->t2, c->gb, 1.0, nullptr, nullptr);     // gb_slope = G^{-1} B slope
     exg::dev::spmv(L, C.rowptr, C.col, C.val, C.n_rows, c->gb, c->t3, nullptr, nullptr, 0);
@@ -1207,6 +1224,131 @@ exg_status exg_er_step(exg_ctx* c, const double* x_k, const double* u_k, const d
     exg_status st = exg_er_begin(c, x_k, u_k, u_k1, h, ptr_kind);
     if (st != EXG_OK) return st;
     return exg_er_eval(c, h, cfg, x_next, m_out, nullptr, ptr_kind);
+}
+
+exg_status exg_set_devices(exg_ctx* c, int n_mos, const int* nodes4, const double* par6) {
+    API_BEGIN
+    require_factors(c);
+    const int n = c->n;
+    dfree(c->mos_par);
+    dfree(c->mos_op);
+    dfree(c->mos_r);
+    if (c->mos_nodes) cudaFree(c->mos_nodes);
+    c->mos_nodes = nullptr;
+    dfree(c->node_ptr);
+    dfree(c->node_list);
+    c->n_mos = n_mos;
+    // per-node contribution lists in device order (drain +, source -)
+    std::vector<int> cnt(n + 1, 0);
+    for (int i = 0; i < n_mos; ++i) {
+        if (nodes4[4 * i] >= 0) cnt[nodes4[4 * i] + 1]++;
+        if (nodes4[4 * i + 2] >= 0) cnt[nodes4[4 * i + 2] + 1]++;
+    }
+    for (int i = 0; i < n; ++i) cnt[i + 1] += cnt[i];
+    std::vector<int> list(cnt[n]), next(cnt.begin(), cnt.end() - 1);
+    for (int i = 0; i < n_mos; ++i) {
+        if (nodes4[4 * i] >= 0) list[next[nodes4[4 * i]]++] = i;
+        if (nodes4[4 * i + 2] >= 0) list[next[nodes4[4 * i + 2]]++] = -1 - i;
+    }
+    c->mos_nodes = static_cast<int4*>(static_cast<void*>(dalloc<int>(4 * (size_t)std::max(n_mos, 1))));
+    c->mos_par = dalloc<double>(6 * (size_t)std::max(n_mos, 1));
+    c->mos_op = dalloc<double>(5 * (size_t)std::max(n_mos, 1));
+    c->mos_r = dalloc<double>(std::max(n_mos, 1));
+    c->node_ptr = dalloc<int>(n + 1);
+    c->node_list = dalloc<int>(std::max(cnt[n], 1));
+    if (n_mos) {
+        ck(cudaMemcpy(c->mos_nodes, nodes4, 4 * sizeof(int) * n_mos, cudaMemcpyHostToDevice), "mos");
+        ck(cudaMemcpy(c->mos_par, par6, 6 * sizeof(double) * n_mos, cudaMemcpyHostToDevice), "mos");
+        ck(cudaMemset(c->mos_op, 0, 5 * sizeof(double) * n_mos), "mos");
+    }
+    ck(cudaMemcpy(c->node_ptr, cnt.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice), "mos");
+    if (cnt[n]) ck(cudaMemcpy(c->node_list, list.data(), sizeof(int) * cnt[n], cudaMemcpyHostToDevice), "mos");
+    double** vs[] = {&c->Fk, &c->dF, &c->nw, &c->nu, &c->nv};
+    for (double** p : vs) {
+        dfree(*p);
+        *p = dalloc<double>(n);
+    }
+    if (!c->aux.ctrl) {
+        c->aux.ctrl = static_cast<Ctrl*>(static_cast<void*>(dalloc<char>(exg::dev::ctrl_size())));
+        void* hp = nullptr;
+        ck(cudaMallocHost(&hp, exg::dev::ctrl_size()), "cudaMallocHost");
+        c->aux.h_ctrl = static_cast<Ctrl*>(hp);
+        std::memset(c->aux.h_ctrl, 0, exg::dev::ctrl_size());
+    }
+    API_END(c)
+}
+
+exg_status exg_set_oppoints(exg_ctx* c, const double* op5) {
+    API_BEGIN
+    if (c->n_mos) ck(cudaMemcpy(c->mos_op, op5, 5 * sizeof(double) * c->n_mos, cudaMemcpyHostToDevice), "op");
+    API_END(c)
+}
+
+exg_status exg_residual_F(exg_ctx* c, const double* x, double* F, int ptr_kind) {
+    API_BEGIN
+    require_factors(c);
+    if (!c->node_ptr) throw ApiError{EXG_E_CONTRACT, "residual_F: no devices (exg_set_devices)"};
+    const int n = c->n;
+    const double* xd = resolve_in(c, x, n, ptr_kind, c->vin);
+    double* Fd = ptr_kind == EXG_PTR_DEVICE ? F : c->vout;
+    exg::dev::mos_residual(c->L(), c->n_mos, c->mos_nodes, c->mos_par, c->mos_op, xd, c->mos_r, n,
+                           c->node_ptr, c->node_list, Fd, nullptr);
+    deliver(c, F, Fd, n, ptr_kind);
+    API_END(c)
+}
+
+// nonlinear error estimate and ER-C correction of the last er_eval
+// (error_from_deltaF / correction_from_deltaF, integrate.cpp:267-298, called
+// as transient() does at :434-445).  x_next (device) is corrected in place.
+exg_status exg_er_nonlinear(exg_ctx* c, double h, const exg_mevp_cfg* cfg, int erc, double gamma,
+                            double* err_norm, int* dims, int* n_dims) {
+    API_BEGIN
+    require_factors(c);
+    if (!c->node_ptr) throw ApiError{EXG_E_CONTRACT, "er_nonlinear: no devices (exg_set_devices)"};
+    const int n = c->n;
+    auto L = c->L();
+    *err_norm = 0.0;
+    *n_dims = 0;
+    // deltaF = residual_F(x_next) - F_k
+    exg::dev::mos_residual(L, c->n_mos, c->mos_nodes, c->mos_par, c->mos_op, c->xnext, c->mos_r, n,
+                           c->node_ptr, c->node_list, c->dF, c->Fk);
+    exg::dev::absmax(L, c->dF, n, c->partials, c->done, c->weight + 2);
+    double dfinf = 0.0;
+    ck(cudaMemcpyAsync(&dfinf, c->weight + 2, sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    if (dfinf == 0.0) return EXG_OK;  // both error and correction vanish
+    solve_dev(c, c->dF, c->nw, 1.0, nullptr, nullptr);  // w = G^{-1} deltaF
+    c->swap_krylov();
+    struct Restore {
+        exg_ctx* c;
+        ~Restore() { c->swap_krylov(); }
+    } restore{c};
+    // error: e_rr = w - e^{hJ} w (skipped when ||w|| == 0)
+    mevp_dev(c, c->nw, h, *cfg, 2, nullptr);
+    if (!c->h_ctrl->skip) {
+        dims[(*n_dims)++] = c->h_ctrl->m;
+        exg::dev::combine(L, c->V, c->ldv, c->coef, n, c->nv, c->ctrl, 0, nullptr, nullptr, nullptr, 0.0);
+        exg::dev::axpby(L, c->nw, -1.0, c->nv, c->nu, n);
+        exg::dev::absmax(L, c->nu, n, c->partials, c->done, c->weight + 2);
+        ck(cudaMemcpyAsync(err_norm, c->weight + 2, sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
+        ck(cudaStreamSynchronize(c->stream), "sync");
+    }
+    if (erc && gamma != 0.0) {
+        // u = G^{-1} C w ; d = gamma (w + (e^{hJ}u - u)/h) ; x_next += d
+        const DCsr& C = mat(c, EXG_MAT_C);
+        exg::dev::spmv(L, C.rowptr, C.col, C.val, C.n_rows, c->nw, c->t, nullptr, nullptr, 0);
+        solve_dev(c, c->t, c->nu, 1.0, nullptr, nullptr);
+        mevp_dev(c, c->nu, h, *cfg, 2, nullptr);
+        int have_u = 0;
+        if (!c->h_ctrl->skip) {
+            dims[(*n_dims)++] = c->h_ctrl->m;
+            exg::dev::combine(L, c->V, c->ldv, c->coef, n, c->nv, c->ctrl, 0, nullptr, nullptr, nullptr, 0.0);
+            have_u = 1;
+        }
+        exg::dev::erc_update(L, c->nw, c->nv, c->nu, have_u, 1.0 / h, gamma, c->xnext, n);
+    }
+    ck(cudaGetLastError(), "er_nonlinear launch");
+    API_END(c)
 }
 
 exg_status exg_gather(exg_ctx* c, const int* idx, int k, double* out) {

@@ -369,6 +369,10 @@ void config4(System& sys, const exg_gen_params& p) {
             mn.nodes[3] = -1;
             mn.aux = 0;
             sys.elems.push_back(mn);
+            // wire load of the output (the reference's inverter_chain has CL,
+            // generator.cpp:98); without it the last output is an algebraic
+            // node whose nonlinear error w - e^{hJ}w does not shrink with h
+            b.two(EXG_EL_C, out, -1, 1e-15);
             prev = out;
         }
     }

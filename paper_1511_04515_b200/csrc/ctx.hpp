@@ -134,7 +134,38 @@ struct exg_ctx {
     double prof_ms[EXG_K_CLASSES] = {};
     long long prof_count[EXG_K_CLASSES] = {};
 
+    // nonlinear devices (config 4)
+    int n_mos = 0;
+    int4* mos_nodes = nullptr;
+    double *mos_par = nullptr, *mos_op = nullptr, *mos_r = nullptr;
+    int *node_ptr = nullptr, *node_list = nullptr;
+    double *Fk = nullptr, *dF = nullptr, *nw = nullptr, *nu = nullptr, *nv = nullptr;
+    // second Krylov workspace for the error / correction MEVPs (the step's
+    // own basis stays cached for the rejection retries, integrate.cpp:249)
+    struct Krylov {
+        int mmax_alloc = 0;
+        long long ldv = 0;
+        double *V = nullptr, *hbar = nullptr, *hinv = nullptr, *coef = nullptr, *dscratch = nullptr;
+        int hld = 0;
+        bool basis_valid = false;
+        exg::dev::Ctrl* ctrl = nullptr;
+        exg::dev::Ctrl* h_ctrl = nullptr;
+    } aux;
+
     exg::dev::Launch L() { return exg::dev::Launch{stream, num_sms, &launches}; }
+    void swap_krylov() {
+        std::swap(mmax_alloc, aux.mmax_alloc);
+        std::swap(ldv, aux.ldv);
+        std::swap(V, aux.V);
+        std::swap(hbar, aux.hbar);
+        std::swap(hinv, aux.hinv);
+        std::swap(coef, aux.coef);
+        std::swap(dscratch, aux.dscratch);
+        std::swap(hld, aux.hld);
+        std::swap(basis_valid, aux.basis_valid);
+        std::swap(ctrl, aux.ctrl);
+        std::swap(h_ctrl, aux.h_ctrl);
+    }
     cudaEvent_t get_event() {
         if (!event_pool.empty()) {
             cudaEvent_t e = event_pool.back();

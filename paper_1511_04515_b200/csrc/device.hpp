@@ -114,7 +114,14 @@ struct Launch {
 void spmv(const Launch& L, const int* rowptr, const int* col, const double* val, int n_rows,
           const double* x, double* y, const Ctrl* ctrl, const double* vbase, long long ldv);
 void spmv_b2(const Launch& L, const int* rowptr, const int* col, const double* val, int n_rows,
-             const double* u_k, const double* u_k1, double h, double* t1, double* t2);
+             const double* u_k, const double* u_k1, double h, double* t1, double* t2, const double* Fk);
+void mos_residual(const Launch& L, int n_mos, const int4* nodes, const double* par,
+                  const double* op, const double* x, double* r, int n, const int* nptr,
+                  const int* nlist, double* F, const double* fsub);
+void absmax(const Launch& L, const double* v, int n, double* partials, unsigned int* done, double* out);
+void axpby(const Launch& L, const double* a, double alpha, const double* b, double* out, int n);
+void erc_update(const Launch& L, const double* w, const double* value, const double* u, int have_u,
+                double ih, double gamma, double* x, int n);
 void trsv(const Launch& L, bool upper, bool reverse, const TrsvArgs& a);
 void trsv_narrow(const Launch& L, bool upper, const NarrowArgs& a, int cluster, size_t smem);
 void trsv_wide(const Launch& L, bool upper, const TrsvArgs& a);

@@ -87,6 +87,21 @@ struct Factor {
 void lu_factor(const Csr& A, double pivot_tol, Factor& f);
 std::vector<int> min_degree_order(const Csr& A);
 
+// nonlinear devices (devices.hpp:14-36): per-MOSFET operating point frozen
+// at the linearization state, and the step-frozen linearization
+struct DeviceOp {
+    double vgs_ref = 0.0, vds_ref = 0.0, id_ref = 0.0, gm = 0.0, gds = 0.0;
+};
+struct Linearization {
+    Csr G, C;
+    std::vector<DeviceOp> op;
+};
+void mosfet_current(const Mosfet& p, double vgs, double vds, double& id, double& gm, double& gds);
+void evaluate(const System& sys, const std::vector<double>& x, Linearization& lin);
+std::vector<double> residual_F(const System& sys, const Linearization& lin, const std::vector<double>& x);
+std::vector<double> lu_solve_host(const Factor& f, const std::vector<double>& b);
+std::vector<double> dc_solve(const System& sys);
+
 // host-side vector helpers with the reference's exact semantics (vec.hpp)
 double norm2(const std::vector<double>& a);
 double norm_inf(const std::vector<double>& a);

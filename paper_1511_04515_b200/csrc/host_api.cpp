@@ -74,6 +74,7 @@ void exg_system_free(exg_system* s) { delete s; }
 int exg_system_n(const exg_system* s) { return s->sys.n; }
 int exg_system_n_nodes(const exg_system* s) { return s->sys.n_nodes; }
 int exg_system_n_inputs(const exg_system* s) { return s->sys.n_inputs(); }
+int exg_system_n_mos(const exg_system* s) { return static_cast<int>(s->sys.mos.size()); }
 
 exg_status exg_system_csr(const exg_system* s, int which, int* n_rows, int* n_cols, int* nnz,
                           const int** rowptr, const int** col, const double** val) {
@@ -119,6 +120,47 @@ exg_status exg_sources_eval(const exg_system* s, double t, double* u) {
     HOST_GUARD_BEGIN
     const auto v = exg::eval_sources(s->sys, t);
     std::memcpy(u, v.data(), sizeof(double) * v.size());
+    HOST_GUARD_END
+}
+
+exg_status exg_dc_solve(const exg_system* s, double* x) {
+    HOST_GUARD_BEGIN
+    const auto v = exg::dc_solve(s->sys);
+    std::memcpy(x, v.data(), sizeof(double) * v.size());
+    HOST_GUARD_END
+}
+
+exg_status exg_linearize(const exg_system* s, const double* x, int which, int* nnz, int* rowptr, int* col,
+                         double* val, double* op5) {
+    HOST_GUARD_BEGIN
+    exg::Linearization lin;
+    exg::evaluate(s->sys, std::vector<double>(x, x + s->sys.n), lin);
+    if (which != 0 && which != 1) throw exg::Error{EXG_E_CONTRACT, "linearize: which must be C or G"};
+    const exg::Csr& A = which == 0 ? lin.C : lin.G;
+    *nnz = A.nnz();
+    if (rowptr) {
+        std::memcpy(rowptr, A.rowptr.data(), sizeof(int) * (A.n_rows + 1));
+        std::memcpy(col, A.col.data(), sizeof(int) * A.nnz());
+        std::memcpy(val, A.val.data(), sizeof(double) * A.nnz());
+    }
+    if (op5)
+        for (size_t i = 0; i < lin.op.size(); ++i) {
+            op5[5 * i] = lin.op[i].vgs_ref;
+            op5[5 * i + 1] = lin.op[i].vds_ref;
+            op5[5 * i + 2] = lin.op[i].id_ref;
+            op5[5 * i + 3] = lin.op[i].gm;
+            op5[5 * i + 4] = lin.op[i].gds;
+        }
+    HOST_GUARD_END
+}
+
+exg_status exg_residual_F_host(const exg_system* s, const double* x_ref, const double* x, double* F) {
+    HOST_GUARD_BEGIN
+    const int n = s->sys.n;
+    exg::Linearization lin;
+    exg::evaluate(s->sys, std::vector<double>(x_ref, x_ref + n), lin);
+    const auto v = exg::residual_F(s->sys, lin, std::vector<double>(x, x + n));
+    std::memcpy(F, v.data(), sizeof(double) * n);
     HOST_GUARD_END
 }
 

@@ -78,12 +78,12 @@ __global__ void __launch_bounds__(kSpmvWarps * 32)
     k_spmv_b2(const int* __restrict__ rowptr, const int* __restrict__ col,
               const double* __restrict__ val, int n_rows, const double* __restrict__ u_k,
               const double* __restrict__ u_k1, double h, double* __restrict__ t1,
-              double* __restrict__ t2) {
+              double* __restrict__ t2, const double* __restrict__ Fk) {
     __shared__ int s_col[kSpmvWarps][kSpmvCap];
     __shared__ double s_val[kSpmvWarps][kSpmvCap];
     const int wg = blockIdx.x * kSpmvWarps + (threadIdx.x >> 5);
     spmv_warp_rows(rowptr, col, val, n_rows, wg, [&](int c) { return u_k[c]; },
-                   [&](int r, double s) { t1[r] = 0.0 + 1.0 * s; }, s_col, s_val);
+                   [&](int r, double s) { t1[r] = (Fk ? Fk[r] : 0.0) + 1.0 * s; }, s_col, s_val);
     const double ih = 1.0 / h;
     spmv_warp_rows(rowptr, col, val, n_rows, wg,
                    [&](int c) { return (u_k1[c] + -1.0 * u_k[c]) * ih; },
@@ -1446,7 +1446,8 @@ __global__ void __launch_bounds__(256)
         for (int b = 0; b < n_part; ++b) xinf = xinf < partials[n_part + b] ? partials[n_part + b] : xinf;
         const double beta = sqrt(tot);
         int go = 1;
-        if (er_mode && beta <= 1e-9 * (1.0 + xinf)) go = 0;  // equilibrium early-out
+        if (er_mode == 1 && beta <= 1e-9 * (1.0 + xinf)) go = 0;  // equilibrium early-out
+        if (er_mode == 2 && beta == 0.0) go = 0;  // error/correction: zero w skips the MEVP
         if (go && beta == 0.0) go = -1;                          // ZeroStartVectorError
         s_beta = beta;
         s_go = go;
@@ -2004,6 +2005,145 @@ __global__ void k_basis_residual_final(Ctrl* c, double* out) {
 }
 
 // ============================================================================
+// Nonlinear devices (config 4): residual_F (devices.cpp:202-233) on the
+// device.  k_mos_r evaluates every MOSFET at x (mosfet_current,
+// devices.cpp:31-66, same arithmetic) and forms r = gm*vgs + gds*vds - id
+// with the frozen operating point; k_node_gather adds the contributions of
+// each node in device order (F[d] += r, F[s] -= r), so the sum order — and
+// the result — is the reference's.
+// ============================================================================
+__device__ __forceinline__ void mos_current(double vth, double kp, double lam, double w, double l,
+                                            double vgs, double vds, double& id, double& gm,
+                                            double& gds) {
+    bool swapped = false;
+    if (vds < 0.0) {
+        vgs = vgs - vds;
+        vds = -vds;
+        swapped = true;
+    }
+    const double k = kp * w / l;
+    const double vov = vgs - vth;
+    if (vov <= 0.0) {
+        id = 0.0;
+        gm = 0.0;
+        gds = 0.0;
+    } else if (vds >= vov) {
+        const double clm = 1.0 + lam * vds;
+        id = 0.5 * k * vov * vov * clm;
+        gm = k * vov * clm;
+        gds = 0.5 * k * vov * vov * lam;
+    } else {
+        const double clm = 1.0 + lam * vds;
+        const double q = vov * vds - 0.5 * vds * vds;
+        id = k * q * clm;
+        gm = k * vds * clm;
+        gds = k * (vov - vds) * clm + k * q * lam;
+    }
+    if (swapped) {
+        const double gm_s = gm;
+        const double gds_s = gds;
+        id = -id;
+        gm = -gm_s;
+        gds = gm_s + gds_s;
+    }
+}
+
+__global__ void __launch_bounds__(256)
+    k_mos_r(int n_mos, const int4* __restrict__ nodes, const double* __restrict__ par,
+            const double* __restrict__ op, const double* __restrict__ x, double* __restrict__ r) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_mos) return;
+    const int4 nd = nodes[i];  // d, g, s, b
+    const double vd = nd.x < 0 ? 0.0 : x[nd.x];
+    const double vg = nd.y < 0 ? 0.0 : x[nd.y];
+    const double vs = nd.z < 0 ? 0.0 : x[nd.z];
+    const double vgs = vg - vs;
+    const double vds = vd - vs;
+    const double* p = par + 6 * i;  // vth kp lambda w l pmos
+    const double sign = p[5] != 0.0 ? -1.0 : 1.0;
+    double id, gm, gds;
+    mos_current(p[0], p[1], p[2], p[3], p[4], sign * vgs, sign * vds, id, gm, gds);
+    id *= sign;
+    const double gm0 = op[5 * i + 3], gds0 = op[5 * i + 4];
+    r[i] = gm0 * vgs + gds0 * vds - id;
+}
+
+// F[i] = sum of the node's contributions in device order; with fsub: the
+// result is F - fsub (deltaF = residual_F(x_next) - F_k, integrate.cpp:435)
+__global__ void __launch_bounds__(256)
+    k_node_gather(int n, const int* __restrict__ ptr, const int* __restrict__ list,
+                  const double* __restrict__ r, double* __restrict__ F,
+                  const double* __restrict__ fsub) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double f = 0.0;
+    for (int k = ptr[i]; k < ptr[i + 1]; ++k) {
+        const int e = list[k];
+        if (e >= 0)
+            f += r[e];
+        else
+            f -= r[-1 - e];
+    }
+    if (fsub) f = f + -1.0 * fsub[i];
+    F[i] = f;
+}
+
+// ||v||_inf (exact: max is order independent), two-stage, and elementwise ops
+// of the nonlinear error / correction (integrate.cpp:267-298)
+__global__ void __launch_bounds__(256)
+    k_absmax(const double* __restrict__ v, int n, double* __restrict__ partials,
+             unsigned int* done, double* out) {
+    __shared__ double sh[32];
+    __shared__ bool s_last;
+    double m = 0.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const double a = fabs(v[i]);
+        m = m < a ? a : m;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const double t = __shfl_down_sync(0xffffffffu, m, o);
+        m = m < t ? t : m;
+    }
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double b = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) b = b < sh[w] ? sh[w] : b;
+        partials[blockIdx.x] = b;
+        __threadfence();
+        s_last = atomicAdd(done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last || threadIdx.x) return;
+    double b = 0.0;
+    for (int k = 0; k < (int)gridDim.x; ++k) {
+        const double t = ld_cg(partials + k);
+        b = b < t ? t : b;
+    }
+    *out = b;
+    *done = 0u;
+}
+
+// out = a + alpha * b  (sub: alpha = -1; axpy)
+__global__ void k_axpby(const double* __restrict__ a, double alpha, const double* __restrict__ b,
+                        double* __restrict__ out, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = a[i] + alpha * b[i];
+}
+
+// d = gamma * (w + (1/h) * (value + (-1.0 * u)));  x += 1.0 * d
+__global__ void k_erc_update(const double* __restrict__ w, const double* __restrict__ value,
+                             const double* __restrict__ u, int have_u, double ih, double gamma,
+                             double* __restrict__ x, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double d = w[i];
+    if (have_u) d += ih * (value[i] + -1.0 * u[i]);
+    d *= gamma;
+    x[i] += 1.0 * d;
+}
+
+// ============================================================================
 // launch wrappers
 // ============================================================================
 namespace {
@@ -2024,10 +2164,10 @@ void spmv(const Launch& L, const int* rowptr, const int* col, const double* val,
 }
 
 void spmv_b2(const Launch& L, const int* rowptr, const int* col, const double* val, int n_rows,
-             const double* u_k, const double* u_k1, double h, double* t1, double* t2) {
+             const double* u_k, const double* u_k1, double h, double* t1, double* t2, const double* Fk) {
     if (n_rows <= 0) return;
     const unsigned int grid = cdiv(cdiv(n_rows, 32), kSpmvWarps);
-    k_spmv_b2<<<grid, kSpmvWarps * 32, 0, L.stream>>>(rowptr, col, val, n_rows, u_k, u_k1, h, t1, t2);
+    k_spmv_b2<<<grid, kSpmvWarps * 32, 0, L.stream>>>(rowptr, col, val, n_rows, u_k, u_k1, h, t1, t2, Fk);
     count(L);
 }
 
@@ -2260,6 +2400,31 @@ void combine(const Launch& L, const double* V, long long ldv, const double* coef
              double* out, const Ctrl* ctrl, int mode, const double* xk, const double* gb,
              const double* start_v, double h) {
     k_combine<<<cdiv(n, 256), 256, 0, L.stream>>>(V, ldv, coef, n, out, ctrl, mode, xk, gb, start_v, h);
+    count(L);
+}
+
+void mos_residual(const Launch& L, int n_mos, const int4* nodes, const double* par,
+                  const double* op, const double* x, double* r, int n, const int* nptr,
+                  const int* nlist, double* F, const double* fsub) {
+    if (n_mos > 0) k_mos_r<<<cdiv(n_mos, 256), 256, 0, L.stream>>>(n_mos, nodes, par, op, x, r);
+    k_node_gather<<<cdiv(n, 256), 256, 0, L.stream>>>(n, nptr, nlist, r, F, fsub);
+    count(L, 2);
+}
+
+void absmax(const Launch& L, const double* v, int n, double* partials, unsigned int* done, double* out) {
+    const unsigned int g = std::min<unsigned int>(cdiv(n, 256), 1024);
+    k_absmax<<<g, 256, 0, L.stream>>>(v, n, partials, done, out);
+    count(L);
+}
+
+void axpby(const Launch& L, const double* a, double alpha, const double* b, double* out, int n) {
+    k_axpby<<<cdiv(n, 256), 256, 0, L.stream>>>(a, alpha, b, out, n);
+    count(L);
+}
+
+void erc_update(const Launch& L, const double* w, const double* value, const double* u, int have_u,
+                double ih, double gamma, double* x, int n) {
+    k_erc_update<<<cdiv(n, 256), 256, 0, L.stream>>>(w, value, u, have_u, ih, gamma, x, n);
     count(L);
 }
 

@@ -9,6 +9,13 @@
 // (exg::lu_factor, bit-identical to exsim::lu_factor) and uploaded; the
 // reference re-factorizes per step with identical results, which
 // ref_transient_cached reproduces on the oracle side.
+//
+// Nonlinear circuits (MOSFETs, config 4): per step the host re-linearizes at
+// x_k (exg::evaluate == exsim::evaluate), factorizes G_k (bit-identical LU) and
+// uploads G_k, C_k, the factors and the operating points; the device runs
+// er_begin (with F(x_k) stamped on the device), er_eval and the nonlinear
+// error / ER-C correction MEVPs of every rejection retry
+// (integrate.cpp:417-447).  The DC point is exg::dc_solve (integrate.cpp:92).
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -50,6 +57,166 @@ void chk(exg_ctx* ctx, exg_status st) {
     }
 }
 
+
+std::vector<int> record_list(const exg::System& sys, const int* rec_idx, int n_rec) {
+    std::vector<int> rec;
+    if (n_rec == 0)
+        for (int i = 0; i < sys.n; ++i) rec.push_back(i);
+    else
+        rec.assign(rec_idx, rec_idx + n_rec);
+    for (int i : rec)
+        if (i < 0 || i >= sys.n) throw Fail{EXG_E_CONTRACT, "unknown record node"};
+    return rec;
+}
+
+void upload_linearization(exg_ctx* ctx, const exg::Linearization& lin, const exg::Factor& f, bool with_op,
+                          bool op_only = false) {
+    if (!op_only) {
+        chk(ctx, exg_set_csr(ctx, EXG_MAT_C, lin.C.n_rows, lin.C.n_cols, lin.C.nnz(), lin.C.rowptr.data(),
+                             lin.C.col.data(), lin.C.val.data()));
+        chk(ctx, exg_set_csr(ctx, EXG_MAT_G, lin.G.n_rows, lin.G.n_cols, lin.G.nnz(), lin.G.rowptr.data(),
+                             lin.G.col.data(), lin.G.val.data()));
+        chk(ctx, exg_set_factors(ctx, f.n, f.L.rowptr.data(), f.L.col.data(), f.L.val.data(), f.U.rowptr.data(),
+                                 f.U.col.data(), f.U.val.data(), f.row_perm.data(), f.col_perm.data()));
+    }
+    if (!with_op && !op_only) return;
+    std::vector<double> op(5 * lin.op.size());
+    for (size_t i = 0; i < lin.op.size(); ++i) {
+        op[5 * i] = lin.op[i].vgs_ref;
+        op[5 * i + 1] = lin.op[i].vds_ref;
+        op[5 * i + 2] = lin.op[i].id_ref;
+        op[5 * i + 3] = lin.op[i].gm;
+        op[5 * i + 4] = lin.op[i].gds;
+    }
+    chk(ctx, exg_set_oppoints(ctx, op.data()));
+}
+
+// integrate.cpp:368-480 with nonlinear devices
+exg_status transient_nonlinear(exg_ctx* ctx, const exg::System& sys, const exg_step_control* ctl,
+                               double t_stop, const int* rec_idx, int n_rec, exg_tran_result** out) {
+    using clock = std::chrono::steady_clock;
+    auto* res = new exg_tran_result();
+    std::unique_ptr<exg_tran_result> guard(res);
+    const std::vector<int> rec = record_list(sys, rec_idx, n_rec);
+    res->n_rec = static_cast<int>(rec.size());
+    const int n = sys.n;
+    const int ni = sys.n_inputs();
+    const bool erc = ctl->method == EXG_METHOD_ERC;
+
+    auto t0 = clock::now();
+    std::vector<double> x;
+    try {
+        x = exg::dc_solve(sys);
+    } catch (const exg::Error& e) {
+        throw Fail{e.status, e.what};
+    }
+    auto t1 = clock::now();
+    res->dc_s = std::chrono::duration<double>(t1 - t0).count();
+    auto emit_host = [&](double t, const std::vector<double>& xv) {
+        res->times.push_back(t);
+        for (int i : rec) res->samples.push_back(xv[i]);
+    };
+    emit_host(0.0, x);
+
+    const std::vector<double> bps = exg::source_breakpoints(sys, 0.0, t_stop);
+    const double hint = sys.opts.has_tran && sys.opts.tran_step > 0.0 ? sys.opts.tran_step : t_stop / 100.0;
+    double h_nominal = ctl->h_init > 0.0 ? ctl->h_init : hint;
+    h_nominal = std::min(h_nominal, ctl->hmax);
+    const double hmin_eff = ctl->hmin > 0.0 ? ctl->hmin : t_stop * 1e-15;
+    const double t_tiny = t_stop * 1e-12;
+    exg_mevp_cfg cfg{ctl->eps, ctl->m_max, 1, 1e-12};
+
+    // B is constant; G_k / C_k / factors / operating points change per step
+    chk(ctx, exg_set_csr(ctx, EXG_MAT_B, sys.B.n_rows, sys.B.n_cols, sys.B.nnz(), sys.B.rowptr.data(),
+                         sys.B.col.data(), sys.B.val.data()));
+    bool devices_set = false;
+    double lu_s = 0.0;
+    double t = 0.0;
+    while (t < t_stop - t_tiny) {
+        const double seg_end = std::min(next_breakpoint_after(bps, t), t_stop);
+        double h_try = std::min(h_nominal, seg_end - t);
+        if (seg_end - t - h_try < t_tiny) h_try = seg_end - t;
+        h_try = std::max(h_try, std::min(hmin_eff, seg_end - t));
+
+        auto ta = clock::now();
+        exg::Linearization lin;
+        exg::Factor f;
+        try {
+            exg::evaluate(sys, x, lin);
+            exg::lu_factor(lin.G, 0.1, f);
+        } catch (const exg::Error& e) {
+            throw Fail{e.status, e.what};
+        }
+        lu_s += std::chrono::duration<double>(clock::now() - ta).count();
+        upload_linearization(ctx, lin, f, devices_set);
+        if (!devices_set) {  // device tables (after the first set_factors fixes n)
+            std::vector<int> nodes(4 * sys.mos.size());
+            std::vector<double> par(6 * sys.mos.size());
+            for (size_t i = 0; i < sys.mos.size(); ++i) {
+                const exg::Mosfet& m = sys.mos[i];
+                for (int j = 0; j < 4; ++j) nodes[4 * i + j] = m.nodes[j];
+                par[6 * i] = m.vth;
+                par[6 * i + 1] = m.kp;
+                par[6 * i + 2] = m.lambda;
+                par[6 * i + 3] = m.w;
+                par[6 * i + 4] = m.l;
+                par[6 * i + 5] = m.pmos ? 1.0 : 0.0;
+            }
+            chk(ctx, exg_set_devices(ctx, static_cast<int>(sys.mos.size()), nodes.data(), par.data()));
+            devices_set = true;
+            upload_linearization(ctx, lin, f, false, true);
+        }
+
+        const std::vector<double> u_k = exg::eval_sources(sys, t);
+        const std::vector<double> u_k1 = exg::eval_sources(sys, t + h_try);
+        chk(ctx, exg_memcpy(ctx, ctx->xk, x.data(), sizeof(double) * n, cudaMemcpyHostToDevice));
+        if (ni) {
+            chk(ctx, exg_memcpy(ctx, ctx->u_k, u_k.data(), sizeof(double) * ni, cudaMemcpyHostToDevice));
+            chk(ctx, exg_memcpy(ctx, ctx->u_k1, u_k1.data(), sizeof(double) * ni, cudaMemcpyHostToDevice));
+        }
+        chk(ctx, exg_er_begin(ctx, ctx->xk, ctx->u_k, ctx->u_k1, h_try, EXG_PTR_DEVICE));
+
+        int rejects = 0;
+        double err_norm = 0.0;
+        while (true) {
+            int m = -1;
+            chk(ctx, exg_er_eval(ctx, h_try, &cfg, nullptr, &m, nullptr, EXG_PTR_DEVICE));
+            if (m >= 0) res->dims.push_back(m);
+            int dims[2], nd = 0;
+            err_norm = 0.0;
+            chk(ctx, exg_er_nonlinear(ctx, h_try, &cfg, erc ? 1 : 0, ctl->gamma, &err_norm, dims, &nd));
+            for (int i = 0; i < nd; ++i) res->dims.push_back(dims[i]);
+            if (ctl->fixed_step || err_norm <= ctl->err_budget) break;
+            ++rejects;
+            if (rejects > ctl->max_rejects)
+                throw Fail{EXG_E_STEP_FAILURE, "transient: too many rejections at t=" + std::to_string(t)};
+            h_try *= ctl->alpha;
+            if (h_try < hmin_eff)
+                throw Fail{EXG_E_STEP_FAILURE, "transient: step size below HMIN at t=" + std::to_string(t)};
+        }
+        res->t.push_back(t + h_try);
+        res->h.push_back(h_try);
+        res->lu.push_back(1);
+        res->rej.push_back(rejects);
+        res->err.push_back(err_norm);
+        res->dims_off.push_back(static_cast<int>(res->dims.size()));
+
+        chk(ctx, exg_memcpy(ctx, x.data(), ctx->xnext, sizeof(double) * n, cudaMemcpyDeviceToHost));
+        t += h_try;
+        emit_host(t, x);
+
+        const bool grow = !ctl->fixed_step &&
+                          (ctl->grow_only_on_clean ? rejects == 0 : rejects < ctl->grow_threshold);
+        const bool clamped = h_try < h_nominal * (1.0 - 1e-12);
+        if (rejects > 0) h_nominal = h_try;
+        if (grow) h_nominal = std::min(ctl->beta * (clamped && rejects == 0 ? h_nominal : h_try), ctl->hmax);
+    }
+    res->lu_s = lu_s;
+    res->loop_s = std::chrono::duration<double>(clock::now() - t1).count();
+    *out = guard.release();
+    return EXG_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -60,8 +227,10 @@ exg_status exg_transient(exg_ctx* ctx, const exg_system* sp, const exg_step_cont
     try {
         const exg::System& sys = sp->sys;
         if (t_stop <= 0.0) throw Fail{EXG_E_CONTRACT, "transient: t_stop must be positive"};
-        if (!sys.mos.empty())
-            throw Fail{EXG_E_CONTRACT, "transient: nonlinear devices are not on the device path yet"};
+        if (!sys.mos.empty()) {
+            *out = nullptr;
+            return transient_nonlinear(ctx, sys, ctl, t_stop, rec_idx, n_rec, out);
+        }
         auto* res = new exg_tran_result();
         std::unique_ptr<exg_tran_result> guard(res);
         std::vector<int> rec;

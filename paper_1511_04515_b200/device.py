@@ -159,6 +159,32 @@ class Context:
                                       h, C.byref(cfg), xn.ctypes.data, C.byref(m), F.EXG_PTR_HOST))
         return xn, m.value
 
+    # ---- nonlinear devices (config 4)
+    def set_devices(self, sys: System):
+        """MOSFET table of `sys` (devices.cpp:122-167 device data) onto the device."""
+        elems, _, _, _, models = sys.elements()
+        nodes, par = [], []
+        for e in elems:
+            if e.kind != F.EXG_EL_M:
+                continue
+            m = models[e.aux]
+            nodes.append([sys.unknown_of_label(e.nodes[j]) if e.nodes[j] >= 0 else -1 for j in range(4)])
+            par.append([m.vth, m.kp, m.lam, m.w, m.l, float(m.pmos)])
+        nodes = np.ascontiguousarray(nodes, np.int32).reshape(-1, 4)
+        par = np.ascontiguousarray(par, np.float64).reshape(-1, 6)
+        self._check(F.lib.exg_set_devices(self._h, nodes.shape[0], F.as_ptr(nodes, C.c_int),
+                                          F.as_ptr(par, C.c_double)))
+
+    def set_oppoints(self, op):
+        op = F.f64(op)
+        self._check(F.lib.exg_set_oppoints(self._h, F.as_ptr(op, C.c_double)))
+
+    def residual_F(self, x) -> np.ndarray:
+        x = F.f64(x)
+        out = np.zeros(self.n)
+        self._check(F.lib.exg_residual_F(self._h, x.ctypes.data, out.ctypes.data, F.EXG_PTR_HOST))
+        return out
+
     def counters(self) -> F.exg_counters:
         c = F.exg_counters()
         self._check(F.lib.exg_counters_get(self._h, C.byref(c)))

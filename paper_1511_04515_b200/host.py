@@ -141,6 +141,42 @@ class System:
         F.lib.exg_breakpoints(self._h, t0, t1, F.as_ptr(out, C.c_double), cnt)
         return out[:cnt]
 
+    @property
+    def n_mos(self) -> int:
+        return F.lib.exg_system_n_mos(self._h)
+
+    def dc_solve(self) -> np.ndarray:
+        """exsim::dc_solve (integrate.cpp:92-115), bit-identical."""
+        x = np.zeros(self.n)
+        _check(F.lib.exg_dc_solve(self._h, F.as_ptr(x, C.c_double)))
+        return x
+
+    def linearize(self, x):
+        """exsim::evaluate (devices.cpp:122-200): (C_k, G_k, op[n_mos, 5])."""
+        x = F.f64(x)
+        out = []
+        for which in (F.EXG_MAT_C, F.EXG_MAT_G):
+            nnz = C.c_int()
+            _check(F.lib.exg_linearize(self._h, F.as_ptr(x, C.c_double), which, C.byref(nnz),
+                                       None, None, None, None))
+            rp = np.zeros(self.n + 1, np.int32)
+            ci = np.zeros(nnz.value, np.int32)
+            va = np.zeros(nnz.value)
+            op = np.zeros((self.n_mos, 5))
+            _check(F.lib.exg_linearize(self._h, F.as_ptr(x, C.c_double), which, C.byref(nnz),
+                                       F.as_ptr(rp, C.c_int), F.as_ptr(ci, C.c_int),
+                                       F.as_ptr(va, C.c_double), F.as_ptr(op, C.c_double)))
+            out.append((Csr(self.n, self.n, rp, ci, va), op))
+        return out[0][0], out[1][0], out[1][1]
+
+    def residual_F(self, x_ref, x) -> np.ndarray:
+        """exsim::residual_F(evaluate(x_ref), x) (devices.cpp:202-233)."""
+        x_ref, x = F.f64(x_ref), F.f64(x)
+        out = np.zeros(self.n)
+        _check(F.lib.exg_residual_F_host(self._h, F.as_ptr(x_ref, C.c_double), F.as_ptr(x, C.c_double),
+                                         F.as_ptr(out, C.c_double)))
+        return out
+
     def step_control(self) -> F.exg_step_control:
         c = F.exg_step_control()
         _check(F.lib.exg_step_control_from(self._h, C.byref(c)))

@@ -208,3 +208,32 @@ def test_mevp_dense_oracle_20():
     J = -np.linalg.solve(Cm.to_dense(), G.to_dense())
     want = expm(J) @ v
     assert np.linalg.norm(got - want) <= 10 * 1e-7 * np.linalg.norm(v)
+
+
+@pytest.mark.parametrize("kw", [dict(width=12, chains=4, stages=4), dict(width=20, chains=16, stages=8)],
+                         ids=["12x12-4x4", "20x20-16x8"])
+def test_residual_F_bit_identical(ref, kw):
+    """Device MOSFET re-evaluation + per-node gather (devices.cpp:202-233)
+    against exsim::residual_F: bit-identical."""
+    s = ex.System.generate(4, **kw)
+    rh = ref_system(ref, s)
+    try:
+        x_ref = ref.dc_solve(rh)
+        rng = np.random.default_rng(5)
+        xs = [x_ref + rng.normal(0.0, sc, s.n) for sc in (1e-3, 0.1, 0.5)]
+        wants = [ref.residual_F(rh, x_ref, x) for x in xs]
+    finally:
+        ref.system_free(rh)
+    Ck, Gk, op = s.linearize(x_ref)
+    f = ex.lu_factor(Gk)
+    with Context(0) as c:
+        c.set_csr(F.EXG_MAT_C, Ck)
+        c.set_csr(F.EXG_MAT_G, Gk)
+        c.set_csr(F.EXG_MAT_B, s.B)
+        c.set_factors(f)
+        c.set_devices(s)
+        c.set_oppoints(op)
+        for x, want in zip(xs, wants):
+            got = c.residual_F(x)
+            assert bit_equal(got, want)
+            assert np.abs(want).max() > 0.0

@@ -85,3 +85,58 @@ def test_configs_vs_cached_oracle(ref, cfg, kw, t_stop, mode, weight):
     with Context(0, trsv_mode=mode, weight_mode=weight) as c:
         got = c.transient(s, ctl, t_stop, rec)
     compare(got, want)
+
+
+# ---- config 4: nonlinear inverter chains on an RC grid ----
+C4_CUTS = [dict(width=12, chains=4, stages=4), dict(width=20, chains=16, stages=8)]
+
+
+def compare_nonlinear(got, want):
+    """Nonlinear bar: the same accept/reject sequence (rejects per step), step
+    times, Krylov dimensions of every MEVP (solution, error, correction), and
+    waveforms within TOL of full scale."""
+    assert np.array_equal(got.rejects, want["rejects"]), "rejection sequence differs"
+    assert np.array_equal(got.t, want["t"]), "accepted step times differ"
+    return compare(got, want)
+
+
+@pytest.mark.parametrize("kw", C4_CUTS, ids=["12x12-4x4", "20x20-16x8"])
+@pytest.mark.parametrize("method", [F.EXG_METHOD_ER, F.EXG_METHOD_ERC], ids=["er", "erc"])
+def test_config4_vs_transient_as_shipped(ref, kw, method):
+    s = ex.System.generate(4, **kw)
+    ctl = s.step_control()
+    ctl.method = method
+    rec = probes(s)
+    rh = ref_system(ref, s)
+    try:
+        want = ref.transient(rh, ctl, s.options().tran_stop, rec, method=method)
+    finally:
+        ref.system_free(rh)
+    with Context(0, trsv_mode=F.EXG_TRSV_EXACT, weight_mode=F.EXG_WEIGHT_APPLY) as c:
+        got = c.transient(s, ctl, s.options().tran_stop, rec)
+    assert int(np.sum(got.rejects)) > 0, "cut exercises no rejection"
+    compare_nonlinear(got, want)
+    # the MEVP values differ from the reference's in the last bits (MGS dot
+    # products reduce in another order), so the estimates agree to rounding
+    np.testing.assert_allclose(got.err_norm, want["err"], rtol=1e-6, atol=1e-20)
+
+
+@pytest.mark.parametrize("method", [F.EXG_METHOD_ER, F.EXG_METHOD_ERC], ids=["er", "erc"])
+def test_config4_fast_mode_close(ref, method):
+    """FAST triangular solves reorder the sums; the step sequence may only
+    differ where an error estimate sits within rounding of the budget, so the
+    check is the waveform at the shared final time."""
+    s = ex.System.generate(4, **C4_CUTS[0])
+    ctl = s.step_control()
+    ctl.method = method
+    rec = probes(s)
+    rh = ref_system(ref, s)
+    try:
+        want = ref.transient(rh, ctl, s.options().tran_stop, rec, method=method)
+    finally:
+        ref.system_free(rh)
+    with Context(0, trsv_mode=F.EXG_TRSV_FAST, weight_mode=F.EXG_WEIGHT_APPLY) as c:
+        got = c.transient(s, ctl, s.options().tran_stop, rec)
+    assert got.times[-1] == want["times"][-1]
+    err = full_scale_err(got.samples[-1:], want["samples"][-1:])
+    assert err <= 1e-6, f"final-state full-scale error {err:.3e}"

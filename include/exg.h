@@ -60,6 +60,12 @@ enum { EXG_TRSV_EXACT = 0, EXG_TRSV_FAST = 1 };
 /* residual weight of the Arnoldi test: the reference's ||P^T L U Q^T v|| (APPLY,
  * krylov.cpp:238) or ||G v|| (GSPMV, the operator mevp_residual uses). */
 enum { EXG_WEIGHT_APPLY = 0, EXG_WEIGHT_GSPMV = 1 };
+/* Arnoldi loop execution: EAGER launches every iteration from the host and
+ * reads the control block back after each one; GRAPH runs the whole loop as
+ * one CUDA graph (a conditional WHILE node whose body is one iteration; the
+ * device decides when to stop) and reads the control block back once per
+ * MEVP.  Same kernels, same results. */
+enum { EXG_LOOP_GRAPH = 0, EXG_LOOP_EAGER = 1 };
 
 typedef struct exg_ctx exg_ctx;
 
@@ -84,6 +90,7 @@ typedef struct exg_mevp_info {
 typedef struct exg_options_dev {
     int32_t trsv_mode;   /* EXG_TRSV_* */
     int32_t weight_mode; /* EXG_WEIGHT_* */
+    int32_t loop_mode;   /* EXG_LOOP_* */
 } exg_options_dev;
 
 typedef struct exg_counters {
@@ -95,6 +102,10 @@ typedef struct exg_counters {
     int32_t u_levels;        /* of U */
     int64_t nnz_l;           /* off-diagonal entries stored on the device */
     int64_t nnz_u;
+    int64_t graph_launches;  /* Arnoldi-loop graph launches */
+    int64_t graph_builds;    /* graph captures + instantiations */
+    int32_t l_schedule;      /* level schedule of L: 0 ASAP, 1 ALAP */
+    int32_t u_schedule;      /* of U */
 } exg_counters;
 
 exg_status exg_create(int device, exg_ctx** out);

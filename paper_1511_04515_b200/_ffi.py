@@ -32,6 +32,7 @@ EXG_MAT_C, EXG_MAT_G, EXG_MAT_B = 0, 1, 2
 EXG_PTR_HOST, EXG_PTR_DEVICE = 0, 1
 EXG_TRSV_EXACT, EXG_TRSV_FAST = 0, 1
 EXG_WEIGHT_APPLY, EXG_WEIGHT_GSPMV = 0, 1
+EXG_LOOP_GRAPH, EXG_LOOP_EAGER = 0, 1
 EXG_METHOD_ER, EXG_METHOD_ERC = 1, 2
 
 EXG_EL_R, EXG_EL_C, EXG_EL_L, EXG_EL_V, EXG_EL_I, EXG_EL_M = range(6)
@@ -87,13 +88,15 @@ class exg_mevp_info(C.Structure):
 
 
 class exg_options_dev(C.Structure):
-    _fields_ = [("trsv_mode", C.c_int32), ("weight_mode", C.c_int32)]
+    _fields_ = [("trsv_mode", C.c_int32), ("weight_mode", C.c_int32), ("loop_mode", C.c_int32)]
 
 
 class exg_counters(C.Structure):
     _fields_ = [("kernel_launches", C.c_int64), ("arnoldi_iters", C.c_int64),
                 ("mevp_calls", C.c_int64), ("trsv_calls", C.c_int64), ("l_levels", C.c_int32),
-                ("u_levels", C.c_int32), ("nnz_l", C.c_int64), ("nnz_u", C.c_int64)]
+                ("u_levels", C.c_int32), ("nnz_l", C.c_int64), ("nnz_u", C.c_int64),
+                ("graph_launches", C.c_int64), ("graph_builds", C.c_int64),
+                ("l_schedule", C.c_int32), ("u_schedule", C.c_int32)]
 
 
 class exg_kernel_times(C.Structure):

@@ -100,6 +100,7 @@ void upload_csr(exg_ctx* c, DCsr& m, int n_rows, int n_cols, int nnz, const int*
 
 void ensure_vectors(exg_ctx* c, int n) {
     if (c->vec_n >= n && c->vin) return;
+    c->clear_graphs();
     dfree(c->partials);
     c->partials = dalloc<double>((size_t)std::max(8192, (n + 255) / 256 + 1024) + 2 * 4096);
     c->mgs_partials_off = (size_t)std::max(8192, (n + 255) / 256 + 1024);
@@ -123,6 +124,7 @@ void ensure_inputs(exg_ctx* c, int ni) {
 
 void ensure_krylov(exg_ctx* c, int mmax) {
     if (c->mmax_alloc >= mmax && c->V) return;
+    c->clear_graphs();
     const int n = c->n;
     dfree(c->V);
     dfree(c->hbar);
@@ -155,7 +157,7 @@ const DCsr& mat(exg_ctx* c, int which) {
 void solve_dev(exg_ctx* c, const double* b, double* final_out, double coef, const double* add,
                const Ctrl* ctrl) {
     const int n = c->n;
-    ck(cudaMemsetAsync(c->trsv_buf, 0xFF, kTrsvHdr + 6 * sizeof(double) * (size_t)n, c->stream), "memset");
+    exg::dev::fill_ones(c->L(), c->trsv_buf, kTrsvHdr + 6 * sizeof(double) * (size_t)n);
     unsigned int* tickets = reinterpret_cast<unsigned int*>(c->trsv_buf);
     double* y = reinterpret_cast<double*>(c->trsv_buf + kTrsvHdr);
     double* x = y + n;
@@ -193,7 +195,7 @@ void solve_dev(exg_ctx* c, const double* b, double* final_out, double coef, cons
             exg::dev::trsv(c->L(), upper, fast, a);
         } else {
             const TriPlan& P = c->plan[tri];
-            static const bool run_timing = getenv("EXG_RUN_TIMING") != nullptr;
+            const bool run_timing = getenv("EXG_RUN_TIMING") != nullptr && !c->capturing;
             std::vector<cudaEvent_t> rev;
             for (const TriPlan::Run& run : P.runs) {
                 if (run_timing) {
@@ -364,33 +366,102 @@ void mevp_dev(exg_ctx* c, const double* v, double h, const exg_mevp_cfg& cfg, in
     exg::dev::DenseArgs da{c->ctrl, c->hbar, c->hld, c->hinv, c->coef, c->dscratch, 0, 0, h};
     const bool gspmv = c->opt.weight_mode == EXG_WEIGHT_GSPMV;
     if (gspmv) mat(c, EXG_MAT_G);
+    // one Arnoldi iteration (krylov.cpp:118-168); every kernel takes j, m and
+    // the stop decision from the control block, so the same launches serve
+    // the eager loop and the graph body.  dense_m bounds the dimension the
+    // dense kernel will see (sizes its shared memory).
+    auto iteration = [&](int dense_m, unsigned long long cond) {
+        // w = -G^{-1}(C v_j)   (krylov.cpp:120-121)
+        cudaEvent_t p0 = c->prof_begin();
+        exg::dev::spmv(L, C.rowptr, C.col, C.val, C.n_rows, nullptr, c->t, c->ctrl, c->V, c->ldv);
+        c->prof_end(EXG_K_SPMV, p0);
+        solve_dev(c, c->t, c->w, -1.0, nullptr, c->ctrl);
+        cudaEvent_t p1 = c->prof_begin();
+        exg::dev::mgs(L, ma, blocks, K);
+        c->prof_end(EXG_K_MGS, p1);
+        cudaEvent_t p2 = c->prof_begin();
+        exg::dev::dense(L, da, dense_m);
+        c->prof_end(EXG_K_DENSE, p2);
+        cudaEvent_t p3 = c->prof_begin();
+        if (gspmv) {
+            const DCsr& G = c->mats[EXG_MAT_G];
+            exg::dev::spmv_norm(L, G.rowptr, G.col, G.val, n, c->V, c->ldv, c->partials, c->done,
+                                c->ctrl, 1, nullptr);
+        } else {
+            apply_dev(c, nullptr, nullptr, c->ctrl, nullptr);
+        }
+        exg::dev::iter_end(L, c->ctrl, cond);
+        c->prof_end(EXG_K_WEIGHT, p3);
+    };
     sync_ctrl(c);  // start-vector decisions (early-out, zero start)
     if (hc.status == 0 && !hc.converged) {
-        for (int jj = 0; jj < cfg.m_max; ++jj) {
-            // w = -G^{-1}(C v_j)   (krylov.cpp:120-121)
-            cudaEvent_t p0 = c->prof_begin();
-            exg::dev::spmv(L, C.rowptr, C.col, C.val, C.n_rows, nullptr, c->t, c->ctrl, c->V, c->ldv);
-            c->prof_end(EXG_K_SPMV, p0);
-            solve_dev(c, c->t, c->w, -1.0, nullptr, c->ctrl);
-            cudaEvent_t p1 = c->prof_begin();
-            exg::dev::mgs(L, ma, blocks, K);
-            c->prof_end(EXG_K_MGS, p1);
-            cudaEvent_t p2 = c->prof_begin();
-            exg::dev::dense(L, da, jj + 1);
-            c->prof_end(EXG_K_DENSE, p2);
-            cudaEvent_t p3 = c->prof_begin();
-            if (gspmv) {
-                const DCsr& G = c->mats[EXG_MAT_G];
-                exg::dev::spmv_norm(L, G.rowptr, G.col, G.val, n, c->V, c->ldv, c->partials, c->done,
-                                    c->ctrl, 1, nullptr);
-            } else {
-                apply_dev(c, nullptr, nullptr, c->ctrl, nullptr);
+        if (c->opt.loop_mode == EXG_LOOP_GRAPH && !c->profiling) {
+            // the whole loop as one graph launch: WHILE node, body = one
+            // iteration, condition set by k_iter_end on the device
+            exg_ctx::GraphKey key{};
+            const DCsr& G = c->mats[EXG_MAT_G];
+            const void* ps[] = {C.rowptr, C.col, C.val, G.rowptr, G.col, G.val, c->V, c->w, c->t,
+                                c->hbar, c->hinv, c->coef, c->dscratch, c->partials, c->bar,
+                                c->done, c->ctrl, c->trsv_buf, c->l_ptr, c->u_ptr, c->tmp, c->t3,
+                                c->v1, c->weight};
+            static_assert(sizeof(ps) / sizeof(ps[0]) <= 24, "graph key");
+            for (size_t i = 0; i < sizeof(ps) / sizeof(ps[0]); ++i) key.p[i] = ps[i];
+            const long long vs[] = {n, c->ldv, blocks, K, cfg.m_max, c->opt.trsv_mode, c->opt.weight_mode,
+                                    C.n_rows};
+            for (size_t i = 0; i < 8; ++i) key.v[i] = vs[i];
+            exg_ctx::ArnoldiGraph* g = nullptr;
+            for (auto& e : c->graphs)
+                if (!std::memcmp(&e.key, &key, sizeof key)) g = &e;
+            if (!g) {
+                exg_ctx::ArnoldiGraph ng;
+                ng.key = key;
+                ck(cudaGraphCreate(&ng.graph, 0), "graph create");
+                cudaGraphConditionalHandle hnd;
+                ck(cudaGraphConditionalHandleCreate(&hnd, ng.graph, 1, cudaGraphCondAssignDefault),
+                   "conditional handle");
+                cudaGraphNodeParams np{};
+                np.type = cudaGraphNodeTypeConditional;
+                np.conditional.handle = hnd;
+                np.conditional.type = cudaGraphCondTypeWhile;
+                np.conditional.size = 1;
+                cudaGraphNode_t node;
+                ck(cudaGraphAddNode(&node, ng.graph, nullptr, 0, &np), "conditional node");
+                cudaGraph_t body = np.conditional.phGraph_out[0];
+                const long long l0 = c->launches;
+                ck(cudaStreamBeginCaptureToGraph(c->stream, body, nullptr, nullptr, 0,
+                                                 cudaStreamCaptureModeThreadLocal), "begin capture");
+                c->capturing = true;
+                try {
+                    iteration(cfg.m_max, (unsigned long long)hnd);
+                } catch (...) {
+                    c->capturing = false;
+                    cudaGraph_t junk;
+                    cudaStreamEndCapture(c->stream, &junk);
+                    cudaGraphDestroy(ng.graph);
+                    throw;
+                }
+                c->capturing = false;
+                cudaGraph_t captured;
+                ck(cudaStreamEndCapture(c->stream, &captured), "end capture");
+                ng.body_kernels = c->launches - l0;
+                c->launches = l0;
+                ck(cudaGraphInstantiate(&ng.exec, ng.graph, 0), "graph instantiate");
+                c->cnt.graph_builds++;
+                c->graphs.push_back(ng);
+                g = &c->graphs.back();
             }
-            exg::dev::iter_end(L, c->ctrl);
-            c->prof_end(EXG_K_WEIGHT, p3);
-            c->cnt.arnoldi_iters++;
+            ck(cudaGraphLaunch(g->exec, c->stream), "graph launch");
+            c->cnt.graph_launches++;
             sync_ctrl(c);
-            if (hc.status || hc.converged) break;
+            c->cnt.arnoldi_iters += hc.arnoldi_iters;
+            c->launches += g->body_kernels * hc.arnoldi_iters;
+        } else {
+            for (int jj = 0; jj < cfg.m_max; ++jj) {
+                iteration(jj + 1, 0);
+                c->cnt.arnoldi_iters++;
+                sync_ctrl(c);
+                if (hc.status || hc.converged) break;
+            }
         }
     }
     ctrl_status(c);
@@ -787,6 +858,7 @@ void exg_destroy(exg_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
+    c->clear_graphs();
     for (DCsr& m : c->mats) {
         dfree(m.rowptr);
         dfree(m.col);
@@ -851,6 +923,7 @@ exg_status exg_set_csr(exg_ctx* c, int which, int n_rows, int n_cols, int nnz, c
     API_BEGIN
     if (which < 0 || which > 2 || n_rows < 0 || n_cols < 0 || nnz < 0 || rowptr[n_rows] != nnz)
         throw ApiError{EXG_E_CONTRACT, "exg_set_csr: bad matrix"};
+    c->clear_graphs();
     upload_csr(c, c->mats[which], n_rows, n_cols, nnz, rowptr, col, val);
     if (which == EXG_MAT_B) ensure_inputs(c, n_cols);
     API_END(c)
@@ -868,6 +941,7 @@ exg_status exg_set_factors(exg_ctx* c, int n, const int* Lp, const int* Li, cons
                            const int* col_perm) {
     API_BEGIN
     if (n <= 0) throw ApiError{EXG_E_CONTRACT, "exg_set_factors: empty factorization"};
+    c->clear_graphs();
     // split: L strictly lower (c < r; the unit diagonal is implicit, as
     // Factorization::solve skips c >= r), U strictly upper + diagonal
     std::vector<int> lp(n + 1, 0), up(n + 1, 0);
@@ -894,15 +968,74 @@ exg_status exg_set_factors(exg_ctx* c, int n, const int* Lp, const int* Li, cons
         }
         up[r + 1] = (int)uc.size();
     }
-    // level analysis (critical-path depth) and level-ordered row lists
-    std::vector<int> lev(n, 0);
-    int l_levels = 0, u_levels = 0;
-    for (int r = 0; r < n; ++r) {
-        int lv_ = 0;
-        for (int k = lp[r]; k < lp[r + 1]; ++k) lv_ = std::max(lv_, lev[lc[k]] + 1);
-        lev[r] = lv_;
-        l_levels = std::max(l_levels, lv_ + 1);
-    }
+    // level analysis and level-ordered row lists.  Two valid schedules per
+    // triangle: ASAP (level = longest dependency chain below the row) and
+    // ALAP (level = critical path - longest chain of dependents above it).
+    // Both have the same depth; they differ in where the thin levels fall.
+    // With a symmetric pattern ALAP of U mirrors ASAP of L: the separator
+    // chains become one long thin stretch (handled on one CTA, pick_schedule)
+    // instead of thin levels interleaved with thousands of half-wide ones.
+    auto asap = [&](bool upper_tri, std::vector<int>& lv_) {
+        const std::vector<int>& p_ = upper_tri ? up : lp;
+        const std::vector<int>& c_ = upper_tri ? uc : lc;
+        lv_.assign(n, 0);
+        int nl = 0;
+        for (int i = 0; i < n; ++i) {
+            const int r = upper_tri ? n - 1 - i : i;
+            int v = 0;
+            for (int k = p_[r]; k < p_[r + 1]; ++k) v = std::max(v, lv_[c_[k]] + 1);
+            lv_[r] = v;
+            nl = std::max(nl, v + 1);
+        }
+        return nl;
+    };
+    auto alap = [&](bool upper_tri, std::vector<int>& lv_) {
+        const std::vector<int>& p_ = upper_tri ? up : lp;
+        const std::vector<int>& c_ = upper_tri ? uc : lc;
+        std::vector<int> h(n, 0);  // longest chain of dependents above the row
+        int H = 0;
+        for (int i = 0; i < n; ++i) {
+            const int r = upper_tri ? i : n - 1 - i;  // dependents of r are already final
+            H = std::max(H, h[r]);
+            for (int k = p_[r]; k < p_[r + 1]; ++k) h[c_[k]] = std::max(h[c_[k]], h[r] + 1);
+        }
+        lv_.resize(n);
+        for (int r = 0; r < n; ++r) lv_[r] = H - h[r];
+        return H + 1;
+    };
+    // schedule cost model (µs): a thin level (<= 16 rows) costs one on-chip
+    // hand-off on the chain CTA, a wide level one L2 hand-off plus its bytes
+    auto sched_cost = [&](const std::vector<int>& lv_, int nl, bool upper_tri) {
+        const std::vector<int>& p_ = upper_tri ? up : lp;
+        std::vector<long long> rows(nl, 0), nz(nl, 0);
+        for (int r = 0; r < n; ++r) {
+            rows[lv_[r]]++;
+            nz[lv_[r]] += p_[r + 1] - p_[r];
+        }
+        double t = 0.0;
+        for (int q = 0; q < nl; ++q)
+            t += rows[q] <= 16 ? 0.2 : 0.5 + 12.0 * (double)nz[q] / 6.0e6;
+        return t;
+    };
+    const char* sched_env = getenv("EXG_LEVELS");  // asap | alap | auto (default)
+    const std::string sched = sched_env ? sched_env : "auto";
+    auto pick_schedule = [&](bool upper_tri, std::vector<int>& lv_) {
+        std::vector<int> a1, a2;
+        const int n1 = asap(upper_tri, a1);
+        if (sched == "asap") {
+            lv_.swap(a1);
+            return n1;
+        }
+        const int n2 = alap(upper_tri, a2);
+        if (sched == "alap" || sched_cost(a2, n2, upper_tri) < sched_cost(a1, n1, upper_tri)) {
+            lv_.swap(a2);
+            c->alap[upper_tri] = 1;
+            return n2;
+        }
+        lv_.swap(a1);
+        c->alap[upper_tri] = 0;
+        return n1;
+    };
     auto order_by = [n](const std::vector<int>& lv_, int nl, bool desc) {
         std::vector<int> cnt(nl + 1, 0), ord(n);
         for (int r = 0; r < n; ++r) cnt[lv_[r] + 1]++;
@@ -913,14 +1046,10 @@ exg_status exg_set_factors(exg_ctx* c, int n, const int* Lp, const int* Li, cons
             for (int r = n - 1; r >= 0; --r) ord[cnt[lv_[r]]++] = r;
         return ord;
     };
-    const std::vector<int> lord = order_by(lev, l_levels, false);
-    const std::vector<int> llev = lev;
-    for (int r = n - 1; r >= 0; --r) {
-        int lv_ = 0;
-        for (int k = up[r]; k < up[r + 1]; ++k) lv_ = std::max(lv_, lev[uc[k]] + 1);
-        lev[r] = lv_;  // reuse: U levels (only c > r are read, already final)
-        u_levels = std::max(u_levels, lv_ + 1);
-    }
+    std::vector<int> llev, lev;
+    const int l_levels = pick_schedule(false, llev);
+    const int u_levels = pick_schedule(true, lev);
+    const std::vector<int> lord = order_by(llev, l_levels, false);
     const std::vector<int> uord = order_by(lev, u_levels, true);
     // warp tasks over the level order: long rows alone, short rows 32 per task
     // Warp tasks over the level order.  A row with more than 32 off-diagonal
@@ -1021,6 +1150,8 @@ exg_status exg_set_factors(exg_ctx* c, int n, const int* Lp, const int* Li, cons
     ensure_vectors(c, n);
     c->cnt.l_levels = l_levels;
     c->cnt.u_levels = u_levels;
+    c->cnt.l_schedule = c->alap[0];
+    c->cnt.u_schedule = c->alap[1];
     c->cnt.nnz_l = (long long)lc.size();
     c->cnt.nnz_u = (long long)uc.size();
     c->mmax_alloc = 0;  // Krylov workspace re-sized on next use
@@ -1433,6 +1564,7 @@ exg_status exg_counters_reset(exg_ctx* c) {
     if (!c) return EXG_E_CONTRACT;
     c->launches = 0;
     c->cnt.arnoldi_iters = c->cnt.mevp_calls = c->cnt.trsv_calls = 0;
+    c->cnt.graph_launches = c->cnt.graph_builds = 0;
     return EXG_OK;
 }
 

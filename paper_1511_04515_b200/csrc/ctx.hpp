@@ -86,7 +86,30 @@ struct exg_ctx {
     exg_counters cnt{};
     std::string err;
     exg_status last = EXG_OK;
-    exg_options_dev opt{EXG_TRSV_EXACT, EXG_WEIGHT_APPLY};
+    exg_options_dev opt{EXG_TRSV_EXACT, EXG_WEIGHT_APPLY, EXG_LOOP_GRAPH};
+
+    // Arnoldi-loop graphs (EXG_LOOP_GRAPH), keyed by everything the loop body
+    // bakes in (buffer addresses, launch shapes, modes); dropped whenever a
+    // device buffer or the factor plan is replaced
+    struct GraphKey {
+        const void* p[24];
+        long long v[8];
+    };
+    struct ArnoldiGraph {
+        GraphKey key;
+        cudaGraph_t graph = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        long long body_kernels = 0;
+    };
+    std::vector<ArnoldiGraph> graphs;
+    bool capturing = false;
+    void clear_graphs() {
+        for (auto& g : graphs) {
+            if (g.exec) cudaGraphExecDestroy(g.exec);
+            if (g.graph) cudaGraphDestroy(g.graph);
+        }
+        graphs.clear();
+    }
 
     DCsr mats[3];  // C, G, B
     // factors
@@ -98,6 +121,7 @@ struct exg_ctx {
     TriPlan plan[2];  // FAST-mode runs of L and U
     int4* meta[2] = {nullptr, nullptr};  // level-order row metadata of L and U
     int cluster = 16;
+    int alap[2] = {0, 0};  // level schedule chosen per triangle (1 = ALAP)
     int n_tasks[4] = {0, 0, 0, 0};
     unsigned long long *trace_l = nullptr, *trace_u = nullptr;
     unsigned long long *ntrace_l = nullptr, *ntrace_u = nullptr;

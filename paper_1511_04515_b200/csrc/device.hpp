@@ -99,7 +99,7 @@ struct DenseArgs {
     double* hinv;     // persistent H_m^-1 (m x m, row-major)
     double* coef;     // final coefficients
     double* scratch;  // global scratch (used when the block does not fit smem)
-    int use_smem;
+    int smem_cap;     // dynamic shared memory of the launch (bytes)
     int mode;
     double h_eval;
 };
@@ -147,7 +147,8 @@ void start(const Launch& L, const double* v, const double* xk, int n, double* pa
 int mgs_max_blocks(int K);
 void mgs(const Launch& L, const MgsArgs& a, int n_blocks, int K);
 void dense(const Launch& L, const DenseArgs& a, int m);
-void iter_end(const Launch& L, Ctrl* ctrl);
+void iter_end(const Launch& L, Ctrl* ctrl, unsigned long long cond = 0);
+void fill_ones(const Launch& L, void* p, size_t bytes);
 void combine(const Launch& L, const double* V, long long ldv, const double* coef, int n,
              double* out, const Ctrl* ctrl, int mode, const double* xk, const double* gb,
              const double* start, double h);

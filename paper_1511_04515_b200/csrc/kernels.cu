@@ -434,27 +434,39 @@ __global__ void __launch_bounds__(256)
     int t = gw;
     if (t >= a.n_tasks) return;
     // metadata of the current task (per lane: its row in a group task)
-    auto load_meta = [&](int tt, int2& task, int4& m, double& b) {
+    // (the diagonal, the output permutation and the add vector of the fused
+    // epilogue are prefetched with it: none of them may sit on the hand-off
+    // path as a dependent HBM load)
+    struct Pre {
+        double b, dg, ad;
+        int qq;
+    };
+    auto load_meta = [&](int tt, int2& task, int4& m, Pre& pr) {
         task = a.tasks[tt];
         const bool lng = task.y & kTaskLong;
         const int lg = lng ? 5 : ((task.y >> 8) & 0x7);
         const int seg = lng ? 0 : (lane >> lg);
         const int cnt = lng ? 1 : (task.y & 0xFF);
+        pr = Pre{0.0, 1.0, 0.0, 0};
         if (seg < cnt) {
             m = a.meta[task.x + seg];
-            b = a.in[m.y];
+            pr.b = a.in[m.y];
+            if (UPPER) pr.dg = a.diag[m.x];
+            if (a.final_out) {
+                pr.qq = a.out_perm[m.x];
+                if (a.add) pr.ad = a.add[pr.qq];
+            }
         } else {
             m = make_int4(0, 0, 0, 0);
-            b = 0.0;
         }
     };
     int2 task, ntask;
     int4 m, nm;
-    double b, nb;
-    load_meta(t, task, m, b);
+    Pre pr, npr;
+    load_meta(t, task, m, pr);
     while (true) {
         const int tn = t + W;
-        if (tn < a.n_tasks) load_meta(tn, ntask, nm, nb);  // prefetch
+        if (tn < a.n_tasks) load_meta(tn, ntask, nm, npr);  // prefetch
         const bool lng = task.y & kTaskLong;
         const int r = m.x, k0 = m.z, k1 = m.w;
         double acc = 0.0;
@@ -483,14 +495,13 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
             if (lane == 0) {
-                double s = b - acc;
-                if (UPPER) s = s / a.diag[r];
+                double s = pr.b - acc;
+                if (UPPER) s = s / pr.dg;
                 st_relaxed(a.out + r, s);
                 if (a.final_out) {
-                    const int qq = a.out_perm[r];
                     double yv = a.coef * s;
-                    if (a.add) yv = a.add[qq] + yv;
-                    a.final_out[qq] = yv;
+                    if (a.add) yv = pr.ad + yv;
+                    a.final_out[pr.qq] = yv;
                 }
             }
         } else {
@@ -523,14 +534,13 @@ __global__ void __launch_bounds__(256)
             }
             for (int o = lpr >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
             if (active && sl == 0) {
-                double s = b - acc;
-                if (UPPER) s = s / a.diag[r];
+                double s = pr.b - acc;
+                if (UPPER) s = s / pr.dg;
                 st_relaxed(a.out + r, s);
                 if (a.final_out) {
-                    const int qq = a.out_perm[r];
                     double yv = a.coef * s;
-                    if (a.add) yv = a.add[qq] + yv;
-                    a.final_out[qq] = yv;
+                    if (a.add) yv = pr.ad + yv;
+                    a.final_out[pr.qq] = yv;
                 }
             }
         }
@@ -538,7 +548,7 @@ __global__ void __launch_bounds__(256)
         t = tn;
         task = ntask;
         m = nm;
-        b = nb;
+        pr = npr;
     }
 }
 
@@ -1340,17 +1350,29 @@ __device__ void decide(Ctrl* c) {
 }
 
 // after every iteration: cap check and advance (krylov.cpp:118,165-168)
-__global__ void k_iter_end(Ctrl* c) {
+// cond != 0: the iteration runs as the body of the Arnoldi graph's WHILE
+// node; the loop continues while the MEVP is neither converged nor failed.
+__global__ void k_iter_end(Ctrl* c, unsigned long long cond) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     c->arnoldi_iters++;
-    if (c->status || c->converged) return;
-    if (c->need_weight) decide(c);  // weight computed by another path
-    if (c->converged) return;
-    if (c->m >= c->m_max) {
-        c->status = 5;  // EXG_E_NO_CONVERGENCE
-        return;
+    if (!(c->status || c->converged)) {
+        if (c->need_weight) decide(c);  // weight computed by another path
+        if (!c->converged) {
+            if (c->m >= c->m_max)
+                c->status = 5;  // EXG_E_NO_CONVERGENCE
+            else
+                c->j = c->m;
+        }
     }
-    c->j = c->m;
+    if (cond) cudaGraphSetConditional((cudaGraphConditionalHandle)cond, (c->status || c->converged) ? 0u : 1u);
+}
+
+// all-ones (NaN sentinel) fill of the solve scratch; a kernel rather than a
+// memset node so the solve can live inside the Arnoldi graph's loop body
+__global__ void __launch_bounds__(256) k_fill_ones(unsigned long long* __restrict__ p, long long n8) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += stride)
+        p[i] = ~0ull;
 }
 
 // ============================================================================
@@ -1892,7 +1914,7 @@ __global__ void __launch_bounds__(256)
     if (a.mode == 1 && (c->status || c->skip)) return;
     const int m = c->m;
     const int mm = m * m;
-    double* S = a.use_smem ? dyn_smem : a.scratch;
+    double* S = (size_t)20 * mm * sizeof(double) <= (size_t)a.smem_cap ? dyn_smem : a.scratch;
     double* hm = S;
     double* hinv_tmp = S + mm;
     double* e = S + 2 * mm;
@@ -2384,15 +2406,24 @@ void dense(const Launch& L, const DenseArgs& a0, int m) {
         cudaFuncSetAttribute(k_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr = true;
     }
+    // m: an upper bound of the dimension the kernel will find in the control
+    // block (exact in eager launches, m_max inside the Arnoldi graph)
     DenseArgs a = a0;
     const size_t need = (size_t)20 * m * m * sizeof(double);
-    a.use_smem = need <= 200 * 1024;
-    k_dense<<<1, 256, a.use_smem ? need : 0, L.stream>>>(a);
+    a.smem_cap = (int)std::min<size_t>(need, 200 * 1024);
+    k_dense<<<1, 256, a.smem_cap, L.stream>>>(a);
     count(L);
 }
 
-void iter_end(const Launch& L, Ctrl* ctrl) {
-    k_iter_end<<<1, 32, 0, L.stream>>>(ctrl);
+void iter_end(const Launch& L, Ctrl* ctrl, unsigned long long cond) {
+    k_iter_end<<<1, 32, 0, L.stream>>>(ctrl, cond);
+    count(L);
+}
+
+void fill_ones(const Launch& L, void* p, size_t bytes) {
+    const long long n8 = (long long)(bytes / 8);
+    const unsigned int grid = (unsigned int)std::min<long long>((long long)L.num_sms * 8, (n8 + 255) / 256);
+    if (grid) k_fill_ones<<<grid, 256, 0, L.stream>>>(reinterpret_cast<unsigned long long*>(p), n8);
     count(L);
 }
 

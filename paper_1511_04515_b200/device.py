@@ -54,14 +54,14 @@ class TransientResult:
 
 class Context:
     def __init__(self, device: int = 0, trsv_mode: int = F.EXG_TRSV_EXACT,
-                 weight_mode: int = F.EXG_WEIGHT_APPLY):
+                 weight_mode: int = F.EXG_WEIGHT_APPLY, loop_mode: int = F.EXG_LOOP_GRAPH):
         h = C.c_void_p()
         st = F.lib.exg_create(device, C.byref(h))
         if st != F.EXG_OK:
             raise_for(st, f"exg_create(device={device}) failed (is an sm_100 GPU visible?)")
         self._h = h
         self.n = 0
-        self.set_options(trsv_mode, weight_mode)
+        self.set_options(trsv_mode, weight_mode, loop_mode)
 
     def close(self):
         if getattr(self, "_h", None):
@@ -87,8 +87,9 @@ class Context:
             F.lib.exg_last_error(self._h, buf, 512)
             raise_for(st, buf.value.decode(), value)
 
-    def set_options(self, trsv_mode: int = F.EXG_TRSV_EXACT, weight_mode: int = F.EXG_WEIGHT_APPLY):
-        o = F.exg_options_dev(trsv_mode, weight_mode)
+    def set_options(self, trsv_mode: int = F.EXG_TRSV_EXACT, weight_mode: int = F.EXG_WEIGHT_APPLY,
+                    loop_mode: int = F.EXG_LOOP_GRAPH):
+        o = F.exg_options_dev(trsv_mode, weight_mode, loop_mode)
         self._check(F.lib.exg_set_options(self._h, C.byref(o)))
 
     # ---- device store

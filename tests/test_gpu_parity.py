@@ -237,3 +237,37 @@ def test_residual_F_bit_identical(ref, kw):
             got = c.residual_F(x)
             assert bit_equal(got, want)
             assert np.abs(want).max() > 0.0
+
+
+@pytest.mark.parametrize("trsv", [F.EXG_TRSV_EXACT, F.EXG_TRSV_FAST], ids=["exact", "fast"])
+@pytest.mark.parametrize("weight", [F.EXG_WEIGHT_APPLY, F.EXG_WEIGHT_GSPMV], ids=["apply", "gspmv"])
+def test_graph_loop_equals_eager(case, trsv, weight):
+    """The Arnoldi loop as one CUDA graph (WHILE node) runs the same kernels as
+    the eager loop: bit-identical values, identical m, one graph launch per
+    MEVP, and the graph is reused across MEVPs."""
+    _, s, f, _ = case
+    opts = s.options()
+    rng = np.random.default_rng(11)
+    vs = [rng.uniform(-1, 1, s.n) for _ in range(3)]
+    res = {}
+    for loop in (F.EXG_LOOP_EAGER, F.EXG_LOOP_GRAPH):
+        with Context(0, trsv_mode=trsv, weight_mode=weight, loop_mode=loop) as c:
+            c.set_system(s)
+            c.set_factors(f)
+            out = []
+            for v in vs:
+                try:
+                    out.append(c.mevp_iks(v, 1e-12, eps=1e-8, m_max=opts.m_max))
+                except ex.NoConvergenceError as e:  # the same failure in both modes
+                    out.append((None, ("no-convergence", e.last_residual)))
+            cn = c.counters()
+            res[loop] = (out, cn.graph_launches, cn.graph_builds, cn.arnoldi_iters)
+    (eo, eg, _, ei), (go, gg, gb, gi) = res[F.EXG_LOOP_EAGER], res[F.EXG_LOOP_GRAPH]
+    assert eg == 0 and gg == len(vs) and gb == 1
+    assert ei == gi
+    for (a, ia), (b, ib) in zip(eo, go):
+        if a is None or b is None:
+            assert ia == ib
+            continue
+        assert ia.m == ib.m and ia.happy == ib.happy
+        assert bit_equal(a, b)

@@ -157,13 +157,16 @@ const DCsr& mat(exg_ctx* c, int which) {
 void solve_dev(exg_ctx* c, const double* b, double* final_out, double coef, const double* add,
                const Ctrl* ctrl) {
     const int n = c->n;
-    exg::dev::fill_ones(c->L(), c->trsv_buf, kTrsvHdr + 6 * sizeof(double) * (size_t)n);
+    // scratch: [tickets][y n][x n][chain s: L rows, U rows][chain partial slots: L, U]
+    const bool fast = c->opt.trsv_mode == EXG_TRSV_FAST;
+    const size_t chain_doubles = fast ? (size_t)(c->plan[0].chain_rows + c->plan[1].chain_rows +
+                                                 c->plan[0].chain_slots + c->plan[1].chain_slots) : 0;
+    exg::dev::fill_ones(c->L(), c->trsv_buf, kTrsvHdr + sizeof(double) * (2 * (size_t)n + chain_doubles));
     unsigned int* tickets = reinterpret_cast<unsigned int*>(c->trsv_buf);
     double* y = reinterpret_cast<double*>(c->trsv_buf + kTrsvHdr);
     double* x = y + n;
-    double* sbuf_dev = x + n;     // chain runs' s vectors (L and U: <= n each... shared)
-    double* pbuf_dev = x + 3 * n;  // chain runs' old partial sums
-    const bool fast = c->opt.trsv_mode == EXG_TRSV_FAST;
+    double* sbuf_dev = x + n;  // chain runs' s vectors, run after run
+    double* pbuf_dev = sbuf_dev + c->plan[0].chain_rows + c->plan[1].chain_rows;  // partial slots
     const int fq = fast ? 2 : 0;
     int next_ticket = 0;
     for (int tri = 0; tri < 2; ++tri) {
@@ -210,13 +213,15 @@ void solve_dev(exg_ctx* c, const double* b, double* final_out, double coef, cons
                     ca.n_rows = ch.n_rows;
                     ca.n_blocks = ch.n_blocks;
                     ca.rows = P.crows + ch.rows_off;
+                    ca.rq = P.crq + ch.rows_off;
                     ca.nptr = P.cnptr + ch.nptr_off;
                     ca.ncol = P.cncol + ch.ent0;
                     ca.nval = P.cnval + ch.ent0;
                     ca.blocks = P.cblocks + 3 * (long long)ch.blk0;
                     ca.pool = P.pool;
                     ca.s = sbuf_dev;
-                    ca.part = pbuf_dev;
+                    ca.part = pbuf_dev + ch.slot0;
+                    ca.pslot = P.cpslot + ch.rows_off;
                     ca.wtasks = P.ctasks + ch.task0;
                     ca.n_tasks = ch.ntasks;
                     ca.in = a.in;
@@ -228,9 +233,10 @@ void solve_dev(exg_ctx* c, const double* b, double* final_out, double coef, cons
                     ca.coef = a.coef;
                     ca.ctrl = ctrl;
                     ca.trace = upper ? c->ntrace_u : c->ntrace_l;
+                    static const unsigned spin = getenv("EXG_CHAIN_SPIN") ? (unsigned)atoi(getenv("EXG_CHAIN_SPIN")) : 0u;
+                    ca.spin_ns = spin;
                     exg::dev::trsv_chain(c->L(), upper, ca);
                     sbuf_dev += ch.n_rows;
-                    pbuf_dev += ch.n_rows;
                     continue;
                 }
                 if (!run.narrow) {
@@ -288,6 +294,7 @@ void solve_dev(exg_ctx* c, const double* b, double* final_out, double coef, cons
                 for (auto e : rev) cudaEventDestroy(e);
             }
         }
+        if (fast) pbuf_dev += c->plan[tri].chain_slots;
         c->prof_end(upper ? EXG_K_TRSV_U : EXG_K_TRSV_L, e0);
     }
     c->cnt.trsv_calls++;
@@ -496,7 +503,8 @@ void deliver(exg_ctx* c, double* user, const double* dev, size_t count, int ptr_
 void plan_triangle(exg_ctx* c, TriPlan& P, bool upper_tri, const std::vector<int>& ord,
                    const std::vector<int>& level, int nl, const std::vector<int>& ptr,
                    const std::vector<int>& col, const std::vector<double>& val,
-                   const std::vector<int2>& tasks, const std::vector<double>* udiag) {
+                   const std::vector<int2>& tasks, const std::vector<double>* udiag,
+                   const int* out_perm) {
     const int n = (int)ord.size();
     P.free_dev();
     P.runs.clear();
@@ -517,8 +525,12 @@ void plan_triangle(exg_ctx* c, TriPlan& P, bool upper_tri, const std::vector<int
     std::vector<int2> regions;
     std::vector<int4> regions4, blocks;
     struct ChainRun {
-        int pos0, rows, blk0, nblocks, ent0, task0 = 0, ntasks = 0;
+        int pos0, rows, blk0, nblocks, ent0, task0 = 0, ntasks = 0, slot0 = 0, slots = 0;
     };
+    constexpr int kChunk = 256;  // entries per worker task (8 per lane)
+    std::vector<int> cpslot;     // per chain position: first partial-sum slot (run-local)
+    std::vector<int2> crq;       // per chain position: (row, output position of the fused epilogue)
+    int slot_total = 0;
     std::vector<int4> ctasks;
     const char* ko = getenv("EXG_CHAIN_OLD");
     const int kOld = ko ? atoi(ko) : 8;
@@ -586,13 +598,15 @@ void plan_triangle(exg_ctx* c, TriPlan& P, bool upper_tri, const std::vector<int
                     const int p = bs + i;
                     const int r = ord[p];
                     crows.push_back(r);
+                    crq.push_back(make_int2(r, out_perm ? out_perm[r] : 0));
                     Dm[i * kB + i] = diag_of(r);
                     if (Dm[i * kB + i] != 1.0) d_ident = false;
-                    std::vector<std::pair<int, double>> oldv, recv;
+                    std::vector<std::pair<int, double>> recv;
+                    std::vector<std::pair<int, int>> oldk;  // (position, k)
                     for (int k = ptr[r]; k < ptr[r + 1]; ++k) {
                         const int pq = pos_of[col[k]];
                         if (pq < pso) {
-                            oldv.push_back({col[k], val[k]});
+                            oldk.push_back({pq, k});
                         } else if (pq < ps2) {
                             recv.push_back({col[k], val[k]});
                         } else if (pq < ps1) {
@@ -607,20 +621,33 @@ void plan_triangle(exg_ctx* c, TriPlan& P, bool upper_tri, const std::vector<int
                         }
                     }
                     const int pl = (int)crows.size() - 1 - cr.pos0;  // run-local position
-                    const int e0 = (int)cncol.size() - cr.ent0;
-                    for (auto& e : oldv) {
-                        cncol.push_back(e.first);
-                        cnval.push_back(e.second);
+                    // old entries by age, cut into chunks of <= kChunk: one
+                    // worker task per chunk, scheduled by its newest entry
+                    // (entries of earlier launches are final at kernel start),
+                    // each writing its own partial-sum slot
+                    std::sort(oldk.begin(), oldk.end());
+                    const int nch = (int)((oldk.size() + kChunk - 1) / kChunk);
+                    cpslot.push_back(cr.slots);
+                    for (int q = 0; q < nch; ++q) {
+                        const int a0 = q * kChunk, a1 = std::min((int)oldk.size(), a0 + kChunk);
+                        const int e0 = (int)cncol.size() - cr.ent0;
+                        for (int z = a0; z < a1; ++z) {
+                            cncol.push_back(col[oldk[z].second]);
+                            cnval.push_back(val[oldk[z].second]);
+                        }
+                        const int e1 = (int)cncol.size() - cr.ent0;
+                        const int newest = oldk[a1 - 1].first;
+                        const int key = newest < p0 ? 0 : (newest - p0) / kB;
+                        wt.push_back({key, make_int4(cr.slots + q, e0, e1, 0)});
                     }
+                    cr.slots += nch;
                     const int e1 = (int)cncol.size() - cr.ent0;
                     for (auto& e : recv) {
                         cncol.push_back(e.first);
                         cnval.push_back(e.second);
                     }
                     const int e2 = (int)cncol.size() - cr.ent0;
-                    const bool has_old = e1 > e0;
-                    if (has_old) wt.push_back({std::max(0, kb - kOld - 1), make_int4(pl, e0, e1, 0)});
-                    wt.push_back({std::max(0, kb - 3), make_int4(pl, e1, e2, 1 | (has_old ? 2 : 0))});
+                    wt.push_back({std::max(0, kb - 3), make_int4(pl, e1, e2, 1 | (nch << 8))});
                     cnptr.push_back(e2);
                 }
                 std::fill(Di.begin(), Di.end(), 0.0);
@@ -630,9 +657,15 @@ void plan_triangle(exg_ctx* c, TriPlan& P, bool upper_tri, const std::vector<int
                         for (int m2 = jc; m2 < i; ++m2) sacc -= Dm[i * kB + m2] * Di[m2 * kB + jc];
                         Di[i * kB + jc] = sacc / Dm[i * kB + i];
                     }
+                // chain layout (k_trsv_chain): thread t of the chain CTA owns
+                // row t/4, columns (t%4)*16 .. +15; element j of thread t is at
+                // j*256 + t, so every shared-memory read is conflict-free
                 auto push_mat = [&](const std::vector<double>& M) {
                     const int o = (int)pool.size();
-                    pool.insert(pool.end(), M.begin(), M.end());
+                    pool.resize(pool.size() + kB * kB);
+                    for (int j = 0; j < 16; ++j)
+                        for (int t = 0; t < 256; ++t)
+                            pool[o + j * 256 + t] = M[(t >> 2) * kB + (t & 3) * 16 + j];
                     return o;
                 };
                 auto times_dinv = [&](const std::vector<double>& E) {
@@ -657,6 +690,8 @@ void plan_triangle(exg_ctx* c, TriPlan& P, bool upper_tri, const std::vector<int
             cr.task0 = (int)ctasks.size();
             for (auto& w : wt) ctasks.push_back(w.second);
             cr.ntasks = (int)wt.size();
+            cr.slot0 = slot_total;
+            slot_total += cr.slots;
             cruns.push_back(cr);
             run.b = run.a + 1;
         } else {
@@ -786,6 +821,10 @@ void plan_triangle(exg_ctx* c, TriPlan& P, bool upper_tri, const std::vector<int
         ck(cudaMemcpy(P.cblocks, cblocks.data(), cblocks.size() * sizeof(int4), cudaMemcpyHostToDevice), "chain");
         P.ctasks = dalloc<int4>(std::max<size_t>(ctasks.size(), 1));
         ck(cudaMemcpy(P.ctasks, ctasks.data(), ctasks.size() * sizeof(int4), cudaMemcpyHostToDevice), "chain");
+        P.crq = dalloc<int2>(std::max<size_t>(crq.size(), 1));
+        ck(cudaMemcpy(P.crq, crq.data(), crq.size() * sizeof(int2), cudaMemcpyHostToDevice), "chain");
+        P.cpslot = dalloc<int>(std::max<size_t>(cpslot.size(), 1));
+        ck(cudaMemcpy(P.cpslot, cpslot.data(), cpslot.size() * sizeof(int), cudaMemcpyHostToDevice), "chain");
         if (!P.pool) {
             P.pool = dalloc<double>(std::max<size_t>(pool.size(), 1));
             if (!pool.empty())
@@ -802,11 +841,15 @@ void plan_triangle(exg_ctx* c, TriPlan& P, bool upper_tri, const std::vector<int
             ch.n_blocks = cruns[q].nblocks;
             ch.task0 = cruns[q].task0;
             ch.ntasks = cruns[q].ntasks;
+            ch.slot0 = cruns[q].slot0;
+            ch.n_slots = cruns[q].slots;
             P.chains.push_back(ch);
+            P.chain_rows += cruns[q].rows;
         }
     }
     P.narrow_rows = (long long)rows.size();
     P.narrow_nnz = (long long)ncol.size();
+    P.chain_slots = slot_total;
     (void)c;
 }
 
@@ -1122,8 +1165,8 @@ exg_status exg_set_factors(exg_ctx* c, int n, const int* Lp, const int* Li, cons
     // FAST-mode plan: runs of wide levels (warp tasks, all SMs) and of narrow
     // levels (one thread-block cluster, DSMEM hand-offs)
     const int lnl = l_levels, unl = u_levels;
-    plan_triangle(c, c->plan[0], false, lord, llev, lnl, lp, lc, lv, ltasks_f, nullptr);
-    plan_triangle(c, c->plan[1], true, uord, lev, unl, up, uc, uv, utasks_f, &ud);
+    plan_triangle(c, c->plan[0], false, lord, llev, lnl, lp, lc, lv, ltasks_f, nullptr, nullptr);
+    plan_triangle(c, c->plan[1], true, uord, lev, unl, up, uc, uv, utasks_f, &ud, col_perm);
     {
         std::vector<int4> lm(n), um(n);
         for (int p = 0; p < n; ++p) {
@@ -1146,7 +1189,9 @@ exg_status exg_set_factors(exg_ctx* c, int n, const int* Lp, const int* Li, cons
         ck(cudaMemcpy(c->tasks[q], tl[q]->data(), tl[q]->size() * sizeof(int2), cudaMemcpyHostToDevice), "tasks");
         c->n_tasks[q] = (int)tl[q]->size();
     }
-    c->trsv_buf = dalloc<char>(kTrsvHdr + 6 * sizeof(double) * (size_t)n);
+    c->trsv_buf = dalloc<char>(kTrsvHdr + sizeof(double) * (2 * (size_t)n + c->plan[0].chain_rows +
+                                                       c->plan[1].chain_rows + c->plan[0].chain_slots +
+                                                       c->plan[1].chain_slots));
     ensure_vectors(c, n);
     c->cnt.l_levels = l_levels;
     c->cnt.u_levels = u_levels;

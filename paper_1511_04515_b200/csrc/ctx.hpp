@@ -38,7 +38,7 @@ struct TriPlan {
     double* pool = nullptr;
     // chain + workers runs
     struct Chain {
-        int rows_off, nptr_off, ent0, n_rows, blk0, n_blocks, task0, ntasks;
+        int rows_off, nptr_off, ent0, n_rows, blk0, n_blocks, task0, ntasks, slot0, n_slots;
     };
     std::vector<Chain> chains;
     int* crows = nullptr;
@@ -47,6 +47,9 @@ struct TriPlan {
     double* cnval = nullptr;
     int4* cblocks = nullptr;
     int4* ctasks = nullptr;
+    int* cpslot = nullptr;
+    int2* crq = nullptr;
+    long long chain_rows = 0, chain_slots = 0;  // scratch of the chain runs (s values, partial slots)
     size_t smem = 0;
     long long narrow_rows = 0, narrow_nnz = 0;
     void free_dev() {
@@ -65,6 +68,11 @@ struct TriPlan {
         if (cnval) cudaFree(cnval);
         if (cblocks) cudaFree(cblocks);
         if (ctasks) cudaFree(ctasks);
+        if (cpslot) cudaFree(cpslot);
+        if (crq) cudaFree(crq);
+        crq = nullptr;
+        cpslot = nullptr;
+        chain_rows = chain_slots = 0;
         ctasks = nullptr;
         crows = cnptr = cncol = nullptr;
         cnval = nullptr;

@@ -60,14 +60,16 @@ struct ChainArgs {
     int n_rows;            // positions of this run
     int n_blocks;
     const int* rows;       // row id per position (run-local)
+    const int2* rq;        // per position: (row id, output position of the fused epilogue)
     const int* nptr;       // per position: entries older than block k-2
     const int* ncol;       // global row ids
     const double* nval;
     const int4* blocks;    // 3 per block: (first pos, rows,-,-), (Dinv, F1, F2 offsets,-), -
     const double* pool;
     double* s;             // per position, sentinel-initialised
-    double* part;          // per position: partial sum of the old entries (sentinel-initialised)
-    const int4* wtasks;    // worker tasks (position, k0, k1, type | has_old << 1)
+    double* part;          // partial sums of the old-entry chunks, one slot each (sentinel-initialised)
+    const int* pslot;      // per position: first partial slot of its row
+    const int4* wtasks;    // worker tasks: chunk (slot, k0, k1, 0) | recent (position, k0, k1, 1 | chunks << 8)
     int n_tasks;
     const double* in;
     const int* in_perm;
@@ -77,7 +79,8 @@ struct ChainArgs {
     const double* add;
     double coef;
     const Ctrl* ctrl;
-    unsigned long long* trace;  // debug: per block (s ready, x published)
+    unsigned long long* trace;  // debug: per block timestamps, then per-position worker timestamps
+    unsigned spin_ns;      // worker back-off between unsuccessful polls (0 = spin)
 };
 
 struct MgsArgs {

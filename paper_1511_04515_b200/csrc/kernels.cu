@@ -240,12 +240,13 @@ __device__ __forceinline__ RowOps row_ops(const TrsvArgs& a, int r) {
 // ready; no lane ever spins alone inside a divergent branch.
 template <int N>
 __device__ __forceinline__ void warp_wait_ready(const double* out, const int* cc, const int* kk,
-                                                int k1, double* y) {
+                                                int k1, double* y, unsigned sleep_ns = 0) {
     bool rd = true;
 #pragma unroll
     for (int q = 0; q < N; ++q)
         rd = rd && !(kk[q] < k1 && __double_as_longlong(y[q]) == (long long)kSentinel);
     while (!__all_sync(0xffffffffu, rd)) {
+        if (sleep_ns) __nanosleep(sleep_ns);
         rd = true;
 #pragma unroll
         for (int q = 0; q < N; ++q) {
@@ -460,20 +461,71 @@ __global__ void __launch_bounds__(256)
             m = make_int4(0, 0, 0, 0);
         }
     };
-    int2 task, ntask;
-    int4 m, nm;
-    Pre pr, npr;
+    // first batch (4 entries per lane) of a task: the same index pattern as
+    // the processing loops below (U: newest dependencies last)
+    auto batch0 = [&](const int2& task, const int4& mm, int* cc, double* v) {
+        const bool lng = task.y & kTaskLong;
+        const int k0 = mm.z, k1 = mm.w;
+        int kk[4];
+        if (lng) {
+            const int nch = (k1 - k0 + 31) >> 5;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int ch = UPPER ? nch - 1 - q : q;
+                kk[q] = q < nch ? k0 + ch * 32 + lane : k1;
+            }
+        } else {
+            const int cnt = task.y & 0xFF;
+            const int lg = (task.y >> 8) & 0x7;
+            const int lpr = 1 << lg;
+            const int seg = lane >> lg, sl = lane & (lpr - 1);
+            const int nj = seg < cnt ? (k1 - k0 - sl + lpr - 1) >> lg : 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int j = UPPER ? nj - 1 - q : q;
+                kk[q] = q < nj ? k0 + sl + (j << lg) : k1;
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            cc[q] = kk[q] < k1 ? a.col[kk[q]] : -1;
+            v[q] = kk[q] < k1 ? a.val[kk[q]] : 0.0;
+        }
+    };
+    // Two-deep software pipeline: while task i runs, the entries of task
+    // i+1 (whose metadata arrived during task i-1) and the metadata of task
+    // i+2 are in flight, so a task's own loads are never on the hand-off path.
+    int2 task, task1, task2;
+    int4 m, m1, m2;
+    Pre pr, pr1, pr2;
+    int cc0[4], cc1[4];
+    double v0[4], v1[4];
     load_meta(t, task, m, pr);
+    const bool has1 = t + W < a.n_tasks;
+    if (has1) load_meta(t + W, task1, m1, pr1);
+    batch0(task, m, cc0, v0);
     while (true) {
-        const int tn = t + W;
-        if (tn < a.n_tasks) load_meta(tn, ntask, nm, npr);  // prefetch
+        const int tn = t + W, tnn = t + 2 * W;
+        if (tnn < a.n_tasks) load_meta(tnn, task2, m2, pr2);
+        if (tn < a.n_tasks) batch0(task1, m1, cc1, v1);
         const bool lng = task.y & kTaskLong;
         const int r = m.x, k0 = m.z, k1 = m.w;
         double acc = 0.0;
+        {  // batch 0 from the prefetched entries
+            int kk[4];
+            double y[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                kk[q] = cc0[q] >= 0 ? k0 : k1;  // validity marker for warp_wait_ready
+                y[q] = cc0[q] >= 0 ? __ldca(a.out + cc0[q]) : 0.0;
+            }
+            warp_wait_ready<4>(a.out, cc0, kk, k1, y);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc += v0[q] * y[q];
+        }
         if (lng) {
             const int nch = (k1 - k0 + 31) >> 5;
-            int ci = 0;
-            for (; ci < nch; ci += 4) {
+            for (int ci = 4; ci < nch; ci += 4) {
                 int kk[4], cc[4];
                 double v[4], y[4];
 #pragma unroll
@@ -512,7 +564,7 @@ __global__ void __launch_bounds__(256)
             const bool active = seg < cnt;
             const int nj = active ? (k1 - k0 - sl + lpr - 1) >> lg : 0;
             const int njmax = __reduce_max_sync(FULL, nj);
-            for (int j0 = 0; j0 < njmax; j0 += 4) {
+            for (int j0 = 4; j0 < njmax; j0 += 4) {
                 int kk[4], cc[4];
                 double v[4], y[4];
 #pragma unroll
@@ -546,9 +598,17 @@ __global__ void __launch_bounds__(256)
         }
         if (tn >= a.n_tasks) return;
         t = tn;
-        task = ntask;
-        m = nm;
-        pr = npr;
+        task = task1;
+        m = m1;
+        pr = pr1;
+        task1 = task2;
+        m1 = m2;
+        pr1 = pr2;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            cc0[q] = cc1[q];
+            v0[q] = v1[q];
+        }
     }
 }
 
@@ -726,6 +786,7 @@ __global__ void __launch_bounds__(EXG_NARROW_THREADS, 1)
 // (DSMEM) and to global memory.
 // ---------------------------------------------------------------------------
 constexpr int kBlk = 64;
+constexpr size_t kChainSmem = 2 * 3 * kBlk * kBlk * sizeof(double);  // chain CTA: 2 stages x (Dinv, F1, F2)
 
 // GEMV of one warp's 8 outputs against a 64-vector held as (x0, x1) =
 // (v[lane], v[lane+32]); f0/f1 hold the warp's 8 matrix rows the same way.
@@ -927,98 +988,232 @@ __global__ void __launch_bounds__(256, EXG_CHAIN_MINB)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (blockIdx.x == 0) {
         // ===================== chain CTA =====================
-        __shared__ double xr[3 * kBlk];  // ring of the last 3 blocks' x
-        const int i0 = warp * 8;
-        for (int kb = 0; kb < a.n_blocks; ++kb) {
-            const int4 B = a.blocks[3 * kb];
-            const int4 O = a.blocks[3 * kb + 1];
-            const int nb = B.y;
-            // matrices of this block: straight from L2/HBM into registers,
-            // issued before the wait on s so the latencies overlap
-            double d0[8], d1[8], g0[8], g1[8], h0[8], h1[8];
-            const int4 B1 = kb >= 1 ? a.blocks[3 * (kb - 1)] : make_int4(0, 0, 0, 0);
-            const int4 B2 = kb >= 2 ? a.blocks[3 * (kb - 2)] : make_int4(0, 0, 0, 0);
-            if (O.x >= 0) load_rows8(a.pool + (long long)O.x, i0, nb, nb, d0, d1);
-            if (O.y >= 0) load_rows8(a.pool + (long long)O.y, i0, nb, B1.y, g0, g1);
-            if (O.z >= 0) load_rows8(a.pool + (long long)O.z, i0, nb, B2.y, h0, h1);
-            // s of this block (published by the workers)
-            double s0 = 0.0, s1 = 0.0;
+        // Block k's Dinv/F1/F2 (3 x 32 KB) arrive in shared memory by TMA
+        // bulk copies issued one block ahead (two stages, one mbarrier each),
+        // in the thread-major layout written by the planner: thread t owns
+        // row t/4 and columns (t%4)*16..+15 of every matrix (conflict-free
+        // reads, a 2-step shuffle reduction).  Block metadata, row ids and
+        // epilogue operands are loaded one or two blocks ahead, and F2 x_{k-2},
+        // F1 x_{k-1} are formed before the wait for s, so after s arrives only
+        // Dinv s, the publication and one barrier remain.
+        constexpr int kXs = 68;  // padded x slot: column c at c + c/16
+        extern __shared__ __align__(128) double smat[];  // [2 stages][3][kBlk*kBlk]
+        __shared__ double xr[3 * kXs];                   // x of the last 3 blocks
+        __shared__ double sw[8 * kXs];                   // each warp's copy of the block's s
+        __shared__ __align__(8) unsigned long long mbar[2];
+        const int tid = threadIdx.x, row = tid >> 2, qd = tid & 3;
+        const unsigned mb0 = (unsigned)__cvta_generic_to_shared(&mbar[0]);
+        if (tid == 0) {
+            asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(mb0));
+            asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(mb0 + 8));
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        for (int i = tid; i < 3 * kXs; i += blockDim.x) xr[i] = 0.0;
+        __syncthreads();
+        auto issue = [&](int kb, int4 O) {  // thread 0
+            const int st = kb & 1;
+            const unsigned mb = mb0 + 8 * st;
+            const unsigned cnt = (O.x >= 0 ? 1u : 0u) + (O.y >= 0 ? 1u : 0u) + (O.z >= 0 ? 1u : 0u);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(mb),
+                         "r"(cnt * (unsigned)(kBlk * kBlk * sizeof(double))) : "memory");
+            const int offs[3] = {O.x, O.y, O.z};
+            // re-read by every solve: keep in L2 while the factors stream past
+            unsigned long long pol;
+            asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                if (offs[q] < 0) continue;
+                const unsigned dst = (unsigned)__cvta_generic_to_shared(smat + (st * 3 + q) * kBlk * kBlk);
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(dst),
+                    "l"(a.pool + offs[q]), "r"((unsigned)(kBlk * kBlk * sizeof(double))), "r"(mb), "l"(pol)
+                    : "memory");
+            }
+        };
+        auto wait_stage = [&](int kb) {
+            const unsigned mb = mb0 + 8 * (kb & 1);
+            const unsigned par = (unsigned)((kb >> 1) & 1);
+            unsigned done = 0;
+            while (!done) {
+                asm volatile(
+                    "{ .reg .pred p; mbarrier.try_wait.parity.shared.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                    : "=r"(done) : "r"(mb), "r"(par) : "memory");
+            }
+        };
+        const int nbk = a.n_blocks;
+        if (nbk == 0) return;
+        int4 Bc = a.blocks[0], Oc = a.blocks[1];
+        int4 B1 = nbk > 1 ? a.blocks[3] : make_int4(0, 0, 0, 0);
+        int4 O1 = nbk > 1 ? a.blocks[4] : make_int4(-1, -1, -1, 0);
+        if (tid == 0) issue(0, Oc);
+        int2 rq = (qd == 0 && row < Bc.y) ? a.rq[Bc.x + row] : make_int2(0, 0);
+        double s0 = lane < Bc.y ? __longlong_as_double(ld_relaxed(a.s + Bc.x + lane)) : 0.0;
+        double s1 = lane + 32 < Bc.y ? __longlong_as_double(ld_relaxed(a.s + Bc.x + lane + 32)) : 0.0;
+        double* swp = sw + warp * kXs;
+        for (int kb = 0; kb < nbk; ++kb) {
+            const int nb = Bc.y;
+            // ---- one and two blocks ahead (nothing below consumes these
+            // before the next iteration, so none of the loads stalls)
+            if (tid == 0 && kb + 1 < nbk) issue(kb + 1, O1);
+            const int4 B2 = kb + 2 < nbk ? a.blocks[3 * (kb + 2)] : make_int4(0, 0, 0, 0);
+            const int4 O2 = kb + 2 < nbk ? a.blocks[3 * (kb + 2) + 1] : make_int4(-1, -1, -1, 0);
+            const int2 rqn = (qd == 0 && kb + 1 < nbk && row < B1.y) ? a.rq[B1.x + row] : make_int2(0, 0);
+            const double sn0 = (kb + 1 < nbk && lane < B1.y) ? __longlong_as_double(ld_relaxed(a.s + B1.x + lane)) : 0.0;
+            const double sn1 = (kb + 1 < nbk && lane + 32 < B1.y) ? __longlong_as_double(ld_relaxed(a.s + B1.x + lane + 32)) : 0.0;
+            const double ad = (a.final_out && a.add && qd == 0 && row < nb) ? a.add[rq.y] : 0.0;
+            // ---- F2 x_{k-2} and F1 x_{k-1}
+            wait_stage(kb);
+            unsigned long long t_w = 0;
+            if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_w));
+            const double* Ms = smat + (kb & 1) * 3 * kBlk * kBlk;
+            double p2 = 0.0, p1 = 0.0;
+            if (Oc.z >= 0) {
+                const double* xg = xr + ((kb - 2) % 3) * kXs + qd * 17;
+                const double* M = Ms + 2 * kBlk * kBlk + tid;
+#pragma unroll
+                for (int j = 0; j < 16; ++j) p2 += M[j * 256] * xg[j];
+                p2 += __shfl_xor_sync(FULL, p2, 1);
+                p2 += __shfl_xor_sync(FULL, p2, 2);
+            }
+            if (Oc.y >= 0) {
+                const double* xg = xr + ((kb - 1) % 3) * kXs + qd * 17;
+                const double* M = Ms + kBlk * kBlk + tid;
+#pragma unroll
+                for (int j = 0; j < 16; ++j) p1 += M[j * 256] * xg[j];
+                p1 += __shfl_xor_sync(FULL, p1, 1);
+                p1 += __shfl_xor_sync(FULL, p1, 2);
+            }
+            unsigned long long t_m = 0;
+            if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_m));
+            // ---- s of this block (published by the workers; each warp polls)
             {
-                const double* sp = a.s + B.x;
-                s0 = lane < nb ? __longlong_as_double(ld_relaxed(sp + lane)) : 0.0;
-                s1 = lane + 32 < nb ? __longlong_as_double(ld_relaxed(sp + lane + 32)) : 0.0;
+                const double* sp = a.s + Bc.x;
                 bool rd = __double_as_longlong(s0) != (long long)kSentinel &&
                           __double_as_longlong(s1) != (long long)kSentinel;
                 while (!__all_sync(FULL, rd)) {
-                    if (lane < nb) s0 = __longlong_as_double(ld_relaxed(sp + lane));
-                    if (lane + 32 < nb) s1 = __longlong_as_double(ld_relaxed(sp + lane + 32));
+                    if (lane < nb && __double_as_longlong(s0) == (long long)kSentinel)
+                        s0 = __longlong_as_double(ld_relaxed(sp + lane));
+                    if (lane + 32 < nb && __double_as_longlong(s1) == (long long)kSentinel)
+                        s1 = __longlong_as_double(ld_relaxed(sp + lane + 32));
                     rd = __double_as_longlong(s0) != (long long)kSentinel &&
                          __double_as_longlong(s1) != (long long)kSentinel;
                 }
             }
             unsigned long long t_s = 0;
             if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_s));
-            double c[8], part[8];
-            if (O.x >= 0) {
-                warp_gemv8(d0, d1, s0, s1, c);
+            swp[lane + (lane >> 4)] = s0;
+            swp[lane + 32 + ((lane + 32) >> 4)] = s1;
+            __syncwarp();
+            double cx;
+            if (Oc.x >= 0) {
+                const double* M = Ms + tid;
+                const double* sg = swp + qd * 17;
+                cx = 0.0;
+#pragma unroll
+                for (int j = 0; j < 16; ++j) cx += M[j * 256] * sg[j];
+                cx += __shfl_xor_sync(FULL, cx, 1);
+                cx += __shfl_xor_sync(FULL, cx, 2);
             } else {
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const int i = i0 + q;
-                    const double v = __shfl_sync(FULL, (i & 32) ? s1 : s0, i & 31);
-                    c[q] = i < nb ? v : 0.0;
-                }
+                cx = row < nb ? swp[row + (row >> 4)] : 0.0;
             }
-            if (O.z >= 0) {
-                const double* xg = xr + ((kb - 2) % 3) * kBlk;
-                warp_gemv8(h0, h1, lane < B2.y ? xg[lane] : 0.0, lane + 32 < B2.y ? xg[lane + 32] : 0.0, part);
-#pragma unroll
-                for (int q = 0; q < 8; ++q) c[q] = c[q] - part[q];
-            }
-            if (O.y >= 0) {
-                const double* xg = xr + ((kb - 1) % 3) * kBlk;
-                warp_gemv8(g0, g1, lane < B1.y ? xg[lane] : 0.0, lane + 32 < B1.y ? xg[lane + 32] : 0.0, part);
-#pragma unroll
-                for (int q = 0; q < 8; ++q) c[q] = c[q] - part[q];
-            }
-            // publish x_k: chain ring (smem) + global solution + fused epilogue
-            double* xk = xr + (kb % 3) * kBlk;
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const int i = i0 + q;
-                if (i < nb && lane == q) {
-                    xk[i] = c[q];
-                    const int r = a.rows[B.x + i];
-                    st_relaxed(a.out + r, c[q]);
-                    if (a.final_out) {
-                        const int qq = a.out_perm[r];
-                        double yo = a.coef * c[q];
-                        if (a.add) yo = a.add[qq] + yo;
-                        a.final_out[qq] = yo;
-                    }
-                }
+            if (Oc.z >= 0) cx = cx - p2;
+            if (Oc.y >= 0) cx = cx - p1;
+            // ---- publish x_k: chain ring + global solution; epilogue after
+            if (qd == 0) {
+                xr[(kb % 3) * kXs + row + (row >> 4)] = row < nb ? cx : 0.0;
+                if (row < nb) st_relaxed(a.out + rq.x, cx);
             }
             __syncthreads();
-            if (a.trace && threadIdx.x == 0) {
+            if (qd == 0 && row < nb && a.final_out) {
+                double yo = a.coef * cx;
+                if (a.add) yo = ad + yo;
+                a.final_out[rq.y] = yo;
+            }
+            if (a.trace && tid == 0) {
                 unsigned long long t_e;
                 asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_e));
-                a.trace[2 * kb] = t_s;
-                a.trace[2 * kb + 1] = t_e;
+                a.trace[4 * kb] = t_w;
+                a.trace[4 * kb + 1] = t_m;
+                a.trace[4 * kb + 2] = t_s;
+                a.trace[4 * kb + 3] = t_e;
             }
+            Bc = B1;
+            Oc = O1;
+            B1 = B2;
+            O1 = O2;
+            rq = rqn;
+            s0 = sn0;
+            s1 = sn1;
         }
         return;
     }
     // ===================== workers =====================
     // tasks in order of the block their newest dependency belongs to:
-    //   type 0 ("old"): part[p] = sum of the row's entries older than block k-8
-    //   type 1 ("recent"): s[p] = b - (part[p] + entries of blocks k-8..k-3)
+    //   chunk: part[slot] = sum of <= 256 entries older than block k-8
+    //   recent: s[p] = b - (sum of the row's chunk partials, in order,
+    //           + entries of blocks k-8..k-3)
+    // Software-pipelined: the next task's descriptor, its first 256 entries
+    // and (recent tasks) right-hand side and chunk partials are loaded while
+    // the current task waits, so a task costs one L2 round trip, not three
+    // dependent HBM loads.
     const int gw = (blockIdx.x - 1) * (blockDim.x >> 5) + warp;
     const int W = (gridDim.x - 1) * (blockDim.x >> 5);
-    for (int t = gw; t < a.n_tasks; t += W) {
-        const int4 T = a.wtasks[t];  // p, k0, k1, type | has_old << 1
-        const int p = T.x, k0 = T.y, k1 = T.z;
+    struct Stage {
+        int4 T;
+        int cc[8];
+        double v[8];
+        double b;
+        int slot0;
+        unsigned long long pv;
+    };
+    auto load_stage = [&](int t, Stage& S) {
+        S.T = a.wtasks[t];
+        const int k0 = S.T.y, k1 = S.T.z;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int k = k0 + lane + 32 * q;
+            S.cc[q] = k < k1 ? a.ncol[k] : -1;
+            S.v[q] = k < k1 ? a.nval[k] : 0.0;
+        }
+        S.b = 0.0;
+        S.slot0 = 0;
+        S.pv = 0ull;
+        if (S.T.w & 1) {
+            if (lane == 0) {
+                const int r = a.rows[S.T.x];
+                S.b = UPPER ? a.in[r] : a.in[a.in_perm[r]];
+            }
+            S.slot0 = a.pslot[S.T.x];
+            if (lane < (S.T.w >> 8)) S.pv = ld_relaxed(a.part + S.slot0 + lane);
+        }
+    };
+    int t = gw;
+    if (t >= a.n_tasks) return;
+    Stage cur, nxt;
+    load_stage(t, cur);
+    while (true) {
+        const int tn = t + W;
+        if (tn < a.n_tasks) load_stage(tn, nxt);
+        const int p = cur.T.x, k0 = cur.T.y, k1 = cur.T.z;
+        const bool recent = cur.T.w & 1;
+        const int nch = cur.T.w >> 8;
+        unsigned long long tr0 = 0, tr1 = 0;
+        if (a.trace && recent) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr0));
         double acc = 0.0;
-        for (int base = k0; base < k1; base += 256) {
+        {
+            int kk[8];
+            double y[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                kk[q] = cur.cc[q] >= 0 ? k0 : k1;  // "valid" marker for warp_wait_ready
+                y[q] = cur.cc[q] >= 0 ? __ldca(a.out + cur.cc[q]) : 0.0;
+            }
+            warp_wait_ready<8>(a.out, cur.cc, kk, k1, y, a.spin_ns);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc += cur.v[q] * y[q];
+        }
+        for (int base = k0 + 256; base < k1; base += 256) {  // long recent tasks only
             int kk[8], cc[8];
             double v[8], y[8];
 #pragma unroll
@@ -1035,21 +1230,36 @@ __global__ void __launch_bounds__(256, EXG_CHAIN_MINB)
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
-        if (lane == 0) {
-            if ((T.w & 1) == 0) {
-                st_relaxed(a.part + p, acc);
-            } else {
-                const int r = a.rows[p];
-                const double b = UPPER ? a.in[r] : a.in[a.in_perm[r]];
-                double old = 0.0;
-                if (T.w & 2) {
-                    unsigned long long ob = ld_relaxed(a.part + p);
-                    while (ob == kSentinel) ob = ld_relaxed(a.part + p);
-                    old = __longlong_as_double(ob);
-                }
-                st_relaxed(a.s + p, b - (old + acc));
+        if (a.trace && recent) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr1));
+        if (!recent) {
+            if (lane == 0) st_relaxed(a.part + p, acc);
+        } else {
+            // chunk partials, summed in chunk order (deterministic)
+            double old = 0.0;
+            unsigned long long pv = cur.pv;
+            for (int c0 = 0; c0 < nch; c0 += 32) {
+                const int ci = c0 + lane;
+                if (c0 > 0) pv = ci < nch ? ld_relaxed(a.part + cur.slot0 + ci) : 0ull;
+                while (!__all_sync(FULL, ci >= nch || pv != kSentinel))
+                    if (ci < nch && pv == kSentinel) pv = ld_relaxed(a.part + cur.slot0 + ci);
+                double g = ci < nch ? __longlong_as_double(pv) : 0.0;  // fixed butterfly: deterministic
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) g += __shfl_xor_sync(FULL, g, o);
+                old += g;
+            }
+            if (lane == 0) st_relaxed(a.s + p, cur.b - (old + acc));
+            if (a.trace && lane == 0) {
+                unsigned long long tr2;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr2));
+                unsigned long long* wt = a.trace + 4 * a.n_blocks + 3 * (long long)p;
+                wt[0] = tr0;
+                wt[1] = tr1;
+                wt[2] = tr2;
             }
         }
+        if (tn >= a.n_tasks) return;
+        t = tn;
+        cur = nxt;
     }
 }
 
@@ -2279,14 +2489,16 @@ void trsv_chain(const Launch& L, bool upper, const ChainArgs& a) {
     static int occ[2] = {0, 0};
     auto fn = upper ? (void*)k_trsv_chain<true> : (void*)k_trsv_chain<false>;
     if (!attr[upper]) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[upper], upper ? k_trsv_chain<true> : k_trsv_chain<false>, 256, 0);
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kChainSmem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[upper], upper ? k_trsv_chain<true> : k_trsv_chain<false>, 256,
+                                                      kChainSmem);
         if (occ[upper] < 1) occ[upper] = 1;
         attr[upper] = true;
     }
     const unsigned int grid = (unsigned int)std::max<long long>(
         2, std::min<long long>((long long)L.num_sms * occ[upper], 1 + ((long long)a.n_rows + 7) / 8));
     void* args[] = {(void*)&a};
-    cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(256), args, 0, L.stream);
+    cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(256), args, kChainSmem, L.stream);
     count(L);
 }
 

@@ -1010,17 +1010,19 @@ __global__ void __launch_bounds__(256, EXG_CHAIN_MINB)
         }
         for (int i = tid; i < 3 * kXs; i += blockDim.x) xr[i] = 0.0;
         __syncthreads();
+        // the chain's matrices are re-read by every solve: keep them in L2
+        // (evict_last) while the factors stream past them
+        unsigned long long pol;
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
         auto issue = [&](int kb, int4 O) {  // thread 0
             const int st = kb & 1;
             const unsigned mb = mb0 + 8 * st;
             const unsigned cnt = (O.x >= 0 ? 1u : 0u) + (O.y >= 0 ? 1u : 0u) + (O.z >= 0 ? 1u : 0u);
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            // (no proxy fence: the stage's previous generic reads are ordered
+            // before this async write by the block barrier that ended them)
             asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(mb),
                          "r"(cnt * (unsigned)(kBlk * kBlk * sizeof(double))) : "memory");
             const int offs[3] = {O.x, O.y, O.z};
-            // re-read by every solve: keep in L2 while the factors stream past
-            unsigned long long pol;
-            asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
 #pragma unroll
             for (int q = 0; q < 3; ++q) {
                 if (offs[q] < 0) continue;

@@ -657,15 +657,17 @@ void plan_triangle(exg_ctx* c, TriPlan& P, bool upper_tri, const std::vector<int
                         for (int m2 = jc; m2 < i; ++m2) sacc -= Dm[i * kB + m2] * Di[m2 * kB + jc];
                         Di[i * kB + jc] = sacc / Dm[i * kB + i];
                     }
-                // chain layout (k_trsv_chain): thread t of the chain CTA owns
-                // row t/4, columns (t%4)*16 .. +15; element j of thread t is at
-                // j*256 + t, so every shared-memory read is conflict-free
+                // chain layout (k_trsv_chain): half c of a matrix (rows
+                // 32c..32c+31) belongs to CTA c of the chain pair; its thread
+                // t owns local row t/8, columns (t%8)*8 .. +7, element j at
+                // c*2048 + j*256 + t, so every shared-memory read is conflict-free
                 auto push_mat = [&](const std::vector<double>& M) {
                     const int o = (int)pool.size();
                     pool.resize(pool.size() + kB * kB);
-                    for (int j = 0; j < 16; ++j)
-                        for (int t = 0; t < 256; ++t)
-                            pool[o + j * 256 + t] = M[(t >> 2) * kB + (t & 3) * 16 + j];
+                    for (int c2 = 0; c2 < 2; ++c2)
+                        for (int j = 0; j < 8; ++j)
+                            for (int t = 0; t < 256; ++t)
+                                pool[o + c2 * 2048 + j * 256 + t] = M[(32 * c2 + (t >> 3)) * kB + (t & 7) * 8 + j];
                     return o;
                 };
                 auto times_dinv = [&](const std::vector<double>& E) {

@@ -37,14 +37,31 @@ __device__ __forceinline__ void spmv_warp_rows(const int* __restrict__ rowptr,
     const int k0 = rowptr[r0], k1 = rowptr[r_end];
     const int r = r0 + lane;
     if (k1 - k0 <= kSpmvCap) {
-        for (int k = k0 + lane; k < k1; k += 32) {
-            s_col[w][k - k0] = col[k];
-            s_val[w][k - k0] = val[k];
+        // staging: 8 independent loads in flight per lane per round trip
+        for (int k = k0 + lane; k < k1; k += 256) {
+            int cc[8];
+            double vv[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int kk = k + 32 * q;
+                cc[q] = kk < k1 ? __ldcs(col + kk) : 0;
+                vv[q] = kk < k1 ? __ldcs(val + kk) : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int kk = k + 32 * q;
+                if (kk < k1) {
+                    s_col[w][kk - k0] = cc[q];
+                    s_val[w][kk - k0] = vv[q];
+                }
+            }
         }
         __syncwarp();
         if (r < n_rows) {
             double s = 0.0;
             const int a = rowptr[r] - k0, b = rowptr[r + 1] - k0;
+            // the gathers are independent of the (in-order) accumulation
+#pragma unroll 4
             for (int k = a; k < b; ++k) s += s_val[w][k] * xfn(s_col[w][k]);
             out(r, s);
         }
@@ -786,7 +803,7 @@ __global__ void __launch_bounds__(EXG_NARROW_THREADS, 1)
 // (DSMEM) and to global memory.
 // ---------------------------------------------------------------------------
 constexpr int kBlk = 64;
-constexpr size_t kChainSmem = 2 * 3 * kBlk * kBlk * sizeof(double);  // chain CTA: 2 stages x (Dinv, F1, F2)
+constexpr size_t kChainSmem = 2 * 3 * (kBlk * kBlk / 2) * sizeof(double);  // chain pair CTA: 2 stages x half of (Dinv, F1, F2)
 
 // GEMV of one warp's 8 outputs against a 64-vector held as (x0, x1) =
 // (v[lane], v[lane+32]); f0/f1 hold the warp's 8 matrix rows the same way.
@@ -986,22 +1003,28 @@ __global__ void __launch_bounds__(256, EXG_CHAIN_MINB)
     if (a.ctrl && (a.ctrl->converged || a.ctrl->status)) return;
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (blockIdx.x == 0) {
-        // ===================== chain CTA =====================
-        // Block k's Dinv/F1/F2 (3 x 32 KB) arrive in shared memory by TMA
-        // bulk copies issued one block ahead (two stages, one mbarrier each),
-        // in the thread-major layout written by the planner: thread t owns
-        // row t/4 and columns (t%4)*16..+15 of every matrix (conflict-free
-        // reads, a 2-step shuffle reduction).  Block metadata, row ids and
-        // epilogue operands are loaded one or two blocks ahead, and F2 x_{k-2},
-        // F1 x_{k-1} are formed before the wait for s, so after s arrives only
-        // Dinv s, the publication and one barrier remain.
-        constexpr int kXs = 68;  // padded x slot: column c at c + c/16
-        extern __shared__ __align__(128) double smat[];  // [2 stages][3][kBlk*kBlk]
-        __shared__ double xr[3 * kXs];                   // x of the last 3 blocks
+    if (blockIdx.x < 2) {
+        // ===================== chain pair =====================
+        // The chain is a 2-CTA cluster on two SMs: CTA c owns rows
+        // 32c..32c+31 of every 64-row block, so each SM ingests and multiplies
+        // half of the block matrices.  Block k's half of Dinv/F1/F2
+        // (3 x 16 KB) arrives by TMA one block ahead (two stages, one mbarrier
+        // each), in the thread-major layout written by the planner: thread t
+        // owns local row t/8 and columns (t%8)*8..+7 (conflict-free reads,
+        // 3-step shuffle reduction).  A block's x values are pushed into both
+        // CTAs' rings (local + DSMEM store) and the pair meets at one cluster
+        // barrier per block.  Metadata, row ids and epilogue operands are
+        // loaded one or two blocks ahead, and F2 x_{k-2}, F1 x_{k-1} are formed
+        // before the wait for s.
+        constexpr int kXs = 72;   // padded x slot: column c at c + c/8
+        constexpr int kHalf = kBlk * kBlk / 2;
+        extern __shared__ __align__(128) double smat[];  // [2 stages][3][kHalf]
+        __shared__ double xr[3 * kXs];                   // x of the last 3 blocks (both halves)
         __shared__ double sw[8 * kXs];                   // each warp's copy of the block's s
         __shared__ __align__(8) unsigned long long mbar[2];
-        const int tid = threadIdx.x, row = tid >> 2, qd = tid & 3;
+        const int cr = blockIdx.x;  // rank in the pair
+        const int tid = threadIdx.x, rl = tid >> 3, oc = tid & 7;
+        const int row = 32 * cr + rl;  // row of the block owned by this thread group
         const unsigned mb0 = (unsigned)__cvta_generic_to_shared(&mbar[0]);
         if (tid == 0) {
             asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(mb0));
@@ -1009,27 +1032,32 @@ __global__ void __launch_bounds__(256, EXG_CHAIN_MINB)
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
         for (int i = tid; i < 3 * kXs; i += blockDim.x) xr[i] = 0.0;
-        __syncthreads();
+        // the peer's ring (DSMEM address of xr in the other CTA)
+        unsigned xr_peer;
+        {
+            const unsigned xl = (unsigned)__cvta_generic_to_shared(xr);
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(xr_peer) : "r"(xl), "r"(cr ^ 1));
+        }
+        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+        asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
         // the chain's matrices are re-read by every solve: keep them in L2
         // (evict_last) while the factors stream past them
         unsigned long long pol;
         asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-        auto issue = [&](int kb, int4 O) {  // thread 0
+        auto issue = [&](int kb, int4 O) {  // thread 0 of each CTA: its half
             const int st = kb & 1;
             const unsigned mb = mb0 + 8 * st;
             const unsigned cnt = (O.x >= 0 ? 1u : 0u) + (O.y >= 0 ? 1u : 0u) + (O.z >= 0 ? 1u : 0u);
-            // (no proxy fence: the stage's previous generic reads are ordered
-            // before this async write by the block barrier that ended them)
             asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(mb),
-                         "r"(cnt * (unsigned)(kBlk * kBlk * sizeof(double))) : "memory");
+                         "r"(cnt * (unsigned)(kHalf * sizeof(double))) : "memory");
             const int offs[3] = {O.x, O.y, O.z};
 #pragma unroll
             for (int q = 0; q < 3; ++q) {
                 if (offs[q] < 0) continue;
-                const unsigned dst = (unsigned)__cvta_generic_to_shared(smat + (st * 3 + q) * kBlk * kBlk);
+                const unsigned dst = (unsigned)__cvta_generic_to_shared(smat + (st * 3 + q) * kHalf);
                 asm volatile(
                     "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(dst),
-                    "l"(a.pool + offs[q]), "r"((unsigned)(kBlk * kBlk * sizeof(double))), "r"(mb), "l"(pol)
+                    "l"(a.pool + offs[q] + cr * kHalf), "r"((unsigned)(kHalf * sizeof(double))), "r"(mb), "l"(pol)
                     : "memory");
             }
         };
@@ -1049,42 +1077,43 @@ __global__ void __launch_bounds__(256, EXG_CHAIN_MINB)
         int4 B1 = nbk > 1 ? a.blocks[3] : make_int4(0, 0, 0, 0);
         int4 O1 = nbk > 1 ? a.blocks[4] : make_int4(-1, -1, -1, 0);
         if (tid == 0) issue(0, Oc);
-        int2 rq = (qd == 0 && row < Bc.y) ? a.rq[Bc.x + row] : make_int2(0, 0);
+        int2 rq = (oc == 0 && row < Bc.y) ? a.rq[Bc.x + row] : make_int2(0, 0);
         double s0 = lane < Bc.y ? __longlong_as_double(ld_relaxed(a.s + Bc.x + lane)) : 0.0;
         double s1 = lane + 32 < Bc.y ? __longlong_as_double(ld_relaxed(a.s + Bc.x + lane + 32)) : 0.0;
         double* swp = sw + warp * kXs;
         for (int kb = 0; kb < nbk; ++kb) {
             const int nb = Bc.y;
-            // ---- one and two blocks ahead (nothing below consumes these
-            // before the next iteration, so none of the loads stalls)
+            // ---- one and two blocks ahead (consumed next iteration: no stall)
             if (tid == 0 && kb + 1 < nbk) issue(kb + 1, O1);
             const int4 B2 = kb + 2 < nbk ? a.blocks[3 * (kb + 2)] : make_int4(0, 0, 0, 0);
             const int4 O2 = kb + 2 < nbk ? a.blocks[3 * (kb + 2) + 1] : make_int4(-1, -1, -1, 0);
-            const int2 rqn = (qd == 0 && kb + 1 < nbk && row < B1.y) ? a.rq[B1.x + row] : make_int2(0, 0);
+            const int2 rqn = (oc == 0 && kb + 1 < nbk && row < B1.y) ? a.rq[B1.x + row] : make_int2(0, 0);
             const double sn0 = (kb + 1 < nbk && lane < B1.y) ? __longlong_as_double(ld_relaxed(a.s + B1.x + lane)) : 0.0;
             const double sn1 = (kb + 1 < nbk && lane + 32 < B1.y) ? __longlong_as_double(ld_relaxed(a.s + B1.x + lane + 32)) : 0.0;
-            const double ad = (a.final_out && a.add && qd == 0 && row < nb) ? a.add[rq.y] : 0.0;
+            const double ad = (a.final_out && a.add && oc == 0 && row < nb) ? a.add[rq.y] : 0.0;
             // ---- F2 x_{k-2} and F1 x_{k-1}
             wait_stage(kb);
             unsigned long long t_w = 0;
             if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_w));
-            const double* Ms = smat + (kb & 1) * 3 * kBlk * kBlk;
+            const double* Ms = smat + (kb & 1) * 3 * kHalf;
             double p2 = 0.0, p1 = 0.0;
             if (Oc.z >= 0) {
-                const double* xg = xr + ((kb - 2) % 3) * kXs + qd * 17;
-                const double* M = Ms + 2 * kBlk * kBlk + tid;
+                const double* xg = xr + ((kb - 2) % 3) * kXs + oc * 9;
+                const double* M = Ms + 2 * kHalf + tid;
 #pragma unroll
-                for (int j = 0; j < 16; ++j) p2 += M[j * 256] * xg[j];
+                for (int j = 0; j < 8; ++j) p2 += M[j * 256] * xg[j];
                 p2 += __shfl_xor_sync(FULL, p2, 1);
                 p2 += __shfl_xor_sync(FULL, p2, 2);
+                p2 += __shfl_xor_sync(FULL, p2, 4);
             }
             if (Oc.y >= 0) {
-                const double* xg = xr + ((kb - 1) % 3) * kXs + qd * 17;
-                const double* M = Ms + kBlk * kBlk + tid;
+                const double* xg = xr + ((kb - 1) % 3) * kXs + oc * 9;
+                const double* M = Ms + kHalf + tid;
 #pragma unroll
-                for (int j = 0; j < 16; ++j) p1 += M[j * 256] * xg[j];
+                for (int j = 0; j < 8; ++j) p1 += M[j * 256] * xg[j];
                 p1 += __shfl_xor_sync(FULL, p1, 1);
                 p1 += __shfl_xor_sync(FULL, p1, 2);
+                p1 += __shfl_xor_sync(FULL, p1, 4);
             }
             unsigned long long t_m = 0;
             if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_m));
@@ -1104,35 +1133,40 @@ __global__ void __launch_bounds__(256, EXG_CHAIN_MINB)
             }
             unsigned long long t_s = 0;
             if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_s));
-            swp[lane + (lane >> 4)] = s0;
-            swp[lane + 32 + ((lane + 32) >> 4)] = s1;
+            swp[lane + (lane >> 3)] = s0;
+            swp[lane + 32 + ((lane + 32) >> 3)] = s1;
             __syncwarp();
             double cx;
             if (Oc.x >= 0) {
                 const double* M = Ms + tid;
-                const double* sg = swp + qd * 17;
+                const double* sg = swp + oc * 9;
                 cx = 0.0;
 #pragma unroll
-                for (int j = 0; j < 16; ++j) cx += M[j * 256] * sg[j];
+                for (int j = 0; j < 8; ++j) cx += M[j * 256] * sg[j];
                 cx += __shfl_xor_sync(FULL, cx, 1);
                 cx += __shfl_xor_sync(FULL, cx, 2);
+                cx += __shfl_xor_sync(FULL, cx, 4);
             } else {
-                cx = row < nb ? swp[row + (row >> 4)] : 0.0;
+                cx = row < nb ? swp[row + (row >> 3)] : 0.0;
             }
             if (Oc.z >= 0) cx = cx - p2;
             if (Oc.y >= 0) cx = cx - p1;
-            // ---- publish x_k: chain ring + global solution; epilogue after
-            if (qd == 0) {
-                xr[(kb % 3) * kXs + row + (row >> 4)] = row < nb ? cx : 0.0;
+            // ---- publish x_k: both rings (local + DSMEM) + global solution
+            if (oc == 0) {
+                const double xv = row < nb ? cx : 0.0;
+                const int xi = (kb % 3) * kXs + row + (row >> 3);
+                xr[xi] = xv;
+                asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(xr_peer + 8u * (unsigned)xi), "d"(xv) : "memory");
                 if (row < nb) st_relaxed(a.out + rq.x, cx);
             }
-            __syncthreads();
-            if (qd == 0 && row < nb && a.final_out) {
+            asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+            asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+            if (oc == 0 && row < nb && a.final_out) {
                 double yo = a.coef * cx;
                 if (a.add) yo = ad + yo;
                 a.final_out[rq.y] = yo;
             }
-            if (a.trace && tid == 0) {
+            if (a.trace && tid == 0 && cr == 0) {
                 unsigned long long t_e;
                 asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_e));
                 a.trace[4 * kb] = t_w;
@@ -1159,8 +1193,8 @@ __global__ void __launch_bounds__(256, EXG_CHAIN_MINB)
     // and (recent tasks) right-hand side and chunk partials are loaded while
     // the current task waits, so a task costs one L2 round trip, not three
     // dependent HBM loads.
-    const int gw = (blockIdx.x - 1) * (blockDim.x >> 5) + warp;
-    const int W = (gridDim.x - 1) * (blockDim.x >> 5);
+    const int gw = (blockIdx.x - 2) * (blockDim.x >> 5) + warp;
+    const int W = (gridDim.x - 2) * (blockDim.x >> 5);
     struct Stage {
         int4 T;
         int cc[8];
@@ -2497,10 +2531,29 @@ void trsv_chain(const Launch& L, bool upper, const ChainArgs& a) {
         if (occ[upper] < 1) occ[upper] = 1;
         attr[upper] = true;
     }
-    const unsigned int grid = (unsigned int)std::max<long long>(
-        2, std::min<long long>((long long)L.num_sms * occ[upper], 1 + ((long long)a.n_rows + 7) / 8));
-    void* args[] = {(void*)&a};
-    cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(256), args, kChainSmem, L.stream);
+    // even grid (clusters of 2: CTAs 0-1 = the chain pair, the rest workers);
+    // cooperative so every worker is resident while the chain waits on them
+    long long g = std::max<long long>(4, std::min<long long>((long long)L.num_sms * occ[upper],
+                                                             2 + ((long long)a.n_rows + 7) / 8));
+    g &= ~1LL;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)g);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = kChainSmem;
+    cfg.stream = L.stream;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeCooperative;
+    at[1].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    if (upper)
+        cudaLaunchKernelEx(&cfg, k_trsv_chain<true>, a);
+    else
+        cudaLaunchKernelEx(&cfg, k_trsv_chain<false>, a);
     count(L);
 }
 

@@ -803,7 +803,12 @@ __global__ void __launch_bounds__(EXG_NARROW_THREADS, 1)
 // (DSMEM) and to global memory.
 // ---------------------------------------------------------------------------
 constexpr int kBlk = 64;
-constexpr size_t kChainSmem = 2 * 3 * (kBlk * kBlk / 2) * sizeof(double);  // chain pair CTA: 2 stages x half of (Dinv, F1, F2)
+constexpr int kChainStages = 3;  // TMA stages of the chain: block k+2 is in flight while k computes
+constexpr size_t kChainMats = kChainStages * 3 * (kBlk * kBlk / 2) * sizeof(double);  // half of (Dinv, F1, F2) per stage
+// launched with more than half an SM's shared memory so that no worker CTA
+// shares an SM with a chain CTA (one CTA per SM)
+constexpr size_t kChainSmem = kChainMats > 120 * 1024 ? kChainMats : 120 * 1024;
+static_assert(kChainSmem >= kChainMats, "chain smem");
 
 // GEMV of one warp's 8 outputs against a 64-vector held as (x0, x1) =
 // (v[lane], v[lane+32]); f0/f1 hold the warp's 8 matrix rows the same way.
@@ -1021,23 +1026,43 @@ __global__ void __launch_bounds__(256, EXG_CHAIN_MINB)
         extern __shared__ __align__(128) double smat[];  // [2 stages][3][kHalf]
         __shared__ double xr[3 * kXs];                   // x of the last 3 blocks (both halves)
         __shared__ double sw[8 * kXs];                   // each warp's copy of the block's s
-        __shared__ __align__(8) unsigned long long mbar[2];
+        __shared__ __align__(8) unsigned long long mbar[kChainStages];
+        __shared__ __align__(8) unsigned long long xbar[2];  // peer's half of x_k landed (st.async)
         const int cr = blockIdx.x;  // rank in the pair
         const int tid = threadIdx.x, rl = tid >> 3, oc = tid & 7;
         const int row = 32 * cr + rl;  // row of the block owned by this thread group
         const unsigned mb0 = (unsigned)__cvta_generic_to_shared(&mbar[0]);
+        const unsigned xb0 = (unsigned)__cvta_generic_to_shared(&xbar[0]);
         if (tid == 0) {
-            asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(mb0));
-            asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(mb0 + 8));
+            for (int q = 0; q < kChainStages; ++q)
+                asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(mb0 + 8 * q));
+            asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(xb0));
+            asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(xb0 + 8));
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
         for (int i = tid; i < 3 * kXs; i += blockDim.x) xr[i] = 0.0;
-        // the peer's ring (DSMEM address of xr in the other CTA)
-        unsigned xr_peer;
+        // the peer's ring and x-arrival barriers (DSMEM addresses in the other CTA)
+        unsigned xr_peer, xb_peer;
         {
             const unsigned xl = (unsigned)__cvta_generic_to_shared(xr);
             asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(xr_peer) : "r"(xl), "r"(cr ^ 1));
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(xb_peer) : "r"(xb0), "r"(cr ^ 1));
         }
+        // block k's peer half: 32 values of 8 B, announced one block ahead
+        auto expect_x = [&](int kb) {
+            asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(xb0 + 8 * (kb & 1)),
+                         "r"(32u * 8u) : "memory");
+        };
+        auto wait_x = [&](int kb) {
+            const unsigned mb = xb0 + 8 * (kb & 1);
+            const unsigned par = (unsigned)((kb >> 1) & 1);
+            unsigned done = 0;
+            while (!done) {
+                asm volatile(
+                    "{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                    : "=r"(done) : "r"(mb), "r"(par) : "memory");
+            }
+        };
         asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
         asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
         // the chain's matrices are re-read by every solve: keep them in L2
@@ -1045,7 +1070,7 @@ __global__ void __launch_bounds__(256, EXG_CHAIN_MINB)
         unsigned long long pol;
         asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
         auto issue = [&](int kb, int4 O) {  // thread 0 of each CTA: its half
-            const int st = kb & 1;
+            const int st = kb % kChainStages;
             const unsigned mb = mb0 + 8 * st;
             const unsigned cnt = (O.x >= 0 ? 1u : 0u) + (O.y >= 0 ? 1u : 0u) + (O.z >= 0 ? 1u : 0u);
             asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(mb),
@@ -1062,8 +1087,8 @@ __global__ void __launch_bounds__(256, EXG_CHAIN_MINB)
             }
         };
         auto wait_stage = [&](int kb) {
-            const unsigned mb = mb0 + 8 * (kb & 1);
-            const unsigned par = (unsigned)((kb >> 1) & 1);
+            const unsigned mb = mb0 + 8 * (kb % kChainStages);
+            const unsigned par = (unsigned)((kb / kChainStages) & 1);
             unsigned done = 0;
             while (!done) {
                 asm volatile(
@@ -1073,20 +1098,39 @@ __global__ void __launch_bounds__(256, EXG_CHAIN_MINB)
         };
         const int nbk = a.n_blocks;
         if (nbk == 0) return;
-        int4 Bc = a.blocks[0], Oc = a.blocks[1];
-        int4 B1 = nbk > 1 ? a.blocks[3] : make_int4(0, 0, 0, 0);
-        int4 O1 = nbk > 1 ? a.blocks[4] : make_int4(-1, -1, -1, 0);
-        if (tid == 0) issue(0, Oc);
+        // block metadata ring in shared memory (block j in slot j % 3): the
+        // copy of block j+2 is loaded by the last thread during block j and
+        // stored just before the block's barrier, so no thread ever stalls on
+        // a metadata load (a register->uniform move of a pending load would)
+        constexpr int kAhead = kChainStages - 1;  // TMA prefetch distance (blocks)
+        constexpr int kMeta = kAhead + 2;          // metadata ring slots
+        __shared__ int4 meta_s[kMeta][2];
+        if (tid < kMeta - 1) {
+            meta_s[tid][0] = tid < nbk ? a.blocks[3 * tid] : make_int4(0, 0, 0, 0);
+            meta_s[tid][1] = tid < nbk ? a.blocks[3 * tid + 1] : make_int4(-1, -1, -1, 0);
+        }
+        __syncthreads();
+        int4 Bc = meta_s[0][0], Oc = meta_s[0][1];
+        if (tid == 0) {
+            for (int q = 0; q < kAhead && q < nbk; ++q) issue(q, meta_s[q][1]);
+            expect_x(0);
+        }
         int2 rq = (oc == 0 && row < Bc.y) ? a.rq[Bc.x + row] : make_int2(0, 0);
         double s0 = lane < Bc.y ? __longlong_as_double(ld_relaxed(a.s + Bc.x + lane)) : 0.0;
         double s1 = lane + 32 < Bc.y ? __longlong_as_double(ld_relaxed(a.s + Bc.x + lane + 32)) : 0.0;
         double* swp = sw + warp * kXs;
         for (int kb = 0; kb < nbk; ++kb) {
+            Bc = meta_s[kb % kMeta][0];
+            Oc = meta_s[kb % kMeta][1];
+            const int4 B1 = meta_s[(kb + 1) % kMeta][0];
             const int nb = Bc.y;
-            // ---- one and two blocks ahead (consumed next iteration: no stall)
-            if (tid == 0 && kb + 1 < nbk) issue(kb + 1, O1);
-            const int4 B2 = kb + 2 < nbk ? a.blocks[3 * (kb + 2)] : make_int4(0, 0, 0, 0);
-            const int4 O2 = kb + 2 < nbk ? a.blocks[3 * (kb + 2) + 1] : make_int4(-1, -1, -1, 0);
+            // ---- blocks ahead (consumed in later iterations: no stall)
+            if (tid == 0 && kb + kAhead < nbk) issue(kb + kAhead, meta_s[(kb + kAhead) % kMeta][1]);
+            int4 B2 = make_int4(0, 0, 0, 0), O2 = make_int4(-1, -1, -1, 0);
+            if (tid == blockDim.x - 1 && kb + kAhead + 1 < nbk) {
+                B2 = a.blocks[3 * (kb + kAhead + 1)];
+                O2 = a.blocks[3 * (kb + kAhead + 1) + 1];
+            }
             const int2 rqn = (oc == 0 && kb + 1 < nbk && row < B1.y) ? a.rq[B1.x + row] : make_int2(0, 0);
             const double sn0 = (kb + 1 < nbk && lane < B1.y) ? __longlong_as_double(ld_relaxed(a.s + B1.x + lane)) : 0.0;
             const double sn1 = (kb + 1 < nbk && lane + 32 < B1.y) ? __longlong_as_double(ld_relaxed(a.s + B1.x + lane + 32)) : 0.0;
@@ -1095,7 +1139,7 @@ __global__ void __launch_bounds__(256, EXG_CHAIN_MINB)
             wait_stage(kb);
             unsigned long long t_w = 0;
             if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_w));
-            const double* Ms = smat + (kb & 1) * 3 * kHalf;
+            const double* Ms = smat + (kb % kChainStages) * 3 * kHalf;
             double p2 = 0.0, p1 = 0.0;
             if (Oc.z >= 0) {
                 const double* xg = xr + ((kb - 2) % 3) * kXs + oc * 9;
@@ -1106,6 +1150,11 @@ __global__ void __launch_bounds__(256, EXG_CHAIN_MINB)
                 p2 += __shfl_xor_sync(FULL, p2, 2);
                 p2 += __shfl_xor_sync(FULL, p2, 4);
             }
+            // the peer's half of x_{k-1} (x_{k-2} was waited for last block);
+            // the barrier just completed is re-armed for block k+1 (the peer
+            // cannot send block k+1 before it has our x_k)
+            if (kb >= 1) wait_x(kb - 1);
+            if (tid == 0 && kb + 1 < nbk) expect_x(kb + 1);
             if (Oc.y >= 0) {
                 const double* xg = xr + ((kb - 1) % 3) * kXs + oc * 9;
                 const double* M = Ms + kHalf + tid;
@@ -1151,16 +1200,24 @@ __global__ void __launch_bounds__(256, EXG_CHAIN_MINB)
             }
             if (Oc.z >= 0) cx = cx - p2;
             if (Oc.y >= 0) cx = cx - p1;
-            // ---- publish x_k: both rings (local + DSMEM) + global solution
+            // ---- publish x_k: own ring, the peer's ring (st.async completing
+            // on the peer's x barrier: no cluster-wide barrier, no release of
+            // the global stores on the hand-off path), global solution
             if (oc == 0) {
                 const double xv = row < nb ? cx : 0.0;
                 const int xi = (kb % 3) * kXs + row + (row >> 3);
                 xr[xi] = xv;
-                asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(xr_peer + 8u * (unsigned)xi), "d"(xv) : "memory");
+                asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(
+                                 xr_peer + 8u * (unsigned)xi),
+                             "l"(__double_as_longlong(xv)), "r"(xb_peer + 8u * (unsigned)(kb & 1))
+                             : "memory");
                 if (row < nb) st_relaxed(a.out + rq.x, cx);
             }
-            asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-            asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+            if (tid == blockDim.x - 1) {
+                meta_s[(kb + kAhead + 1) % kMeta][0] = B2;
+                meta_s[(kb + kAhead + 1) % kMeta][1] = O2;
+            }
+            __syncthreads();
             if (oc == 0 && row < nb && a.final_out) {
                 double yo = a.coef * cx;
                 if (a.add) yo = ad + yo;
@@ -1174,14 +1231,14 @@ __global__ void __launch_bounds__(256, EXG_CHAIN_MINB)
                 a.trace[4 * kb + 2] = t_s;
                 a.trace[4 * kb + 3] = t_e;
             }
-            Bc = B1;
-            Oc = O1;
-            B1 = B2;
-            O1 = O2;
             rq = rqn;
             s0 = sn0;
             s1 = sn1;
         }
+        // the peer's last st.async must land before this CTA may exit
+        wait_x(nbk - 1);
+        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+        asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
         return;
     }
     // ===================== workers =====================

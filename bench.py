@@ -36,6 +36,11 @@ FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
 METRIC = "time-steps/s (ER, config 1: 1M-node RC mesh)"
 
 
+def CFG_FIXED_STEP(s) -> bool:
+    """BASELINE.json runs configs 0 and 3 with fixed 1 ps steps."""
+    return getattr(s, "config", None) in (0, 3)
+
+
 # ---------------------------------------------------------------------------
 def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -159,7 +164,12 @@ def hbm_peak():
 def setup_system(args):
     import paper_1511_04515_b200 as ex
     t0 = time.perf_counter()
-    s = ex.System.generate(args.config, width=args.width)
+    width = args.width if args.config in (1, 2, 4) else 0  # configs 0 and 3 have fixed sizes
+    if args.config == 2 and args.width == 1000:
+        width = 0  # config 2's full size is 500x500
+    if args.config == 4 and args.width == 1000:
+        width = 0
+    s = ex.System.generate(args.config, width=width)
     t1 = time.perf_counter()
     # optional on-disk factor cache for profiling sessions (several bench
     # invocations in one gpurun call); keyed by the exact G arrays
@@ -223,8 +233,11 @@ def run_ours(args, rank, world, local):
 
     s, f, setup = setup_system(args)
     ctl = s.step_control()
+    if CFG_FIXED_STEP(s):  # configs 0 and 3: fixed 1 ps steps (BASELINE.json)
+        ctl.fixed_step = 1
+        ctl.h_init = 1e-12
     t_stop = s.options().tran_stop
-    sched = step_schedule(s, ctl, t_stop, args.warmup + args.steps + args.e2e_steps + 4)
+    sched = step_schedule(s, ctl, t_stop, args.warmup + args.steps + 4)
     if len(sched) < args.warmup + args.steps:
         raise SystemExit("transient too short for the requested steps")
     mode = F.EXG_TRSV_FAST if args.trsv == "fast" else F.EXG_TRSV_EXACT
@@ -334,28 +347,37 @@ def run_ours(args, rank, world, local):
                 "per_kernel": roof, "l_levels": cn.l_levels, "u_levels": cn.u_levels,
                 "kernel_ms": ktimes}
 
-    # ---- e2e: the public per-step call with HOST buffers (H2D of x_k and the
-    # source values, D2H of x_next), continuing the same transient right
-    # after the timed steps
-    xh = np.zeros(n)
-    ctx._check(lib.exg_memcpy(h, xh.ctypes.data, dx, 8 * n, 2))  # state after the timed region
-    e2e_steps = min(args.e2e_steps, len(sched) - nsteps)
-    xn = np.zeros(n)
+    # ---- e2e: the public per-step call with HOST buffers over the SAME steps
+    # as the timed region (state restored to the post-warm-up x): every step
+    # copies x_k and the source values from pinned host memory to the device
+    # and reads x_next back (exg_er_step, EXG_PTR_HOST)
+    xh_t = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    xn_t = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    ni1 = max(ni, 1)
+    uk_t = torch.empty(ni1, dtype=torch.float64, pin_memory=True)
+    uk1_t = torch.empty(ni1, dtype=torch.float64, pin_memory=True)
+    xh_t.numpy()[:] = x_w
+    e2e_steps = args.steps
+    e2e_m = []
     ctx.synchronize()
     barrier(world)
     t0 = time.perf_counter()
-    for i in range(nsteps, nsteps + e2e_steps):
+    for i in range(args.warmup, nsteps):
         t, hh = sched[i]
-        uk = np.ascontiguousarray(s.eval_sources(t))
-        uk1 = np.ascontiguousarray(s.eval_sources(t + hh))
+        uk_t.numpy()[:ni] = s.eval_sources(t)
+        uk1_t.numpy()[:ni] = s.eval_sources(t + hh)
         m = C.c_int(-1)
-        ctx._check(lib.exg_er_step(h, xh.ctypes.data, uk.ctypes.data, uk1.ctypes.data, hh, C.byref(cfg),
-                                   xn.ctypes.data, C.byref(m), F.EXG_PTR_HOST))
-        xh, xn = xn, xh
+        ctx._check(lib.exg_er_step(h, C.c_void_p(xh_t.data_ptr()), C.c_void_p(uk_t.data_ptr()),
+                                   C.c_void_p(uk1_t.data_ptr()), hh, C.byref(cfg),
+                                   C.c_void_p(xn_t.data_ptr()), C.byref(m), F.EXG_PTR_HOST))
+        e2e_m.append(m.value)
+        xh_t, xn_t = xn_t, xh_t
     ctx.synchronize()
     e2e_s = allmax(world, time.perf_counter() - t0)
     barrier(world)
     e2e_val = allsum(world, float(e2e_steps)) / e2e_s
+    if e2e_m != m_seq:
+        raise SystemExit(f"e2e Krylov dimensions {e2e_m} differ from the timed region's {m_seq}")
 
     # ---- CPU baseline (rank 0, N = 1): the reference on a bounded sample
     cpu = None
@@ -384,7 +406,7 @@ def run_ours(args, rank, world, local):
         "roofline": roofline, "cpu_baseline": cpu,
         "e2e": {"value": round(e2e_val, 4), "unit": "steps/s",
                 "h2d_bytes_per_step": 8 * n + 16 * ni, "d2h_bytes_per_step": 8 * n,
-                "steps": e2e_steps, "api": "exg_er_step(host buffers)"},
+                "steps": e2e_steps, "api": "exg_er_step(pinned host buffers), same steps as the timed region"},
         "clocks": clk.summary(), "setup": setup,
     }
     if rank == 0:
@@ -401,6 +423,9 @@ def run_reference(args, rank, world):
     from ref import Ref
     s, f, setup = setup_system(args)
     ctl = s.step_control()
+    if CFG_FIXED_STEP(s):  # configs 0 and 3: fixed 1 ps steps (BASELINE.json)
+        ctl.fixed_step = 1
+        ctl.h_init = 1e-12
     t_stop = s.options().tran_stop
     ref = Ref()
     from helpers_bench import ref_system_for
@@ -447,7 +472,7 @@ def main():
     ap.add_argument("--weight", default="gspmv", choices=["apply", "gspmv"])
     ap.add_argument("--loop", default="graph", choices=["graph", "eager"],
                     help="Arnoldi loop as one CUDA graph (default) or eager launches (ncu launch lists)")
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=0, help="(ignored: e2e re-runs the timed steps)")
     ap.add_argument("--profile-steps", type=int, default=2)
     ap.add_argument("--cpu-steps", type=int, default=2)
     args = ap.parse_args()

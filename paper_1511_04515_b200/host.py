@@ -53,7 +53,9 @@ class System:
         p = F.exg_gen_params(config, width, height, n, seed, chains, stages)
         h = C.c_void_p()
         _check(F.lib.exg_system_generate(C.byref(p), C.byref(h)))
-        return cls(h)
+        sys_ = cls(h)
+        sys_.config = config
+        return sys_
 
     @classmethod
     def build(cls, elems, sources, pwl_t, pwl_v, models, opts) -> "System":

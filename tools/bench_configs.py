@@ -26,6 +26,7 @@ ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "oracle"))
 import paper_1511_04515_b200 as ex  # noqa: E402
+from bench import CFG_FIXED_STEP  # noqa: E402
 from paper_1511_04515_b200 import _ffi as F  # noqa: E402
 from paper_1511_04515_b200.device import Context  # noqa: E402
 
@@ -41,6 +42,9 @@ for cfg in [int(x) for x in args.configs.split(",")]:
     s = ex.System.generate(cfg)
     gen_s = time.perf_counter() - t0
     ctl = s.step_control()
+    if CFG_FIXED_STEP(s):  # configs 0 and 3: fixed 1 ps steps (BASELINE.json)
+        ctl.fixed_step = 1
+        ctl.h_init = 1e-12
     t_stop = s.options().tran_stop
     n = s.n
     rng = np.random.default_rng(5)

@@ -657,20 +657,24 @@ void plan_triangle(exg_ctx* c, TriPlan& P, bool upper_tri, const std::vector<int
                         for (int m2 = jc; m2 < i; ++m2) sacc -= Dm[i * kB + m2] * Di[m2 * kB + jc];
                         Di[i * kB + jc] = sacc / Dm[i * kB + i];
                     }
-                // chain layout (k_trsv_chain): half c of a matrix (rows
-                // 32c..32c+31) belongs to CTA c of the chain pair; its thread
-                // t owns local row t/8, columns (t%8)*8 .. +7, element j at
-                // c*2048 + j*256 + t, so every shared-memory read is conflict-free
-                auto push_mat = [&](const std::vector<double>& M) {
-                    const int o = (int)pool.size();
-                    pool.resize(pool.size() + kB * kB);
+                // chain layout (k_trsv_chain): one record of 3 x 64 x 64 per
+                // block, [CTA 0 half: Dinv F1 F2][CTA 1 half: Dinv F1 F2], so
+                // each CTA of the chain pair fetches its 48 KB with ONE bulk
+                // copy.  Half c holds rows 32c..32c+31; its thread t owns local
+                // row t/8, columns (t%8)*8 .. +7, element j at j*256 + t
+                // (conflict-free shared-memory reads).  Absent matrices are
+                // zeros and flagged -1 in the block descriptor.
+                const int rec = (int)pool.size();
+                pool.resize(pool.size() + 3 * kB * kB, 0.0);
+                auto put_mat = [&](const std::vector<double>& M, int q) {
                     for (int c2 = 0; c2 < 2; ++c2)
                         for (int j = 0; j < 8; ++j)
                             for (int t = 0; t < 256; ++t)
-                                pool[o + c2 * 2048 + j * 256 + t] = M[(32 * c2 + (t >> 3)) * kB + (t & 7) * 8 + j];
-                    return o;
+                                pool[rec + c2 * 3 * 2048 + q * 2048 + j * 256 + t] =
+                                    M[(32 * c2 + (t >> 3)) * kB + (t & 7) * 8 + j];
+                    return rec;
                 };
-                auto times_dinv = [&](const std::vector<double>& E) {
+                auto times_dinv = [&](const std::vector<double>& E, int q) {
                     std::fill(Fm.begin(), Fm.end(), 0.0);
                     for (int i = 0; i < bc; ++i)
                         for (int j = 0; j < kB; ++j) {
@@ -678,13 +682,13 @@ void plan_triangle(exg_ctx* c, TriPlan& P, bool upper_tri, const std::vector<int
                             for (int m2 = 0; m2 <= i; ++m2) sacc += Di[i * kB + m2] * E[m2 * kB + j];
                             Fm[i * kB + j] = sacc;
                         }
-                    return push_mat(Fm);
+                    return put_mat(Fm, q);
                 };
-                const int dofs = d_ident ? -1 : push_mat(Di);
-                const int f1 = e1_zero ? -1 : times_dinv(Em);
-                const int f2 = e2_zero ? -1 : times_dinv(E2);
+                const int dofs = d_ident ? -1 : put_mat(Di, 0);
+                const int f1 = e1_zero ? -1 : times_dinv(Em, 1);
+                const int f2 = e2_zero ? -1 : times_dinv(E2, 2);
                 cblocks.push_back(make_int4(kb * kB, bc, 0, 0));
-                cblocks.push_back(make_int4(dofs, f1, f2, 0));
+                cblocks.push_back(make_int4(dofs, f1, f2, rec));  // .w: record offset
                 cblocks.push_back(make_int4(0, 0, 0, 0));
             }
             std::stable_sort(wt.begin(), wt.end(),

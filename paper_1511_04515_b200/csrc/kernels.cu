@@ -1069,22 +1069,16 @@ __global__ void __launch_bounds__(256, EXG_CHAIN_MINB)
         // (evict_last) while the factors stream past them
         unsigned long long pol;
         asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-        auto issue = [&](int kb, int4 O) {  // thread 0 of each CTA: its half
+        auto issue = [&](int kb, int4 O) {  // thread 0 of each CTA: its half, one bulk copy
             const int st = kb % kChainStages;
             const unsigned mb = mb0 + 8 * st;
-            const unsigned cnt = (O.x >= 0 ? 1u : 0u) + (O.y >= 0 ? 1u : 0u) + (O.z >= 0 ? 1u : 0u);
-            asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(mb),
-                         "r"(cnt * (unsigned)(kHalf * sizeof(double))) : "memory");
-            const int offs[3] = {O.x, O.y, O.z};
-#pragma unroll
-            for (int q = 0; q < 3; ++q) {
-                if (offs[q] < 0) continue;
-                const unsigned dst = (unsigned)__cvta_generic_to_shared(smat + (st * 3 + q) * kHalf);
-                asm volatile(
-                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(dst),
-                    "l"(a.pool + offs[q] + cr * kHalf), "r"((unsigned)(kHalf * sizeof(double))), "r"(mb), "l"(pol)
-                    : "memory");
-            }
+            constexpr unsigned bytes = 3u * kHalf * sizeof(double);
+            asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
+            const unsigned dst = (unsigned)__cvta_generic_to_shared(smat + st * 3 * kHalf);
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(dst),
+                "l"(a.pool + O.w + cr * 3 * kHalf), "r"(bytes), "r"(mb), "l"(pol)
+                : "memory");
         };
         auto wait_stage = [&](int kb) {
             const unsigned mb = mb0 + 8 * (kb % kChainStages);
@@ -1116,8 +1110,6 @@ __global__ void __launch_bounds__(256, EXG_CHAIN_MINB)
             expect_x(0);
         }
         int2 rq = (oc == 0 && row < Bc.y) ? a.rq[Bc.x + row] : make_int2(0, 0);
-        double s0 = lane < Bc.y ? __longlong_as_double(ld_relaxed(a.s + Bc.x + lane)) : 0.0;
-        double s1 = lane + 32 < Bc.y ? __longlong_as_double(ld_relaxed(a.s + Bc.x + lane + 32)) : 0.0;
         double* swp = sw + warp * kXs;
         for (int kb = 0; kb < nbk; ++kb) {
             Bc = meta_s[kb % kMeta][0];
@@ -1132,9 +1124,11 @@ __global__ void __launch_bounds__(256, EXG_CHAIN_MINB)
                 O2 = a.blocks[3 * (kb + kAhead + 1) + 1];
             }
             const int2 rqn = (oc == 0 && kb + 1 < nbk && row < B1.y) ? a.rq[B1.x + row] : make_int2(0, 0);
-            const double sn0 = (kb + 1 < nbk && lane < B1.y) ? __longlong_as_double(ld_relaxed(a.s + B1.x + lane)) : 0.0;
-            const double sn1 = (kb + 1 < nbk && lane + 32 < B1.y) ? __longlong_as_double(ld_relaxed(a.s + B1.x + lane + 32)) : 0.0;
             const double ad = (a.final_out && a.add && oc == 0 && row < nb) ? a.add[rq.y] : 0.0;
+            // this block's s: loaded now (the workers published it about a
+            // block ago), consumed after the F gemvs, which hide the round trip
+            double s0 = lane < nb ? __longlong_as_double(ld_relaxed(a.s + Bc.x + lane)) : 0.0;
+            double s1 = lane + 32 < nb ? __longlong_as_double(ld_relaxed(a.s + Bc.x + lane + 32)) : 0.0;
             // ---- F2 x_{k-2} and F1 x_{k-1}
             wait_stage(kb);
             unsigned long long t_w = 0;
@@ -1232,8 +1226,6 @@ __global__ void __launch_bounds__(256, EXG_CHAIN_MINB)
                 a.trace[4 * kb + 3] = t_e;
             }
             rq = rqn;
-            s0 = sn0;
-            s1 = sn1;
         }
         // the peer's last st.async must land before this CTA may exit
         wait_x(nbk - 1);

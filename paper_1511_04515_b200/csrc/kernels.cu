@@ -804,10 +804,11 @@ __global__ void __launch_bounds__(EXG_NARROW_THREADS, 1)
 // ---------------------------------------------------------------------------
 constexpr int kBlk = 64;
 constexpr int kChainStages = 3;  // TMA stages of the chain: block k+2 is in flight while k computes
+constexpr int kChainThreads = 288;  // chain CTAs: 8 compute warps + 1 producer warp; workers use all 9
 constexpr size_t kChainMats = kChainStages * 3 * (kBlk * kBlk / 2) * sizeof(double);  // half of (Dinv, F1, F2) per stage
 // launched with more than half an SM's shared memory so that no worker CTA
 // shares an SM with a chain CTA (one CTA per SM)
-constexpr size_t kChainSmem = kChainMats > 120 * 1024 ? kChainMats : 120 * 1024;
+constexpr size_t kChainSmem = kChainMats > 120 * 1024 ? kChainMats : 120 * 1024;  // > half an SM: one CTA per SM
 static_assert(kChainSmem >= kChainMats, "chain smem");
 
 // GEMV of one warp's 8 outputs against a 64-vector held as (x0, x1) =
@@ -1003,7 +1004,7 @@ __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_g
 #define EXG_CHAIN_MINB 1
 #endif
 template <bool UPPER>
-__global__ void __launch_bounds__(256, EXG_CHAIN_MINB)
+__global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
     k_trsv_chain(ChainArgs a) {
     if (a.ctrl && (a.ctrl->converged || a.ctrl->status)) return;
     const unsigned FULL = 0xffffffffu;
@@ -1011,44 +1012,129 @@ __global__ void __launch_bounds__(256, EXG_CHAIN_MINB)
     if (blockIdx.x < 2) {
         // ===================== chain pair =====================
         // The chain is a 2-CTA cluster on two SMs: CTA c owns rows
-        // 32c..32c+31 of every 64-row block, so each SM ingests and multiplies
-        // half of the block matrices.  Block k's half of Dinv/F1/F2
-        // (3 x 16 KB) arrives by TMA one block ahead (two stages, one mbarrier
-        // each), in the thread-major layout written by the planner: thread t
-        // owns local row t/8 and columns (t%8)*8..+7 (conflict-free reads,
-        // 3-step shuffle reduction).  A block's x values are pushed into both
-        // CTAs' rings (local + DSMEM store) and the pair meets at one cluster
-        // barrier per block.  Metadata, row ids and epilogue operands are
-        // loaded one or two blocks ahead, and F2 x_{k-2}, F1 x_{k-1} are formed
-        // before the wait for s.
+        // 32c..32c+31 of every 64-row block.  Warp-specialised:
+        // * warp 8 (producer) walks the blocks up to kChainStages ahead: it
+        //   issues the TMA bulk copy of the block's half of Dinv/F1/F2
+        //   (planner record, thread-major layout: thread t owns local row t/8,
+        //   columns (t%8)*8..+7), polls the block's s values published by the
+        //   workers, stages s, the row ids and the epilogue operands in shared
+        //   memory and arrives on the stage's FULL barrier;
+        // * warps 0-7 (compute) per block: pre = Dinv s - F2 x_{k-2} (nothing
+        //   here waits on the chain itself), then the peer's half of x_{k-1}
+        //   (st.async + mbarrier), c = pre - F1 x_{k-1}, publication of x_k
+        //   (own ring, the peer's ring, global solution), and an EMPTY arrive
+        //   that hands the stage back to the producer.
+        // The loop-carried path is one 8-FMA gemv, the DSMEM hand-off and a
+        // 256-thread named barrier.
         constexpr int kXs = 72;   // padded x slot: column c at c + c/8
         constexpr int kHalf = kBlk * kBlk / 2;
-        extern __shared__ __align__(128) double smat[];  // [2 stages][3][kHalf]
+        constexpr int kS = kChainStages;
+        constexpr unsigned kMatBytes = 3u * kHalf * sizeof(double);
+        extern __shared__ __align__(128) double smat[];  // [kS stages][3][kHalf]
         __shared__ double xr[3 * kXs];                   // x of the last 3 blocks (both halves)
-        __shared__ double sw[8 * kXs];                   // each warp's copy of the block's s
-        __shared__ __align__(8) unsigned long long mbar[kChainStages];
-        __shared__ __align__(8) unsigned long long xbar[2];  // peer's half of x_k landed (st.async)
+        __shared__ double sst[kS][kXs];                  // staged s (padded layout)
+        __shared__ int2 rqst[kS][32];                    // staged (row id, output position) of own rows
+        __shared__ int4 mst[kS][2];                      // staged block descriptor (B, O)
+        __shared__ __align__(8) unsigned long long full_b[kS], empty_b[kS], xbar[2];
         const int cr = blockIdx.x;  // rank in the pair
-        const int tid = threadIdx.x, rl = tid >> 3, oc = tid & 7;
-        const int row = 32 * cr + rl;  // row of the block owned by this thread group
-        const unsigned mb0 = (unsigned)__cvta_generic_to_shared(&mbar[0]);
+        const int tid = threadIdx.x;
+        const unsigned fb0 = (unsigned)__cvta_generic_to_shared(&full_b[0]);
+        const unsigned eb0 = (unsigned)__cvta_generic_to_shared(&empty_b[0]);
         const unsigned xb0 = (unsigned)__cvta_generic_to_shared(&xbar[0]);
         if (tid == 0) {
-            for (int q = 0; q < kChainStages; ++q)
-                asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(mb0 + 8 * q));
+            for (int q = 0; q < kS; ++q) {
+                asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(fb0 + 8 * q));
+                asm volatile("mbarrier.init.shared.b64 [%0], 8;" ::"r"(eb0 + 8 * q));
+            }
             asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(xb0));
             asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(xb0 + 8));
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
         for (int i = tid; i < 3 * kXs; i += blockDim.x) xr[i] = 0.0;
-        // the peer's ring and x-arrival barriers (DSMEM addresses in the other CTA)
-        unsigned xr_peer, xb_peer;
+        unsigned xr_peer, xb_peer;  // the peer's ring and x-arrival barriers (DSMEM)
         {
             const unsigned xl = (unsigned)__cvta_generic_to_shared(xr);
             asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(xr_peer) : "r"(xl), "r"(cr ^ 1));
             asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(xb_peer) : "r"(xb0), "r"(cr ^ 1));
         }
-        // block k's peer half: 32 values of 8 B, announced one block ahead
+        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+        asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+        auto mb_wait = [](unsigned mb, unsigned par) {
+            unsigned done = 0;
+            while (!done) {
+                asm volatile(
+                    "{ .reg .pred p; mbarrier.try_wait.parity.shared.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                    : "=r"(done) : "r"(mb), "r"(par) : "memory");
+            }
+        };
+        const int nbk = a.n_blocks;
+        if (nbk == 0) return;
+        if (warp == 8) {
+            // ---------------- producer ----------------
+            // software-pipelined: block k+2's descriptor and block k+1's row
+            // ids are loaded while block k's s is polled, so the only wait per
+            // block is the s values themselves
+            unsigned long long pol;
+            asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+            int4 B0 = a.blocks[0], O0 = a.blocks[1];
+            int4 B1 = nbk > 1 ? a.blocks[3] : make_int4(0, 0, 0, 0);
+            int4 O1 = nbk > 1 ? a.blocks[4] : make_int4(-1, -1, -1, 0);
+            int2 rq0 = (32 * cr + lane < B0.y) ? a.rq[B0.x + 32 * cr + lane] : make_int2(0, 0);
+            for (int kb = 0; kb < nbk; ++kb) {
+                const int st = kb % kS;
+                if (kb >= kS) mb_wait(eb0 + 8 * st, (unsigned)(((kb / kS) - 1) & 1));
+                if (lane == 0) {
+                    const unsigned dst = (unsigned)__cvta_generic_to_shared(smat + st * 3 * kHalf);
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(dst),
+                        "l"(a.pool + O0.w + cr * 3 * kHalf), "r"(kMatBytes), "r"(fb0 + 8 * st), "l"(pol)
+                        : "memory");
+                }
+                // ahead: descriptor of block k+2, row ids of block k+1
+                const int4 B2 = kb + 2 < nbk ? a.blocks[3 * (kb + 2)] : make_int4(0, 0, 0, 0);
+                const int4 O2 = kb + 2 < nbk ? a.blocks[3 * (kb + 2) + 1] : make_int4(-1, -1, -1, 0);
+                const int2 rq1 = (kb + 1 < nbk && 32 * cr + lane < B1.y) ? a.rq[B1.x + 32 * cr + lane]
+                                                                         : make_int2(0, 0);
+                // s of block k (published by the workers)
+                const int nb = B0.y;
+                const double* sp = a.s + B0.x;
+                double s0 = lane < nb ? __longlong_as_double(ld_relaxed(sp + lane)) : 0.0;
+                double s1 = lane + 32 < nb ? __longlong_as_double(ld_relaxed(sp + lane + 32)) : 0.0;
+                bool rd = __double_as_longlong(s0) != (long long)kSentinel &&
+                          __double_as_longlong(s1) != (long long)kSentinel;
+                while (!__all_sync(FULL, rd)) {
+                    if (lane < nb && __double_as_longlong(s0) == (long long)kSentinel)
+                        s0 = __longlong_as_double(ld_relaxed(sp + lane));
+                    if (lane + 32 < nb && __double_as_longlong(s1) == (long long)kSentinel)
+                        s1 = __longlong_as_double(ld_relaxed(sp + lane + 32));
+                    rd = __double_as_longlong(s0) != (long long)kSentinel &&
+                         __double_as_longlong(s1) != (long long)kSentinel;
+                }
+                sst[st][lane + (lane >> 3)] = s0;
+                sst[st][lane + 32 + ((lane + 32) >> 3)] = s1;
+                rqst[st][lane] = rq0;
+                if (lane == 0) {
+                    mst[st][0] = B0;
+                    mst[st][1] = O0;
+                }
+                __syncwarp();
+                if (lane == 0)  // release the staged values with the TMA's byte count
+                    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(fb0 + 8 * st),
+                                 "r"(kMatBytes) : "memory");
+                B0 = B1;
+                O0 = O1;
+                B1 = B2;
+                O1 = O2;
+                rq0 = rq1;
+            }
+            // the peer's last st.async must land before this CTA may exit
+            asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+            asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+            return;
+        }
+        // ---------------- compute warps 0-7 ----------------
+        const int rl = tid >> 3, oc = tid & 7;
+        const int row = 32 * cr + rl;  // row of the block owned by this thread group
         auto expect_x = [&](int kb) {
             asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(xb0 + 8 * (kb & 1)),
                          "r"(32u * 8u) : "memory");
@@ -1063,126 +1149,25 @@ __global__ void __launch_bounds__(256, EXG_CHAIN_MINB)
                     : "=r"(done) : "r"(mb), "r"(par) : "memory");
             }
         };
-        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-        asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-        // the chain's matrices are re-read by every solve: keep them in L2
-        // (evict_last) while the factors stream past them
-        unsigned long long pol;
-        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-        auto issue = [&](int kb, int4 O) {  // thread 0 of each CTA: its half, one bulk copy
-            const int st = kb % kChainStages;
-            const unsigned mb = mb0 + 8 * st;
-            constexpr unsigned bytes = 3u * kHalf * sizeof(double);
-            asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
-            const unsigned dst = (unsigned)__cvta_generic_to_shared(smat + st * 3 * kHalf);
-            asm volatile(
-                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(dst),
-                "l"(a.pool + O.w + cr * 3 * kHalf), "r"(bytes), "r"(mb), "l"(pol)
-                : "memory");
-        };
-        auto wait_stage = [&](int kb) {
-            const unsigned mb = mb0 + 8 * (kb % kChainStages);
-            const unsigned par = (unsigned)((kb / kChainStages) & 1);
-            unsigned done = 0;
-            while (!done) {
-                asm volatile(
-                    "{ .reg .pred p; mbarrier.try_wait.parity.shared.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                    : "=r"(done) : "r"(mb), "r"(par) : "memory");
-            }
-        };
-        const int nbk = a.n_blocks;
-        if (nbk == 0) return;
-        // block metadata ring in shared memory (block j in slot j % 3): the
-        // copy of block j+2 is loaded by the last thread during block j and
-        // stored just before the block's barrier, so no thread ever stalls on
-        // a metadata load (a register->uniform move of a pending load would)
-        constexpr int kAhead = kChainStages - 1;  // TMA prefetch distance (blocks)
-        constexpr int kMeta = kAhead + 2;          // metadata ring slots
-        __shared__ int4 meta_s[kMeta][2];
-        if (tid < kMeta - 1) {
-            meta_s[tid][0] = tid < nbk ? a.blocks[3 * tid] : make_int4(0, 0, 0, 0);
-            meta_s[tid][1] = tid < nbk ? a.blocks[3 * tid + 1] : make_int4(-1, -1, -1, 0);
-        }
-        __syncthreads();
-        int4 Bc = meta_s[0][0], Oc = meta_s[0][1];
         if (tid == 0) {
-            for (int q = 0; q < kAhead && q < nbk; ++q) issue(q, meta_s[q][1]);
             expect_x(0);
+            if (nbk > 1) expect_x(1);
         }
-        int2 rq = (oc == 0 && row < Bc.y) ? a.rq[Bc.x + row] : make_int2(0, 0);
-        double* swp = sw + warp * kXs;
         for (int kb = 0; kb < nbk; ++kb) {
-            Bc = meta_s[kb % kMeta][0];
-            Oc = meta_s[kb % kMeta][1];
-            const int4 B1 = meta_s[(kb + 1) % kMeta][0];
-            const int nb = Bc.y;
-            // ---- blocks ahead (consumed in later iterations: no stall)
-            if (tid == 0 && kb + kAhead < nbk) issue(kb + kAhead, meta_s[(kb + kAhead) % kMeta][1]);
-            int4 B2 = make_int4(0, 0, 0, 0), O2 = make_int4(-1, -1, -1, 0);
-            if (tid == blockDim.x - 1 && kb + kAhead + 1 < nbk) {
-                B2 = a.blocks[3 * (kb + kAhead + 1)];
-                O2 = a.blocks[3 * (kb + kAhead + 1) + 1];
-            }
-            const int2 rqn = (oc == 0 && kb + 1 < nbk && row < B1.y) ? a.rq[B1.x + row] : make_int2(0, 0);
-            const double ad = (a.final_out && a.add && oc == 0 && row < nb) ? a.add[rq.y] : 0.0;
-            // this block's s: loaded now (the workers published it about a
-            // block ago), consumed after the F gemvs, which hide the round trip
-            double s0 = lane < nb ? __longlong_as_double(ld_relaxed(a.s + Bc.x + lane)) : 0.0;
-            double s1 = lane + 32 < nb ? __longlong_as_double(ld_relaxed(a.s + Bc.x + lane + 32)) : 0.0;
-            // ---- F2 x_{k-2} and F1 x_{k-1}
-            wait_stage(kb);
+            const int st = kb % kS;
+            mb_wait(fb0 + 8 * st, (unsigned)((kb / kS) & 1));
             unsigned long long t_w = 0;
             if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_w));
-            const double* Ms = smat + (kb % kChainStages) * 3 * kHalf;
-            double p2 = 0.0, p1 = 0.0;
-            if (Oc.z >= 0) {
-                const double* xg = xr + ((kb - 2) % 3) * kXs + oc * 9;
-                const double* M = Ms + 2 * kHalf + tid;
-#pragma unroll
-                for (int j = 0; j < 8; ++j) p2 += M[j * 256] * xg[j];
-                p2 += __shfl_xor_sync(FULL, p2, 1);
-                p2 += __shfl_xor_sync(FULL, p2, 2);
-                p2 += __shfl_xor_sync(FULL, p2, 4);
-            }
-            // the peer's half of x_{k-1} (x_{k-2} was waited for last block);
-            // the barrier just completed is re-armed for block k+1 (the peer
-            // cannot send block k+1 before it has our x_k)
-            if (kb >= 1) wait_x(kb - 1);
-            if (tid == 0 && kb + 1 < nbk) expect_x(kb + 1);
-            if (Oc.y >= 0) {
-                const double* xg = xr + ((kb - 1) % 3) * kXs + oc * 9;
-                const double* M = Ms + kHalf + tid;
-#pragma unroll
-                for (int j = 0; j < 8; ++j) p1 += M[j * 256] * xg[j];
-                p1 += __shfl_xor_sync(FULL, p1, 1);
-                p1 += __shfl_xor_sync(FULL, p1, 2);
-                p1 += __shfl_xor_sync(FULL, p1, 4);
-            }
-            unsigned long long t_m = 0;
-            if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_m));
-            // ---- s of this block (published by the workers; each warp polls)
-            {
-                const double* sp = a.s + Bc.x;
-                bool rd = __double_as_longlong(s0) != (long long)kSentinel &&
-                          __double_as_longlong(s1) != (long long)kSentinel;
-                while (!__all_sync(FULL, rd)) {
-                    if (lane < nb && __double_as_longlong(s0) == (long long)kSentinel)
-                        s0 = __longlong_as_double(ld_relaxed(sp + lane));
-                    if (lane + 32 < nb && __double_as_longlong(s1) == (long long)kSentinel)
-                        s1 = __longlong_as_double(ld_relaxed(sp + lane + 32));
-                    rd = __double_as_longlong(s0) != (long long)kSentinel &&
-                         __double_as_longlong(s1) != (long long)kSentinel;
-                }
-            }
-            unsigned long long t_s = 0;
-            if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_s));
-            swp[lane + (lane >> 3)] = s0;
-            swp[lane + 32 + ((lane + 32) >> 3)] = s1;
-            __syncwarp();
+            const int4 Bc = mst[st][0], Oc = mst[st][1];
+            const int nb = Bc.y;
+            const double* Ms = smat + st * 3 * kHalf;
+            // epilogue operand: issued now, consumed at the publication
+            const double ad = (oc == 0 && row < nb && a.final_out && a.add) ? a.add[rqst[st][rl].y] : 0.0;
+            // pre = Dinv s - F2 x_{k-2}
             double cx;
             if (Oc.x >= 0) {
                 const double* M = Ms + tid;
-                const double* sg = swp + oc * 9;
+                const double* sg = sst[st] + oc * 9;
                 cx = 0.0;
 #pragma unroll
                 for (int j = 0; j < 8; ++j) cx += M[j * 256] * sg[j];
@@ -1190,13 +1175,43 @@ __global__ void __launch_bounds__(256, EXG_CHAIN_MINB)
                 cx += __shfl_xor_sync(FULL, cx, 2);
                 cx += __shfl_xor_sync(FULL, cx, 4);
             } else {
-                cx = row < nb ? swp[row + (row >> 3)] : 0.0;
+                cx = row < nb ? sst[st][row + (row >> 3)] : 0.0;
             }
-            if (Oc.z >= 0) cx = cx - p2;
-            if (Oc.y >= 0) cx = cx - p1;
-            // ---- publish x_k: own ring, the peer's ring (st.async completing
-            // on the peer's x barrier: no cluster-wide barrier, no release of
-            // the global stores on the hand-off path), global solution
+            if (Oc.z >= 0) {
+                const double* xg = xr + ((kb + 1) % 3) * kXs + oc * 9;  // slot of block k-2
+                const double* M = Ms + 2 * kHalf + tid;
+                double p2 = 0.0;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) p2 += M[j * 256] * xg[j];
+                p2 += __shfl_xor_sync(FULL, p2, 1);
+                p2 += __shfl_xor_sync(FULL, p2, 2);
+                p2 += __shfl_xor_sync(FULL, p2, 4);
+                cx = cx - p2;
+            }
+            unsigned long long t_m = 0;
+            if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_m));
+            // x_{k-1}: own half (named barrier over the compute warps) and the
+            // peer's half (DSMEM); re-arm that x barrier for block k+1
+            asm volatile("bar.sync 1, 256;" ::: "memory");
+            if (kb >= 1) {
+                wait_x(kb - 1);
+                if (tid == 0 && kb + 1 < nbk) expect_x(kb + 1);
+            }
+            unsigned long long t_s = 0;
+            if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_s));
+            if (Oc.y >= 0) {
+                const double* xg = xr + ((kb + 2) % 3) * kXs + oc * 9;  // slot of block k-1
+                const double* M = Ms + kHalf + tid;
+                double p1 = 0.0;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) p1 += M[j * 256] * xg[j];
+                p1 += __shfl_xor_sync(FULL, p1, 1);
+                p1 += __shfl_xor_sync(FULL, p1, 2);
+                p1 += __shfl_xor_sync(FULL, p1, 4);
+                cx = cx - p1;
+            }
+            // publish x_k: own ring, the peer's ring (st.async completing on
+            // the peer's x barrier), global solution, epilogue
             if (oc == 0) {
                 const double xv = row < nb ? cx : 0.0;
                 const int xi = (kb % 3) * kXs + row + (row >> 3);
@@ -1205,18 +1220,18 @@ __global__ void __launch_bounds__(256, EXG_CHAIN_MINB)
                                  xr_peer + 8u * (unsigned)xi),
                              "l"(__double_as_longlong(xv)), "r"(xb_peer + 8u * (unsigned)(kb & 1))
                              : "memory");
-                if (row < nb) st_relaxed(a.out + rq.x, cx);
+                if (row < nb) {
+                    const int2 rq = rqst[st][rl];
+                    st_relaxed(a.out + rq.x, cx);
+                    if (a.final_out) {
+                        double yo = a.coef * cx;
+                        if (a.add) yo = ad + yo;
+                        a.final_out[rq.y] = yo;
+                    }
+                }
             }
-            if (tid == blockDim.x - 1) {
-                meta_s[(kb + kAhead + 1) % kMeta][0] = B2;
-                meta_s[(kb + kAhead + 1) % kMeta][1] = O2;
-            }
-            __syncthreads();
-            if (oc == 0 && row < nb && a.final_out) {
-                double yo = a.coef * cx;
-                if (a.add) yo = ad + yo;
-                a.final_out[rq.y] = yo;
-            }
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(eb0 + 8 * st) : "memory");
             if (a.trace && tid == 0 && cr == 0) {
                 unsigned long long t_e;
                 asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_e));
@@ -1225,7 +1240,6 @@ __global__ void __launch_bounds__(256, EXG_CHAIN_MINB)
                 a.trace[4 * kb + 2] = t_s;
                 a.trace[4 * kb + 3] = t_e;
             }
-            rq = rqn;
         }
         // the peer's last st.async must land before this CTA may exit
         wait_x(nbk - 1);
@@ -2575,19 +2589,19 @@ void trsv_chain(const Launch& L, bool upper, const ChainArgs& a) {
     auto fn = upper ? (void*)k_trsv_chain<true> : (void*)k_trsv_chain<false>;
     if (!attr[upper]) {
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kChainSmem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[upper], upper ? k_trsv_chain<true> : k_trsv_chain<false>, 256,
-                                                      kChainSmem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[upper], upper ? k_trsv_chain<true> : k_trsv_chain<false>,
+                                                      kChainThreads, kChainSmem);
         if (occ[upper] < 1) occ[upper] = 1;
         attr[upper] = true;
     }
     // even grid (clusters of 2: CTAs 0-1 = the chain pair, the rest workers);
     // cooperative so every worker is resident while the chain waits on them
     long long g = std::max<long long>(4, std::min<long long>((long long)L.num_sms * occ[upper],
-                                                             2 + ((long long)a.n_rows + 7) / 8));
+                                                             2 + ((long long)a.n_rows + 8) / 9));
     g &= ~1LL;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)g);
-    cfg.blockDim = dim3(256);
+    cfg.blockDim = dim3(kChainThreads);
     cfg.dynamicSmemBytes = kChainSmem;
     cfg.stream = L.stream;
     cudaLaunchAttribute at[2];

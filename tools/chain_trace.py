@@ -44,12 +44,12 @@ for name, arr in (("L", nt[:3 * n]), ("U", nt[3 * n:])):
     if nb == 0:
         continue
     tr = arr[:4 * nb].reshape(nb, 4)
-    tw, tm, ts, te = tr[:, 0], tr[:, 1], tr[:, 2], tr[:, 3]  # matrices in, F1/F2 done, s ready, published
+    tw, tm, ts, te = tr[:, 0], tr[:, 1], tr[:, 2], tr[:, 3]  # stage full, pre done, x_{k-1} in, published
     prev_e = np.concatenate([[tw[0]], te[:-1]])
     span = (te[-1] - tw[0]) / 1e3
     med = lambda v: float(np.median(v))  # noqa: E731
-    print(f"{name}: chain blocks {nb}, span {span:.1f} us; per block median ns: wait matrices {med(tw - prev_e):.0f}, "
-          f"F1/F2 gemvs {med(tm - tw):.0f}, wait s {med(ts - tm):.0f}, Dinv s + publish {med(te - ts):.0f}; "
+    print(f"{name}: chain blocks {nb}, span {span:.1f} us; per block median ns: wait stage {med(tw - prev_e):.0f}, "
+          f"Dinv s - F2 x {med(tm - tw):.0f}, wait x(k-1) {med(ts - tm):.0f}, F1 gemv + publish {med(te - ts):.0f}; "
           f"total {med(te - prev_e):.0f}")
     rows = nb * 64
     w = arr[4 * nb: 4 * nb + 3 * rows].reshape(rows, 3)
@@ -64,6 +64,6 @@ for name, arr in (("L", nt[:3 * n]), ("U", nt[3 * n:])):
         lat["start"].append(np.median(w[sel, 0] - dep))
         lat["ready"].append(np.median(w[sel, 1] - dep))
         lat["pub"].append(np.max(w[sel, 2] - dep))
-        lat["chain"].append(ts[k] - dep)
+        lat["chain"].append(tw[k] - dep)
     print(f"   workers vs publication of block k-3 (ns): task start {med(lat['start']):.0f}, entries ready "
-          f"{med(lat['ready']):.0f}, last s published {med(lat['pub']):.0f}, chain has all s {med(lat['chain']):.0f}")
+          f"{med(lat['ready']):.0f}, last s published {med(lat['pub']):.0f}, chain stage full {med(lat['chain']):.0f}")

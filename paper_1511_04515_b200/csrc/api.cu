@@ -533,7 +533,7 @@ void plan_triangle(exg_ctx* c, TriPlan& P, bool upper_tri, const std::vector<int
     int slot_total = 0;
     std::vector<int4> ctasks;
     const char* ko = getenv("EXG_CHAIN_OLD");
-    const int kOld = ko ? atoi(ko) : 8;
+    const int kOld = ko ? atoi(ko) : 6;  // recent window k-6..k-3: <= 256 entries, one prefetched batch
     std::vector<ChainRun> cruns;
     std::vector<int> crows, cnptr, cncol;
     std::vector<int4> cblocks;

@@ -1035,15 +1035,17 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
         __shared__ double sst[kS][kXs];                  // staged s (padded layout)
         __shared__ int2 rqst[kS][32];                    // staged (row id, output position) of own rows
         __shared__ int4 mst[kS][2];                      // staged block descriptor (B, O)
-        __shared__ __align__(8) unsigned long long full_b[kS], empty_b[kS], xbar[2];
+        __shared__ __align__(8) unsigned long long full_b[kS], sful_b[kS], empty_b[kS], xbar[2];
         const int cr = blockIdx.x;  // rank in the pair
         const int tid = threadIdx.x;
-        const unsigned fb0 = (unsigned)__cvta_generic_to_shared(&full_b[0]);
+        const unsigned fb0 = (unsigned)__cvta_generic_to_shared(&full_b[0]);  // matrices + descriptor
+        const unsigned sb0 = (unsigned)__cvta_generic_to_shared(&sful_b[0]);  // s + row ids
         const unsigned eb0 = (unsigned)__cvta_generic_to_shared(&empty_b[0]);
         const unsigned xb0 = (unsigned)__cvta_generic_to_shared(&xbar[0]);
         if (tid == 0) {
             for (int q = 0; q < kS; ++q) {
                 asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(fb0 + 8 * q));
+                asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(sb0 + 8 * q));
                 asm volatile("mbarrier.init.shared.b64 [%0], 8;" ::"r"(eb0 + 8 * q));
             }
             asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(xb0));
@@ -1090,6 +1092,14 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
                         "l"(a.pool + O0.w + cr * 3 * kHalf), "r"(kMatBytes), "r"(fb0 + 8 * st), "l"(pol)
                         : "memory");
                 }
+                // the descriptor goes out with the matrices (compute starts
+                // F2 x_{k-2} as soon as they land, before s is known)
+                if (lane == 0) {
+                    mst[st][0] = B0;
+                    mst[st][1] = O0;
+                    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(fb0 + 8 * st),
+                                 "r"(kMatBytes) : "memory");
+                }
                 // ahead: descriptor of block k+2, row ids of block k+1
                 const int4 B2 = kb + 2 < nbk ? a.blocks[3 * (kb + 2)] : make_int4(0, 0, 0, 0);
                 const int4 O2 = kb + 2 < nbk ? a.blocks[3 * (kb + 2) + 1] : make_int4(-1, -1, -1, 0);
@@ -1113,14 +1123,8 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
                 sst[st][lane + (lane >> 3)] = s0;
                 sst[st][lane + 32 + ((lane + 32) >> 3)] = s1;
                 rqst[st][lane] = rq0;
-                if (lane == 0) {
-                    mst[st][0] = B0;
-                    mst[st][1] = O0;
-                }
                 __syncwarp();
-                if (lane == 0)  // release the staged values with the TMA's byte count
-                    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(fb0 + 8 * st),
-                                 "r"(kMatBytes) : "memory");
+                if (lane == 0) asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(sb0 + 8 * st) : "memory");
                 B0 = B1;
                 O0 = O1;
                 B1 = B2;
@@ -1156,14 +1160,26 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
         for (int kb = 0; kb < nbk; ++kb) {
             const int st = kb % kS;
             mb_wait(fb0 + 8 * st, (unsigned)((kb / kS) & 1));
-            unsigned long long t_w = 0;
-            if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_w));
             const int4 Bc = mst[st][0], Oc = mst[st][1];
             const int nb = Bc.y;
             const double* Ms = smat + st * 3 * kHalf;
+            // F2 x_{k-2}: needs only the matrices
+            double p2 = 0.0;
+            if (Oc.z >= 0) {
+                const double* xg = xr + ((kb + 1) % 3) * kXs + oc * 9;  // slot of block k-2
+                const double* M = Ms + 2 * kHalf + tid;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) p2 += M[j * 256] * xg[j];
+                p2 += __shfl_xor_sync(FULL, p2, 1);
+                p2 += __shfl_xor_sync(FULL, p2, 2);
+                p2 += __shfl_xor_sync(FULL, p2, 4);
+            }
+            mb_wait(sb0 + 8 * st, (unsigned)((kb / kS) & 1));
+            unsigned long long t_w = 0;
+            if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_w));
             // epilogue operand: issued now, consumed at the publication
             const double ad = (oc == 0 && row < nb && a.final_out && a.add) ? a.add[rqst[st][rl].y] : 0.0;
-            // pre = Dinv s - F2 x_{k-2}
+            // Dinv s - F2 x_{k-2}
             double cx;
             if (Oc.x >= 0) {
                 const double* M = Ms + tid;
@@ -1177,17 +1193,7 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
             } else {
                 cx = row < nb ? sst[st][row + (row >> 3)] : 0.0;
             }
-            if (Oc.z >= 0) {
-                const double* xg = xr + ((kb + 1) % 3) * kXs + oc * 9;  // slot of block k-2
-                const double* M = Ms + 2 * kHalf + tid;
-                double p2 = 0.0;
-#pragma unroll
-                for (int j = 0; j < 8; ++j) p2 += M[j * 256] * xg[j];
-                p2 += __shfl_xor_sync(FULL, p2, 1);
-                p2 += __shfl_xor_sync(FULL, p2, 2);
-                p2 += __shfl_xor_sync(FULL, p2, 4);
-                cx = cx - p2;
-            }
+            if (Oc.z >= 0) cx = cx - p2;
             unsigned long long t_m = 0;
             if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_m));
             // x_{k-1}: own half (named barrier over the compute warps) and the

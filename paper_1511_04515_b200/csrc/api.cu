@@ -533,7 +533,7 @@ void plan_triangle(exg_ctx* c, TriPlan& P, bool upper_tri, const std::vector<int
     int slot_total = 0;
     std::vector<int4> ctasks;
     const char* ko = getenv("EXG_CHAIN_OLD");
-    const int kOld = ko ? atoi(ko) : 6;  // recent window k-6..k-3: <= 256 entries, one prefetched batch
+    const int kOld = ko ? std::max(atoi(ko), 4) : 7;  // recent window k-7..k-4: <= 256 entries, one prefetched batch
     std::vector<ChainRun> cruns;
     std::vector<int> crows, cnptr, cncol;
     std::vector<int4> cblocks;
@@ -543,7 +543,7 @@ void plan_triangle(exg_ctx* c, TriPlan& P, bool upper_tri, const std::vector<int
     std::vector<int> rows, nptr{0}, nmid, ncol;
     std::vector<double> nval, pool;
     constexpr int kB = 64;
-    std::vector<double> Dm(kB * kB), Em(kB * kB), E2(kB * kB), Di(kB * kB), Fm(kB * kB);
+    std::vector<double> Dm(kB * kB), Em(kB * kB), E2(kB * kB), E3(kB * kB), Di(kB * kB), Fm(kB * kB);
     auto diag_of = [&](int r) { return udiag ? (*udiag)[r] : 1.0; };
     // level classes, then absorb short wide stretches into the narrow runs
     // (a launch costs more than a few fat levels on the cluster)
@@ -587,13 +587,17 @@ void plan_triangle(exg_ctx* c, TriPlan& P, bool upper_tri, const std::vector<int
             for (int kb = 0; kb < nblk; ++kb) {
                 const int bs = p0 + kb * kB;
                 const int bc = std::min(kB, p0 + pc - bs);
+                // the chain itself handles blocks k-1..k-3 (F1..F3); the
+                // workers' "recent" tasks blocks k-kOld..k-4, chunks the rest
                 const int ps1 = kb >= 1 ? bs - kB : bs;
                 const int ps2 = kb >= 2 ? bs - 2 * kB : ps1;
+                const int ps3 = kb >= 3 ? bs - 3 * kB : ps2;
                 std::fill(Dm.begin(), Dm.end(), 0.0);
                 std::fill(Em.begin(), Em.end(), 0.0);
                 std::fill(E2.begin(), E2.end(), 0.0);
-                bool d_ident = true, e1_zero = true, e2_zero = true;
-                const int pso = kb >= kOld ? bs - kOld * kB : p0;  // first position of block k-8
+                std::fill(E3.begin(), E3.end(), 0.0);
+                bool d_ident = true, e1_zero = true, e2_zero = true, e3_zero = true;
+                const int pso = kb >= kOld ? bs - kOld * kB : p0;  // first position of block k-kOld
                 for (int i = 0; i < bc; ++i) {
                     const int p = bs + i;
                     const int r = ord[p];
@@ -607,8 +611,11 @@ void plan_triangle(exg_ctx* c, TriPlan& P, bool upper_tri, const std::vector<int
                         const int pq = pos_of[col[k]];
                         if (pq < pso) {
                             oldk.push_back({pq, k});
-                        } else if (pq < ps2) {
+                        } else if (pq < ps3) {
                             recv.push_back({col[k], val[k]});
+                        } else if (pq < ps2) {
+                            E3[i * kB + (pq - ps3)] = val[k];
+                            e3_zero = false;
                         } else if (pq < ps1) {
                             E2[i * kB + (pq - ps2)] = val[k];
                             e2_zero = false;
@@ -647,7 +654,7 @@ void plan_triangle(exg_ctx* c, TriPlan& P, bool upper_tri, const std::vector<int
                         cnval.push_back(e.second);
                     }
                     const int e2 = (int)cncol.size() - cr.ent0;
-                    wt.push_back({std::max(0, kb - 3), make_int4(pl, e1, e2, 1 | (nch << 8))});
+                    wt.push_back({std::max(0, kb - 4), make_int4(pl, e1, e2, 1 | (nch << 8))});
                     cnptr.push_back(e2);
                 }
                 std::fill(Di.begin(), Di.end(), 0.0);
@@ -657,20 +664,20 @@ void plan_triangle(exg_ctx* c, TriPlan& P, bool upper_tri, const std::vector<int
                         for (int m2 = jc; m2 < i; ++m2) sacc -= Dm[i * kB + m2] * Di[m2 * kB + jc];
                         Di[i * kB + jc] = sacc / Dm[i * kB + i];
                     }
-                // chain layout (k_trsv_chain): one record of 3 x 64 x 64 per
-                // block, [CTA 0 half: Dinv F1 F2][CTA 1 half: Dinv F1 F2], so
-                // each CTA of the chain pair fetches its 48 KB with ONE bulk
+                // chain layout (k_trsv_chain): one record of 4 x 64 x 64 per
+                // block, [CTA 0 half: Dinv F1 F2 F3][CTA 1 half: ...], so
+                // each CTA of the chain pair fetches its 64 KB with ONE bulk
                 // copy.  Half c holds rows 32c..32c+31; its thread t owns local
                 // row t/8, columns (t%8)*8 .. +7, element j at j*256 + t
                 // (conflict-free shared-memory reads).  Absent matrices are
                 // zeros and flagged -1 in the block descriptor.
                 const int rec = (int)pool.size();
-                pool.resize(pool.size() + 3 * kB * kB, 0.0);
+                pool.resize(pool.size() + 4 * kB * kB, 0.0);
                 auto put_mat = [&](const std::vector<double>& M, int q) {
                     for (int c2 = 0; c2 < 2; ++c2)
                         for (int j = 0; j < 8; ++j)
                             for (int t = 0; t < 256; ++t)
-                                pool[rec + c2 * 3 * 2048 + q * 2048 + j * 256 + t] =
+                                pool[rec + c2 * 4 * 2048 + q * 2048 + j * 256 + t] =
                                     M[(32 * c2 + (t >> 3)) * kB + (t & 7) * 8 + j];
                     return rec;
                 };
@@ -687,7 +694,8 @@ void plan_triangle(exg_ctx* c, TriPlan& P, bool upper_tri, const std::vector<int
                 const int dofs = d_ident ? -1 : put_mat(Di, 0);
                 const int f1 = e1_zero ? -1 : times_dinv(Em, 1);
                 const int f2 = e2_zero ? -1 : times_dinv(E2, 2);
-                cblocks.push_back(make_int4(kb * kB, bc, 0, 0));
+                const int f3 = e3_zero ? -1 : times_dinv(E3, 3);
+                cblocks.push_back(make_int4(kb * kB, bc, f3, 0));  // .z: F3 present (>= 0)
                 cblocks.push_back(make_int4(dofs, f1, f2, rec));  // .w: record offset
                 cblocks.push_back(make_int4(0, 0, 0, 0));
             }

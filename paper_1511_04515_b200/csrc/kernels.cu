@@ -805,7 +805,7 @@ __global__ void __launch_bounds__(EXG_NARROW_THREADS, 1)
 constexpr int kBlk = 64;
 constexpr int kChainStages = 3;  // TMA stages of the chain: block k+2 is in flight while k computes
 constexpr int kChainThreads = 288;  // chain CTAs: 8 compute warps + 1 producer warp; workers use all 9
-constexpr size_t kChainMats = kChainStages * 3 * (kBlk * kBlk / 2) * sizeof(double);  // half of (Dinv, F1, F2) per stage
+constexpr size_t kChainMats = kChainStages * 4 * (kBlk * kBlk / 2) * sizeof(double);  // half of (Dinv, F1, F2, F3) per stage
 // launched with more than half an SM's shared memory so that no worker CTA
 // shares an SM with a chain CTA (one CTA per SM)
 constexpr size_t kChainSmem = kChainMats > 120 * 1024 ? kChainMats : 120 * 1024;  // > half an SM: one CTA per SM
@@ -1029,9 +1029,9 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
         constexpr int kXs = 72;   // padded x slot: column c at c + c/8
         constexpr int kHalf = kBlk * kBlk / 2;
         constexpr int kS = kChainStages;
-        constexpr unsigned kMatBytes = 3u * kHalf * sizeof(double);
-        extern __shared__ __align__(128) double smat[];  // [kS stages][3][kHalf]
-        __shared__ double xr[3 * kXs];                   // x of the last 3 blocks (both halves)
+        constexpr unsigned kMatBytes = 4u * kHalf * sizeof(double);
+        extern __shared__ __align__(128) double smat[];  // [kS stages][4][kHalf]
+        __shared__ double xr[4 * kXs];                   // x of the last 4 blocks (both halves), slot k % 4
         __shared__ double sst[kS][kXs];                  // staged s (padded layout)
         __shared__ int2 rqst[kS][32];                    // staged (row id, output position) of own rows
         __shared__ int4 mst[kS][2];                      // staged block descriptor (B, O)
@@ -1052,7 +1052,7 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
             asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(xb0 + 8));
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
-        for (int i = tid; i < 3 * kXs; i += blockDim.x) xr[i] = 0.0;
+        for (int i = tid; i < 4 * kXs; i += blockDim.x) xr[i] = 0.0;
         unsigned xr_peer, xb_peer;  // the peer's ring and x-arrival barriers (DSMEM)
         {
             const unsigned xl = (unsigned)__cvta_generic_to_shared(xr);
@@ -1086,10 +1086,10 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
                 const int st = kb % kS;
                 if (kb >= kS) mb_wait(eb0 + 8 * st, (unsigned)(((kb / kS) - 1) & 1));
                 if (lane == 0) {
-                    const unsigned dst = (unsigned)__cvta_generic_to_shared(smat + st * 3 * kHalf);
+                    const unsigned dst = (unsigned)__cvta_generic_to_shared(smat + st * 4 * kHalf);
                     asm volatile(
                         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(dst),
-                        "l"(a.pool + O0.w + cr * 3 * kHalf), "r"(kMatBytes), "r"(fb0 + 8 * st), "l"(pol)
+                        "l"(a.pool + O0.w + cr * 4 * kHalf), "r"(kMatBytes), "r"(fb0 + 8 * st), "l"(pol)
                         : "memory");
                 }
                 // the descriptor goes out with the matrices (compute starts
@@ -1162,11 +1162,20 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
             mb_wait(fb0 + 8 * st, (unsigned)((kb / kS) & 1));
             const int4 Bc = mst[st][0], Oc = mst[st][1];
             const int nb = Bc.y;
-            const double* Ms = smat + st * 3 * kHalf;
-            // F2 x_{k-2}: needs only the matrices
-            double p2 = 0.0;
+            const double* Ms = smat + st * 4 * kHalf;
+            // F3 x_{k-3} + F2 x_{k-2}: need only the matrices
+            double p2 = 0.0, p3 = 0.0;
+            if (Bc.z >= 0) {
+                const double* xg = xr + ((kb + 1) % 4) * kXs + oc * 9;  // slot of block k-3
+                const double* M = Ms + 3 * kHalf + tid;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) p3 += M[j * 256] * xg[j];
+                p3 += __shfl_xor_sync(FULL, p3, 1);
+                p3 += __shfl_xor_sync(FULL, p3, 2);
+                p3 += __shfl_xor_sync(FULL, p3, 4);
+            }
             if (Oc.z >= 0) {
-                const double* xg = xr + ((kb + 1) % 3) * kXs + oc * 9;  // slot of block k-2
+                const double* xg = xr + ((kb + 2) % 4) * kXs + oc * 9;  // slot of block k-2
                 const double* M = Ms + 2 * kHalf + tid;
 #pragma unroll
                 for (int j = 0; j < 8; ++j) p2 += M[j * 256] * xg[j];
@@ -1193,6 +1202,7 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
             } else {
                 cx = row < nb ? sst[st][row + (row >> 3)] : 0.0;
             }
+            if (Bc.z >= 0) cx = cx - p3;
             if (Oc.z >= 0) cx = cx - p2;
             unsigned long long t_m = 0;
             if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_m));
@@ -1206,7 +1216,7 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
             unsigned long long t_s = 0;
             if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_s));
             if (Oc.y >= 0) {
-                const double* xg = xr + ((kb + 2) % 3) * kXs + oc * 9;  // slot of block k-1
+                const double* xg = xr + ((kb + 3) % 4) * kXs + oc * 9;  // slot of block k-1
                 const double* M = Ms + kHalf + tid;
                 double p1 = 0.0;
 #pragma unroll
@@ -1220,7 +1230,7 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
             // the peer's x barrier), global solution, epilogue
             if (oc == 0) {
                 const double xv = row < nb ? cx : 0.0;
-                const int xi = (kb % 3) * kXs + row + (row >> 3);
+                const int xi = (kb % 4) * kXs + row + (row >> 3);
                 xr[xi] = xv;
                 asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(
                                  xr_peer + 8u * (unsigned)xi),

@@ -538,7 +538,7 @@ __global__ void __launch_bounds__(256)
             }
             warp_wait_ready<4>(a.out, cc0, kk, k1, y);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) acc += v0[q] * y[q];
+            for (int q = 0; q < 4; ++q) acc = __fma_rn(v0[q], y[q], acc);
         }
         if (lng) {
             const int nch = (k1 - k0 + 31) >> 5;
@@ -559,7 +559,7 @@ __global__ void __launch_bounds__(256)
                 for (int q = 0; q < 4; ++q) y[q] = kk[q] < k1 ? __ldca(a.out + cc[q]) : 0.0;
                 warp_wait_ready<4>(a.out, cc, kk, k1, y);
 #pragma unroll
-                for (int q = 0; q < 4; ++q) acc += v[q] * y[q];
+                for (int q = 0; q < 4; ++q) acc = __fma_rn(v[q], y[q], acc);
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
@@ -599,7 +599,7 @@ __global__ void __launch_bounds__(256)
                 for (int q = 0; q < 4; ++q) y[q] = kk[q] < k1 ? __ldca(a.out + cc[q]) : 0.0;
                 warp_wait_ready<4>(a.out, cc, kk, k1, y);
 #pragma unroll
-                for (int q = 0; q < 4; ++q) acc += v[q] * y[q];
+                for (int q = 0; q < 4; ++q) acc = __fma_rn(v[q], y[q], acc);
             }
             for (int o = lpr >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
             if (active && sl == 0) {
@@ -1163,47 +1163,37 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
             const int4 Bc = mst[st][0], Oc = mst[st][1];
             const int nb = Bc.y;
             const double* Ms = smat + st * 4 * kHalf;
-            // F3 x_{k-3} + F2 x_{k-2}: need only the matrices
-            double p2 = 0.0, p3 = 0.0;
+            // Each thread accumulates its 8-column slice of
+            //   Dinv s - F3 x_{k-3} - F2 x_{k-2} - F1 x_{k-1}
+            // with fused multiply-adds and ONE 3-step reduction at the end; F3
+            // and F2 need only the matrices, Dinv s the staged s, and only F1 +
+            // the reduction follow the arrival of x_{k-1}.
+            double q = 0.0;
             if (Bc.z >= 0) {
                 const double* xg = xr + ((kb + 1) % 4) * kXs + oc * 9;  // slot of block k-3
                 const double* M = Ms + 3 * kHalf + tid;
 #pragma unroll
-                for (int j = 0; j < 8; ++j) p3 += M[j * 256] * xg[j];
-                p3 += __shfl_xor_sync(FULL, p3, 1);
-                p3 += __shfl_xor_sync(FULL, p3, 2);
-                p3 += __shfl_xor_sync(FULL, p3, 4);
+                for (int j = 0; j < 8; ++j) q = __fma_rn(-M[j * 256], xg[j], q);
             }
             if (Oc.z >= 0) {
                 const double* xg = xr + ((kb + 2) % 4) * kXs + oc * 9;  // slot of block k-2
                 const double* M = Ms + 2 * kHalf + tid;
 #pragma unroll
-                for (int j = 0; j < 8; ++j) p2 += M[j * 256] * xg[j];
-                p2 += __shfl_xor_sync(FULL, p2, 1);
-                p2 += __shfl_xor_sync(FULL, p2, 2);
-                p2 += __shfl_xor_sync(FULL, p2, 4);
+                for (int j = 0; j < 8; ++j) q = __fma_rn(-M[j * 256], xg[j], q);
             }
             mb_wait(sb0 + 8 * st, (unsigned)((kb / kS) & 1));
             unsigned long long t_w = 0;
             if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_w));
             // epilogue operand: issued now, consumed at the publication
             const double ad = (oc == 0 && row < nb && a.final_out && a.add) ? a.add[rqst[st][rl].y] : 0.0;
-            // Dinv s - F2 x_{k-2}
-            double cx;
             if (Oc.x >= 0) {
                 const double* M = Ms + tid;
                 const double* sg = sst[st] + oc * 9;
-                cx = 0.0;
 #pragma unroll
-                for (int j = 0; j < 8; ++j) cx += M[j * 256] * sg[j];
-                cx += __shfl_xor_sync(FULL, cx, 1);
-                cx += __shfl_xor_sync(FULL, cx, 2);
-                cx += __shfl_xor_sync(FULL, cx, 4);
-            } else {
-                cx = row < nb ? sst[st][row + (row >> 3)] : 0.0;
+                for (int j = 0; j < 8; ++j) q = __fma_rn(M[j * 256], sg[j], q);
+            } else if (oc == (row & 63) >> 3 && row < nb) {
+                q += sst[st][row + (row >> 3)];  // identity Dinv: s_row
             }
-            if (Bc.z >= 0) cx = cx - p3;
-            if (Oc.z >= 0) cx = cx - p2;
             unsigned long long t_m = 0;
             if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_m));
             // x_{k-1}: own half (named barrier over the compute warps) and the
@@ -1218,14 +1208,13 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
             if (Oc.y >= 0) {
                 const double* xg = xr + ((kb + 3) % 4) * kXs + oc * 9;  // slot of block k-1
                 const double* M = Ms + kHalf + tid;
-                double p1 = 0.0;
 #pragma unroll
-                for (int j = 0; j < 8; ++j) p1 += M[j * 256] * xg[j];
-                p1 += __shfl_xor_sync(FULL, p1, 1);
-                p1 += __shfl_xor_sync(FULL, p1, 2);
-                p1 += __shfl_xor_sync(FULL, p1, 4);
-                cx = cx - p1;
+                for (int j = 0; j < 8; ++j) q = __fma_rn(-M[j * 256], xg[j], q);
             }
+            q += __shfl_xor_sync(FULL, q, 1);
+            q += __shfl_xor_sync(FULL, q, 2);
+            q += __shfl_xor_sync(FULL, q, 4);
+            const double cx = q;
             // publish x_k: own ring, the peer's ring (st.async completing on
             // the peer's x barrier), global solution, epilogue
             if (oc == 0) {
@@ -1326,7 +1315,7 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
             }
             warp_wait_ready<8>(a.out, cur.cc, kk, k1, y, a.spin_ns);
 #pragma unroll
-            for (int q = 0; q < 8; ++q) acc += cur.v[q] * y[q];
+            for (int q = 0; q < 8; ++q) acc = __fma_rn(cur.v[q], y[q], acc);
         }
         for (int base = k0 + 256; base < k1; base += 256) {  // long recent tasks only
             int kk[8], cc[8];
@@ -1341,7 +1330,7 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
             for (int q = 0; q < 8; ++q) y[q] = kk[q] < k1 ? __ldca(a.out + cc[q]) : 0.0;
             warp_wait_ready<8>(a.out, cc, kk, k1, y);
 #pragma unroll
-            for (int q = 0; q < 8; ++q) acc += v[q] * y[q];
+            for (int q = 0; q < 8; ++q) acc = __fma_rn(v[q], y[q], acc);
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
@@ -2628,7 +2617,11 @@ void trsv_chain(const Launch& L, bool upper, const ChainArgs& a) {
     at[1].id = cudaLaunchAttributeCooperative;
     at[1].val.cooperative = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 2;
+    // EXG_NO_COOP: plain cluster launch (ncu cannot replay a cooperative
+    // cluster launch); co-residency then rests on one CTA per SM and a grid
+    // of at most one CTA per SM, which the occupancy sizing above guarantees
+    static const bool no_coop = getenv("EXG_NO_COOP") != nullptr;
+    cfg.numAttrs = no_coop ? 1 : 2;
     if (upper)
         cudaLaunchKernelEx(&cfg, k_trsv_chain<true>, a);
     else

@@ -2,6 +2,7 @@
 # of the solve kernels and of the other hot-path kernels.  Run under gpurun
 # only after the same bench command exited 0 without ncu.
 export EXG_FACTOR_CACHE=/tmp/exg_fc
+export EXG_NO_COOP=1  # ncu cannot replay cooperative cluster launches
 mkdir -p gpurun_out
 B="python bench.py --steps 2 --warmup 3 --cpu-steps 0 --e2e-steps 1 --profile-steps 1"
 timeout 600 $B > gpurun_out/prof_bench.log 2>&1; echo rc=$? >> gpurun_out/prof_bench.log

@@ -275,6 +275,33 @@ __device__ __forceinline__ void warp_wait_ready(const double* out, const int* cc
     }
 }
 
+// warp_wait_ready plus one extra 64-bit value per lane (a chunk partial sum
+// of a chain worker's "recent" task) polled in the same rounds, so the
+// partials cost no extra round trip once the entries are ready
+template <int N>
+__device__ __forceinline__ void warp_wait_ready_p(const double* out, const int* cc, const int* kk,
+                                                  int k1, double* y, const double* paddr, bool pvalid,
+                                                  unsigned long long& pv) {
+    bool rd = !(pvalid && pv == kSentinel);
+#pragma unroll
+    for (int q = 0; q < N; ++q)
+        rd = rd && !(kk[q] < k1 && __double_as_longlong(y[q]) == (long long)kSentinel);
+    while (!__all_sync(0xffffffffu, rd)) {
+        rd = true;
+#pragma unroll
+        for (int q = 0; q < N; ++q) {
+            if (kk[q] < k1 && __double_as_longlong(y[q]) == (long long)kSentinel) {
+                y[q] = __longlong_as_double(ld_relaxed(out + cc[q]));
+                rd = rd && __double_as_longlong(y[q]) != (long long)kSentinel;
+            }
+        }
+        if (pvalid && pv == kSentinel) {
+            pv = ld_relaxed(paddr);
+            rd = rd && pv != kSentinel;
+        }
+    }
+}
+
 template <bool UPPER>
 __device__ __forceinline__ void trsv_finish(const TrsvArgs& a, int r, double s, const RowOps& o) {
     if (UPPER) s = s / o.dg;
@@ -1082,6 +1109,10 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
             int4 B1 = nbk > 1 ? a.blocks[3] : make_int4(0, 0, 0, 0);
             int4 O1 = nbk > 1 ? a.blocks[4] : make_int4(-1, -1, -1, 0);
             int2 rq0 = (32 * cr + lane < B0.y) ? a.rq[B0.x + 32 * cr + lane] : make_int2(0, 0);
+            // s polls run one block ahead: block k+1's first load is issued
+            // before block k is polled, so the round trips overlap
+            double sn0 = lane < B0.y ? __longlong_as_double(ld_relaxed(a.s + B0.x + lane)) : 0.0;
+            double sn1 = lane + 32 < B0.y ? __longlong_as_double(ld_relaxed(a.s + B0.x + lane + 32)) : 0.0;
             for (int kb = 0; kb < nbk; ++kb) {
                 const int st = kb % kS;
                 if (kb >= kS) mb_wait(eb0 + 8 * st, (unsigned)(((kb / kS) - 1) & 1));
@@ -1108,8 +1139,11 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
                 // s of block k (published by the workers)
                 const int nb = B0.y;
                 const double* sp = a.s + B0.x;
-                double s0 = lane < nb ? __longlong_as_double(ld_relaxed(sp + lane)) : 0.0;
-                double s1 = lane + 32 < nb ? __longlong_as_double(ld_relaxed(sp + lane + 32)) : 0.0;
+                double s0 = sn0, s1 = sn1;
+                if (kb + 1 < nbk) {
+                    sn0 = lane < B1.y ? __longlong_as_double(ld_relaxed(a.s + B1.x + lane)) : 0.0;
+                    sn1 = lane + 32 < B1.y ? __longlong_as_double(ld_relaxed(a.s + B1.x + lane + 32)) : 0.0;
+                }
                 bool rd = __double_as_longlong(s0) != (long long)kSentinel &&
                           __double_as_longlong(s1) != (long long)kSentinel;
                 while (!__all_sync(FULL, rd)) {
@@ -1305,6 +1339,7 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
         unsigned long long tr0 = 0, tr1 = 0;
         if (a.trace && recent) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr0));
         double acc = 0.0;
+        unsigned long long pv = cur.pv;
         {
             int kk[8];
             double y[8];
@@ -1313,7 +1348,11 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
                 kk[q] = cur.cc[q] >= 0 ? k0 : k1;  // "valid" marker for warp_wait_ready
                 y[q] = cur.cc[q] >= 0 ? __ldca(a.out + cur.cc[q]) : 0.0;
             }
-            warp_wait_ready<8>(a.out, cur.cc, kk, k1, y, a.spin_ns);
+            // a recent task's first 32 chunk partials are polled together
+            // with its entries
+            const bool pvalid = recent && lane < nch;
+            if (pvalid && pv == kSentinel) pv = ld_relaxed(a.part + cur.slot0 + lane);
+            warp_wait_ready_p<8>(a.out, cur.cc, kk, k1, y, a.part + cur.slot0 + lane, pvalid, pv);
 #pragma unroll
             for (int q = 0; q < 8; ++q) acc = __fma_rn(cur.v[q], y[q], acc);
         }
@@ -1340,7 +1379,6 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
         } else {
             // chunk partials, summed in chunk order (deterministic)
             double old = 0.0;
-            unsigned long long pv = cur.pv;
             for (int c0 = 0; c0 < nch; c0 += 32) {
                 const int ci = c0 + lane;
                 if (c0 > 0) pv = ci < nch ? ld_relaxed(a.part + cur.slot0 + ci) : 0ull;

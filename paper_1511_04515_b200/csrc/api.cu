@@ -235,7 +235,9 @@ void solve_dev(exg_ctx* c, const double* b, double* final_out, double coef, cons
                     ca.trace = upper ? c->ntrace_u : c->ntrace_l;
                     static const unsigned spin = getenv("EXG_CHAIN_SPIN") ? (unsigned)atoi(getenv("EXG_CHAIN_SPIN")) : 0u;
                     ca.spin_ns = spin;
-                    exg::dev::trsv_chain(c->L(), upper, ca);
+                    // a failed launch would leave the sentinels in place and
+                    // every later kernel waiting: fail loudly instead
+                    ck(exg::dev::trsv_chain(c->L(), upper, ca), "chain launch");
                     sbuf_dev += ch.n_rows;
                     continue;
                 }

@@ -129,7 +129,7 @@ void trsv(const Launch& L, bool upper, bool reverse, const TrsvArgs& a);
 void trsv_narrow(const Launch& L, bool upper, const NarrowArgs& a, int cluster, size_t smem);
 void trsv_wide(const Launch& L, bool upper, const TrsvArgs& a);
 void trsv_blk(const Launch& L, bool upper, const NarrowArgs& a, int cluster, size_t smem);
-void trsv_chain(const Launch& L, bool upper, const ChainArgs& a);
+cudaError_t trsv_chain(const Launch& L, bool upper, const ChainArgs& a);
 void apply_weight(const Launch& L, const int* uptr, const int* ucol, const double* uval,
                   const double* udiag, const int* lptr, const int* lcol, const double* lval, int n,
                   const int* col_perm, const int* row_perm, const double* x, double* t,

@@ -1036,23 +1036,23 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
     if (a.ctrl && (a.ctrl->converged || a.ctrl->status)) return;
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (blockIdx.x < 2) {
-        // ===================== chain pair =====================
-        // The chain is a 2-CTA cluster on two SMs: CTA c owns rows
-        // 32c..32c+31 of every 64-row block.  Warp-specialised:
-        // * warp 8 (producer) walks the blocks up to kChainStages ahead: it
-        //   issues the TMA bulk copy of the block's half of Dinv/F1/F2
-        //   (planner record, thread-major layout: thread t owns local row t/8,
-        //   columns (t%8)*8..+7), polls the block's s values published by the
-        //   workers, stages s, the row ids and the epilogue operands in shared
-        //   memory and arrives on the stage's FULL barrier;
-        // * warps 0-7 (compute) per block: pre = Dinv s - F2 x_{k-2} (nothing
-        //   here waits on the chain itself), then the peer's half of x_{k-1}
-        //   (st.async + mbarrier), c = pre - F1 x_{k-1}, publication of x_k
-        //   (own ring, the peer's ring, global solution), and an EMPTY arrive
-        //   that hands the stage back to the producer.
-        // The loop-carried path is one 8-FMA gemv, the DSMEM hand-off and a
-        // 256-thread named barrier.
+    if (blockIdx.x < 4) {
+        // ===================== chain: two pairs =====================
+        // The chain is a 4-CTA thread-block cluster on four SMs: pair p
+        // (CTAs 2p, 2p+1) takes the blocks k == p (mod 2), and CTA h of a pair
+        // owns rows 32h..32h+31 of each of them, so the per-block work that
+        // does not depend on x_{k-1} (F3 x_{k-3}, F2 x_{k-2}, Dinv s) of one
+        // pair overlaps the loop-carried F1 x_{k-1} + publication of the
+        // other.  Per CTA, warp-specialised:
+        // * warp 8 (producer) walks its pair's blocks up to kChainStages
+        //   ahead: TMA bulk copy of its half of the block record
+        //   (Dinv F1 F2 F3, thread-major layout: thread t owns local row t/8,
+        //   columns (t%8)*8..+7), the block's s values published by the
+        //   workers (polled one block ahead), row ids; FULL barriers;
+        // * warps 0-7 (compute): Dinv s - F3 x_{k-3} - F2 x_{k-2} - F1 x_{k-1}
+        //   with fused multiply-adds and one 3-step reduction; x_k's half is
+        //   pushed into the other three CTAs' rings with st.async completing
+        //   on their x barriers (block j lands on barrier j % 4).
         constexpr int kXs = 72;   // padded x slot: column c at c + c/8
         constexpr int kHalf = kBlk * kBlk / 2;
         constexpr int kS = kChainStages;
@@ -1062,8 +1062,9 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
         __shared__ double sst[kS][kXs];                  // staged s (padded layout)
         __shared__ int2 rqst[kS][32];                    // staged (row id, output position) of own rows
         __shared__ int4 mst[kS][2];                      // staged block descriptor (B, O)
-        __shared__ __align__(8) unsigned long long full_b[kS], sful_b[kS], empty_b[kS], xbar[2];
-        const int cr = blockIdx.x;  // rank in the pair
+        __shared__ __align__(8) unsigned long long full_b[kS], sful_b[kS], empty_b[kS], xbar[4];
+        const int cr = blockIdx.x;       // rank in the cluster
+        const int pr = cr >> 1, hf = cr & 1;
         const int tid = threadIdx.x;
         const unsigned fb0 = (unsigned)__cvta_generic_to_shared(&full_b[0]);  // matrices + descriptor
         const unsigned sb0 = (unsigned)__cvta_generic_to_shared(&sful_b[0]);  // s + row ids
@@ -1075,17 +1076,40 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
                 asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(sb0 + 8 * q));
                 asm volatile("mbarrier.init.shared.b64 [%0], 8;" ::"r"(eb0 + 8 * q));
             }
-            asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(xb0));
-            asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(xb0 + 8));
+            for (int q = 0; q < 4; ++q) asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(xb0 + 8 * q));
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
         for (int i = tid; i < 4 * kXs; i += blockDim.x) xr[i] = 0.0;
-        unsigned xr_peer, xb_peer;  // the peer's ring and x-arrival barriers (DSMEM)
+        unsigned xr_rem[3], xb_rem[3];  // the other three CTAs' rings and x barriers (DSMEM)
         {
             const unsigned xl = (unsigned)__cvta_generic_to_shared(xr);
-            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(xr_peer) : "r"(xl), "r"(cr ^ 1));
-            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(xb_peer) : "r"(xb0), "r"(cr ^ 1));
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                const int other = (cr + 1 + q) & 3;
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(xr_rem[q]) : "r"(xl), "r"(other));
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(xb_rem[q]) : "r"(xb0), "r"(other));
+            }
         }
+        const int nbk = a.n_blocks;
+        // bytes block j brings to this CTA: the mate's half (own pair) or
+        // both halves (other pair)
+        auto xbytes = [&](int j) { return (j & 1) == pr ? 32u * 8u : 64u * 8u; };
+        auto expect_x = [&](int j) {
+            asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(xb0 + 8 * (j & 3)),
+                         "r"(xbytes(j)) : "memory");
+        };
+        auto wait_x = [&](int j) {
+            const unsigned mb = xb0 + 8 * (j & 3);
+            const unsigned par = (unsigned)((j >> 2) & 1);
+            unsigned done = 0;
+            while (!done) {
+                asm volatile(
+                    "{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                    : "=r"(done) : "r"(mb), "r"(par) : "memory");
+            }
+        };
+        if (tid == 0)
+            for (int j = 0; j < 4 && j < nbk; ++j) expect_x(j);
         asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
         asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
         auto mb_wait = [](unsigned mb, unsigned par) {
@@ -1096,51 +1120,47 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
                     : "=r"(done) : "r"(mb), "r"(par) : "memory");
             }
         };
-        const int nbk = a.n_blocks;
-        if (nbk == 0) return;
+        const int nmine = nbk > pr ? (nbk - pr + 1) / 2 : 0;  // blocks of this pair
         if (warp == 8) {
             // ---------------- producer ----------------
-            // software-pipelined: block k+2's descriptor and block k+1's row
-            // ids are loaded while block k's s is polled, so the only wait per
-            // block is the s values themselves
             unsigned long long pol;
             asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-            int4 B0 = a.blocks[0], O0 = a.blocks[1];
-            int4 B1 = nbk > 1 ? a.blocks[3] : make_int4(0, 0, 0, 0);
-            int4 O1 = nbk > 1 ? a.blocks[4] : make_int4(-1, -1, -1, 0);
-            int2 rq0 = (32 * cr + lane < B0.y) ? a.rq[B0.x + 32 * cr + lane] : make_int2(0, 0);
-            // s polls run one block ahead: block k+1's first load is issued
-            // before block k is polled, so the round trips overlap
-            double sn0 = lane < B0.y ? __longlong_as_double(ld_relaxed(a.s + B0.x + lane)) : 0.0;
-            double sn1 = lane + 32 < B0.y ? __longlong_as_double(ld_relaxed(a.s + B0.x + lane + 32)) : 0.0;
-            for (int kb = 0; kb < nbk; ++kb) {
-                const int st = kb % kS;
-                if (kb >= kS) mb_wait(eb0 + 8 * st, (unsigned)(((kb / kS) - 1) & 1));
+            auto blk = [&](int u) { return pr + 2 * u; };
+            int4 B0 = make_int4(0, 0, 0, 0), O0 = make_int4(-1, -1, -1, 0);
+            int4 B1 = B0, O1 = O0;
+            if (nmine > 0) {
+                B0 = a.blocks[3 * blk(0)];
+                O0 = a.blocks[3 * blk(0) + 1];
+            }
+            if (nmine > 1) {
+                B1 = a.blocks[3 * blk(1)];
+                O1 = a.blocks[3 * blk(1) + 1];
+            }
+            int2 rq0 = (nmine > 0 && 32 * hf + lane < B0.y) ? a.rq[B0.x + 32 * hf + lane] : make_int2(0, 0);
+            double sn0 = (nmine > 0 && lane < B0.y) ? __longlong_as_double(ld_relaxed(a.s + B0.x + lane)) : 0.0;
+            double sn1 = (nmine > 0 && lane + 32 < B0.y) ? __longlong_as_double(ld_relaxed(a.s + B0.x + lane + 32)) : 0.0;
+            for (int u = 0; u < nmine; ++u) {
+                const int st = u % kS;
+                if (u >= kS) mb_wait(eb0 + 8 * st, (unsigned)(((u / kS) - 1) & 1));
                 if (lane == 0) {
                     const unsigned dst = (unsigned)__cvta_generic_to_shared(smat + st * 4 * kHalf);
                     asm volatile(
                         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(dst),
-                        "l"(a.pool + O0.w + cr * 4 * kHalf), "r"(kMatBytes), "r"(fb0 + 8 * st), "l"(pol)
+                        "l"(a.pool + O0.w + hf * 4 * kHalf), "r"(kMatBytes), "r"(fb0 + 8 * st), "l"(pol)
                         : "memory");
-                }
-                // the descriptor goes out with the matrices (compute starts
-                // F2 x_{k-2} as soon as they land, before s is known)
-                if (lane == 0) {
                     mst[st][0] = B0;
                     mst[st][1] = O0;
                     asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(fb0 + 8 * st),
                                  "r"(kMatBytes) : "memory");
                 }
-                // ahead: descriptor of block k+2, row ids of block k+1
-                const int4 B2 = kb + 2 < nbk ? a.blocks[3 * (kb + 2)] : make_int4(0, 0, 0, 0);
-                const int4 O2 = kb + 2 < nbk ? a.blocks[3 * (kb + 2) + 1] : make_int4(-1, -1, -1, 0);
-                const int2 rq1 = (kb + 1 < nbk && 32 * cr + lane < B1.y) ? a.rq[B1.x + 32 * cr + lane]
-                                                                         : make_int2(0, 0);
-                // s of block k (published by the workers)
+                const int4 B2 = u + 2 < nmine ? a.blocks[3 * blk(u + 2)] : make_int4(0, 0, 0, 0);
+                const int4 O2 = u + 2 < nmine ? a.blocks[3 * blk(u + 2) + 1] : make_int4(-1, -1, -1, 0);
+                const int2 rq1 = (u + 1 < nmine && 32 * hf + lane < B1.y) ? a.rq[B1.x + 32 * hf + lane]
+                                                                          : make_int2(0, 0);
                 const int nb = B0.y;
                 const double* sp = a.s + B0.x;
                 double s0 = sn0, s1 = sn1;
-                if (kb + 1 < nbk) {
+                if (u + 1 < nmine) {
                     sn0 = lane < B1.y ? __longlong_as_double(ld_relaxed(a.s + B1.x + lane)) : 0.0;
                     sn1 = lane + 32 < B1.y ? __longlong_as_double(ld_relaxed(a.s + B1.x + lane + 32)) : 0.0;
                 }
@@ -1165,49 +1185,33 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
                 O1 = O2;
                 rq0 = rq1;
             }
-            // the peer's last st.async must land before this CTA may exit
             asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
             asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
             return;
         }
         // ---------------- compute warps 0-7 ----------------
         const int rl = tid >> 3, oc = tid & 7;
-        const int row = 32 * cr + rl;  // row of the block owned by this thread group
-        auto expect_x = [&](int kb) {
-            asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(xb0 + 8 * (kb & 1)),
-                         "r"(32u * 8u) : "memory");
-        };
-        auto wait_x = [&](int kb) {
-            const unsigned mb = xb0 + 8 * (kb & 1);
-            const unsigned par = (unsigned)((kb >> 1) & 1);
-            unsigned done = 0;
-            while (!done) {
-                asm volatile(
-                    "{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                    : "=r"(done) : "r"(mb), "r"(par) : "memory");
-            }
-        };
-        if (tid == 0) {
-            expect_x(0);
-            if (nbk > 1) expect_x(1);
-        }
-        for (int kb = 0; kb < nbk; ++kb) {
-            const int st = kb % kS;
-            mb_wait(fb0 + 8 * st, (unsigned)((kb / kS) & 1));
+        const int row = 32 * hf + rl;  // row of the block owned by this thread group
+        for (int u = 0; u < nmine; ++u) {
+            const int kb = pr + 2 * u;
+            const int st = u % kS;
+            mb_wait(fb0 + 8 * st, (unsigned)((u / kS) & 1));
             const int4 Bc = mst[st][0], Oc = mst[st][1];
             const int nb = Bc.y;
             const double* Ms = smat + st * 4 * kHalf;
-            // Each thread accumulates its 8-column slice of
-            //   Dinv s - F3 x_{k-3} - F2 x_{k-2} - F1 x_{k-1}
-            // with fused multiply-adds and ONE 3-step reduction at the end; F3
-            // and F2 need only the matrices, Dinv s the staged s, and only F1 +
-            // the reduction follow the arrival of x_{k-1}.
             double q = 0.0;
+            // x_{k-3} (other pair) was waited for at the previous block
             if (Bc.z >= 0) {
                 const double* xg = xr + ((kb + 1) % 4) * kXs + oc * 9;  // slot of block k-3
                 const double* M = Ms + 3 * kHalf + tid;
 #pragma unroll
                 for (int j = 0; j < 8; ++j) q = __fma_rn(-M[j * 256], xg[j], q);
+            }
+            // x_{k-2} (own pair): own half from the block barrier at the end of
+            // the previous block, the mate's half by DSMEM; re-arm for k+2
+            if (kb >= 2) {
+                wait_x(kb - 2);
+                if (tid == 0 && kb + 2 < nbk) expect_x(kb + 2);
             }
             if (Oc.z >= 0) {
                 const double* xg = xr + ((kb + 2) % 4) * kXs + oc * 9;  // slot of block k-2
@@ -1215,27 +1219,24 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
 #pragma unroll
                 for (int j = 0; j < 8; ++j) q = __fma_rn(-M[j * 256], xg[j], q);
             }
-            mb_wait(sb0 + 8 * st, (unsigned)((kb / kS) & 1));
+            mb_wait(sb0 + 8 * st, (unsigned)((u / kS) & 1));
             unsigned long long t_w = 0;
             if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_w));
-            // epilogue operand: issued now, consumed at the publication
             const double ad = (oc == 0 && row < nb && a.final_out && a.add) ? a.add[rqst[st][rl].y] : 0.0;
             if (Oc.x >= 0) {
                 const double* M = Ms + tid;
                 const double* sg = sst[st] + oc * 9;
 #pragma unroll
                 for (int j = 0; j < 8; ++j) q = __fma_rn(M[j * 256], sg[j], q);
-            } else if (oc == (row & 63) >> 3 && row < nb) {
+            } else if (oc == (row >> 3) && row < nb) {
                 q += sst[st][row + (row >> 3)];  // identity Dinv: s_row
             }
             unsigned long long t_m = 0;
             if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_m));
-            // x_{k-1}: own half (named barrier over the compute warps) and the
-            // peer's half (DSMEM); re-arm that x barrier for block k+1
-            asm volatile("bar.sync 1, 256;" ::: "memory");
+            // x_{k-1}: both halves from the other pair; re-arm for k+3
             if (kb >= 1) {
                 wait_x(kb - 1);
-                if (tid == 0 && kb + 1 < nbk) expect_x(kb + 1);
+                if (tid == 0 && kb + 3 < nbk) expect_x(kb + 3);
             }
             unsigned long long t_s = 0;
             if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_s));
@@ -1249,16 +1250,17 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
             q += __shfl_xor_sync(FULL, q, 2);
             q += __shfl_xor_sync(FULL, q, 4);
             const double cx = q;
-            // publish x_k: own ring, the peer's ring (st.async completing on
-            // the peer's x barrier), global solution, epilogue
+            // publish x_k: own ring, the other three rings, global, epilogue
             if (oc == 0) {
                 const double xv = row < nb ? cx : 0.0;
                 const int xi = (kb % 4) * kXs + row + (row >> 3);
                 xr[xi] = xv;
-                asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(
-                                 xr_peer + 8u * (unsigned)xi),
-                             "l"(__double_as_longlong(xv)), "r"(xb_peer + 8u * (unsigned)(kb & 1))
-                             : "memory");
+#pragma unroll
+                for (int r2 = 0; r2 < 3; ++r2)
+                    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(
+                                     xr_rem[r2] + 8u * (unsigned)xi),
+                                 "l"(__double_as_longlong(xv)), "r"(xb_rem[r2] + 8u * (unsigned)(kb & 3))
+                                 : "memory");
                 if (row < nb) {
                     const int2 rq = rqst[st][rl];
                     st_relaxed(a.out + rq.x, cx);
@@ -1271,7 +1273,8 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
             }
             __syncwarp();
             if (lane == 0) asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(eb0 + 8 * st) : "memory");
-            if (a.trace && tid == 0 && cr == 0) {
+            asm volatile("bar.sync 1, 256;" ::: "memory");  // own half of x_k for this pair's next block
+            if (a.trace && tid == 0 && hf == 0) {
                 unsigned long long t_e;
                 asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_e));
                 a.trace[4 * kb] = t_w;
@@ -1280,8 +1283,12 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
                 a.trace[4 * kb + 3] = t_e;
             }
         }
-        // the peer's last st.async must land before this CTA may exit
-        wait_x(nbk - 1);
+        // x blocks that arrive but are never consumed (the last ones) must
+        // land before the CTA exits
+        for (int j = nbk - 2 > 0 ? nbk - 2 : 0; j < nbk; ++j) {
+            const bool waited = ((j & 1) != pr) ? (j + 1 < nbk) : (j + 2 < nbk);
+            if (!waited) wait_x(j);
+        }
         asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
         asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
         return;
@@ -1295,8 +1302,8 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
     // and (recent tasks) right-hand side and chunk partials are loaded while
     // the current task waits, so a task costs one L2 round trip, not three
     // dependent HBM loads.
-    const int gw = (blockIdx.x - 2) * (blockDim.x >> 5) + warp;
-    const int W = (gridDim.x - 2) * (blockDim.x >> 5);
+    const int gw = (blockIdx.x - 4) * (blockDim.x >> 5) + warp;
+    const int W = (gridDim.x - 4) * (blockDim.x >> 5);
     struct Stage {
         int4 T;
         int cc[8];
@@ -2626,45 +2633,53 @@ void trsv_blk(const Launch& L, bool upper, const NarrowArgs& a, int cluster, siz
     count(L);
 }
 
-void trsv_chain(const Launch& L, bool upper, const ChainArgs& a) {
+cudaError_t trsv_chain(const Launch& L, bool upper, const ChainArgs& a) {
     static bool attr[2] = {false, false};
-    static int occ[2] = {0, 0};
+    static int max_clusters[2] = {0, 0};
     auto fn = upper ? (void*)k_trsv_chain<true> : (void*)k_trsv_chain<false>;
-    if (!attr[upper]) {
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kChainSmem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[upper], upper ? k_trsv_chain<true> : k_trsv_chain<false>,
-                                                      kChainThreads, kChainSmem);
-        if (occ[upper] < 1) occ[upper] = 1;
-        attr[upper] = true;
-    }
-    // even grid (clusters of 2: CTAs 0-1 = the chain pair, the rest workers);
-    // cooperative so every worker is resident while the chain waits on them
-    long long g = std::max<long long>(4, std::min<long long>((long long)L.num_sms * occ[upper],
-                                                             2 + ((long long)a.n_rows + 8) / 9));
-    g &= ~1LL;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3((unsigned)g);
     cfg.blockDim = dim3(kChainThreads);
     cfg.dynamicSmemBytes = kChainSmem;
     cfg.stream = L.stream;
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.x = 4;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     at[1].id = cudaLaunchAttributeCooperative;
     at[1].val.cooperative = 1;
     cfg.attrs = at;
+    if (!attr[upper]) {
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kChainSmem);
+        cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        // how many 4-CTA clusters fit at once (not every GPC holds a
+        // multiple of 4 SMs: 33 clusters on a 148-SM B200)
+        cfg.gridDim = dim3(4 * (unsigned)L.num_sms);
+        cfg.numAttrs = 1;
+        int mc = 0;
+        if (upper)
+            cudaOccupancyMaxActiveClusters(&mc, k_trsv_chain<true>, &cfg);
+        else
+            cudaOccupancyMaxActiveClusters(&mc, k_trsv_chain<false>, &cfg);
+        max_clusters[upper] = mc > 1 ? mc : 2;
+        attr[upper] = true;
+    }
+    // clusters of 4 (CTAs 0-3 = the chain, the rest workers); cooperative so
+    // every worker is resident while the chain waits on them
+    const long long want = 1 + ((long long)a.n_rows + 8) / 9 / 4 + 1;
+    const long long nclu = std::max<long long>(2, std::min<long long>(max_clusters[upper], want));
+    cfg.gridDim = dim3((unsigned)(4 * nclu));
     // EXG_NO_COOP: plain cluster launch (ncu cannot replay a cooperative
-    // cluster launch); co-residency then rests on one CTA per SM and a grid
-    // of at most one CTA per SM, which the occupancy sizing above guarantees
+    // cluster launch); co-residency then rests on the occupancy sizing above
     static const bool no_coop = getenv("EXG_NO_COOP") != nullptr;
     cfg.numAttrs = no_coop ? 1 : 2;
+    cudaError_t e;
     if (upper)
-        cudaLaunchKernelEx(&cfg, k_trsv_chain<true>, a);
+        e = cudaLaunchKernelEx(&cfg, k_trsv_chain<true>, a);
     else
-        cudaLaunchKernelEx(&cfg, k_trsv_chain<false>, a);
+        e = cudaLaunchKernelEx(&cfg, k_trsv_chain<false>, a);
     count(L);
+    return e;
 }
 
 void trsv_wide(const Launch& L, bool upper, const TrsvArgs& a) {

@@ -1365,10 +1365,20 @@ exg_status exg_er_begin(exg_ctx* c, const double* x_k, const double* u_k, const 
         Fk = c->Fk;
     }
     exg::dev::spmv_b2(L, B.rowptr, B.col, B.val, B.n_rows, c->u_k, c->u_k1, h, c->t1, c->t2, Fk);
-    solve_dev(c, c->t1, c->v1, -1.0, c->xk, nullptr);      // v1 = x_k - G^{-1} rhs
-    solve_dev(c, c->t2, c->gb, 1.0, nullptr, nullptr);     // gb_slope = G^{-1} B slope
-    exg::dev::spmv(L, C.rowptr, C.col, C.val, C.n_rows, c->gb, c->t3, nullptr, nullptr, 0);
-    solve_dev(c, c->t3, c->startv, 1.0, c->v1, nullptr);   // start = v1 + G^{-1} C gb
+    if (c->opt.trsv_mode == EXG_TRSV_FAST) {
+        // start = v1 + v2 = x_k - G^{-1} rhs + G^{-1} C gb = x_k + G^{-1}(C gb - rhs):
+        // two solves instead of three (the same value up to rounding, which
+        // FAST mode already reorders)
+        solve_dev(c, c->t2, c->gb, 1.0, nullptr, nullptr);     // gb_slope = G^{-1} B slope
+        exg::dev::spmv_sub(L, C.rowptr, C.col, C.val, C.n_rows, c->gb, c->t1, c->t3);
+        solve_dev(c, c->t3, c->startv, 1.0, c->xk, nullptr);   // start = x_k + G^{-1}(C gb - rhs)
+    } else {
+        // the reference's order (integrate.cpp:224-231), bit for bit
+        solve_dev(c, c->t1, c->v1, -1.0, c->xk, nullptr);      // v1 = x_k - G^{-1} rhs
+        solve_dev(c, c->t2, c->gb, 1.0, nullptr, nullptr);     // gb_slope = G^{-1} B slope
+        exg::dev::spmv(L, C.rowptr, C.col, C.val, C.n_rows, c->gb, c->t3, nullptr, nullptr, 0);
+        solve_dev(c, c->t3, c->startv, 1.0, c->v1, nullptr);   // start = v1 + G^{-1} C gb
+    }
     c->h_built = h;
     c->basis_valid = false;
     ck(cudaGetLastError(), "er_begin launch");

@@ -91,6 +91,17 @@ __global__ void __launch_bounds__(kSpmvWarps * 32)
 
 // t1 = 0.0 + 1.0 * (B u_k)  (add(residual_F == 0, spmv(B, u_k)), integrate.cpp:224)
 // t2 = B * slope, slope = (u_k1 - u_k) * (1/h)              (integrate.cpp:220-221,228)
+// y = A x - z (FAST-mode er_begin: C gb_slope - rhs in one pass)
+__global__ void __launch_bounds__(kSpmvWarps * 32)
+    k_spmv_sub(const int* __restrict__ rowptr, const int* __restrict__ col,
+               const double* __restrict__ val, int n_rows, const double* __restrict__ x,
+               const double* __restrict__ z, double* __restrict__ y) {
+    __shared__ int s_col[kSpmvWarps][kSpmvCap];
+    __shared__ double s_val[kSpmvWarps][kSpmvCap];
+    const int wg = blockIdx.x * kSpmvWarps + (threadIdx.x >> 5);
+    spmv_warp_rows(rowptr, col, val, n_rows, wg, [&](int c) { return x[c]; },
+                   [&](int r, double sv) { y[r] = sv - z[r]; }, s_col, s_val);
+}
 __global__ void __launch_bounds__(kSpmvWarps * 32)
     k_spmv_b2(const int* __restrict__ rowptr, const int* __restrict__ col,
               const double* __restrict__ val, int n_rows, const double* __restrict__ u_k,
@@ -2541,6 +2552,14 @@ void spmv(const Launch& L, const int* rowptr, const int* col, const double* val,
     if (n_rows <= 0) return;
     const unsigned int grid = cdiv(cdiv(n_rows, 32), kSpmvWarps);
     k_spmv<<<grid, kSpmvWarps * 32, 0, L.stream>>>(rowptr, col, val, n_rows, x, y, ctrl, vbase, ldv);
+    count(L);
+}
+
+void spmv_sub(const Launch& L, const int* rowptr, const int* col, const double* val, int n_rows,
+              const double* x, const double* z, double* y) {
+    if (n_rows <= 0) return;
+    const unsigned int grid = cdiv(cdiv(n_rows, 32), kSpmvWarps);
+    k_spmv_sub<<<grid, kSpmvWarps * 32, 0, L.stream>>>(rowptr, col, val, n_rows, x, z, y);
     count(L);
 }
 

@@ -382,7 +382,10 @@ void mevp_dev(exg_ctx* c, const double* v, double h, const exg_mevp_cfg& cfg, in
     auto iteration = [&](int dense_m, unsigned long long cond) {
         // w = -G^{-1}(C v_j)   (krylov.cpp:120-121)
         cudaEvent_t p0 = c->prof_begin();
-        exg::dev::spmv(L, C.rowptr, C.col, C.val, C.n_rows, nullptr, c->t, c->ctrl, c->V, c->ldv);
+        if (c->opt.trsv_mode == EXG_TRSV_FAST)
+            exg::dev::spmv_v4(L, C.rowptr, C.col, C.val, C.n_rows, c->t, c->ctrl, c->V, c->ldv);
+        else
+            exg::dev::spmv(L, C.rowptr, C.col, C.val, C.n_rows, nullptr, c->t, c->ctrl, c->V, c->ldv);
         c->prof_end(EXG_K_SPMV, p0);
         solve_dev(c, c->t, c->w, -1.0, nullptr, c->ctrl);
         cudaEvent_t p1 = c->prof_begin();

@@ -116,6 +116,8 @@ struct Launch {
 
 void spmv(const Launch& L, const int* rowptr, const int* col, const double* val, int n_rows,
           const double* x, double* y, const Ctrl* ctrl, const double* vbase, long long ldv);
+void spmv_v4(const Launch& L, const int* rowptr, const int* col, const double* val, int n_rows,
+             double* y, const Ctrl* ctrl, const double* vbase, long long ldv);
 void spmv_sub(const Launch& L, const int* rowptr, const int* col, const double* val, int n_rows,
               const double* x, const double* z, double* y);
 void spmv_b2(const Launch& L, const int* rowptr, const int* col, const double* val, int n_rows,

@@ -91,6 +91,29 @@ __global__ void __launch_bounds__(kSpmvWarps * 32)
 
 // t1 = 0.0 + 1.0 * (B u_k)  (add(residual_F == 0, spmv(B, u_k)), integrate.cpp:224)
 // t2 = B * slope, slope = (u_k1 - u_k) * (1/h)              (integrate.cpp:220-221,228)
+// FAST-mode SpMV of the Arnoldi loop: 4 lanes per row (CSR-vector), each
+// lane strides the row's entries by 4 with fused multiply-adds, a fixed
+// 2-step butterfly combines them (deterministic; not the reference's
+// row-sequential order, which k_spmv keeps).  Coalesced col/val loads and
+// neighbouring gathers instead of one long per-lane chain.
+__global__ void __launch_bounds__(256)
+    k_spmv_v4(const int* __restrict__ rowptr, const int* __restrict__ col,
+              const double* __restrict__ val, int n_rows, double* __restrict__ y, const Ctrl* ctrl,
+              const double* __restrict__ xcol_base, long long ldv) {
+    if (ctrl->converged || ctrl->status) return;
+    const double* xs = xcol_base + (long long)ctrl->j * ldv;
+    const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 2;
+    const int sub = threadIdx.x & 3;
+    double acc = 0.0;
+    if (r < n_rows) {
+        const int k1 = __ldg(rowptr + r + 1);
+        for (int k = __ldg(rowptr + r) + sub; k < k1; k += 4) acc = __fma_rn(__ldcs(val + k), xs[__ldcs(col + k)], acc);
+    }
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    if (r < n_rows && sub == 0) y[r] = acc;
+}
+
 // y = A x - z (FAST-mode er_begin: C gb_slope - rhs in one pass)
 __global__ void __launch_bounds__(kSpmvWarps * 32)
     k_spmv_sub(const int* __restrict__ rowptr, const int* __restrict__ col,
@@ -2552,6 +2575,14 @@ void spmv(const Launch& L, const int* rowptr, const int* col, const double* val,
     if (n_rows <= 0) return;
     const unsigned int grid = cdiv(cdiv(n_rows, 32), kSpmvWarps);
     k_spmv<<<grid, kSpmvWarps * 32, 0, L.stream>>>(rowptr, col, val, n_rows, x, y, ctrl, vbase, ldv);
+    count(L);
+}
+
+void spmv_v4(const Launch& L, const int* rowptr, const int* col, const double* val, int n_rows,
+             double* y, const Ctrl* ctrl, const double* vbase, long long ldv) {
+    if (n_rows <= 0) return;
+    const unsigned int grid = cdiv(n_rows, 64);
+    k_spmv_v4<<<grid, 256, 0, L.stream>>>(rowptr, col, val, n_rows, y, ctrl, vbase, ldv);
     count(L);
 }
 

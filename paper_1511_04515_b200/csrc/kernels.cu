@@ -1783,12 +1783,13 @@ __global__ void __launch_bounds__(256)
         if (!ctrl->need_weight || ctrl->converged || ctrl->status) return;
         x = vbase + (long long)ctrl->m * ldv;
     }
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    // grid-stride rows (a few partials per SM, not one per 256 rows: the
+    // last block's final sum is the tail of this kernel)
     double sq = 0.0;
-    if (r < n) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
         double s = 0.0;
         for (int k = rowptr[r]; k < rowptr[r + 1]; ++k) s += val[k] * x[col[k]];
-        sq = s * s;
+        sq += s * s;
     }
     const double bs = block_sum(sq, sh);
     if (threadIdx.x == 0) {
@@ -2795,7 +2796,8 @@ void apply_tasks(const Launch& L, const int2* utasks, int n_utasks, const int* u
 void spmv_norm(const Launch& L, const int* rowptr, const int* col, const double* val, int n,
                const double* vbase, long long ldv, double* partials, unsigned int* done,
                Ctrl* ctrl, int from_ctrl_m, double* weight_out) {
-    k_spmv_norm<<<cdiv(n, 256), 256, 0, L.stream>>>(rowptr, col, val, n, vbase, ldv, partials,
+    const unsigned int grid = std::min<unsigned int>(cdiv(n, 256), (unsigned int)L.num_sms * 4);
+    k_spmv_norm<<<grid, 256, 0, L.stream>>>(rowptr, col, val, n, vbase, ldv, partials,
                                                    done, ctrl, from_ctrl_m, weight_out);
     count(L);
 }

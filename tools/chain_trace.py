@@ -32,9 +32,14 @@ nt = t[4 * n:].astype(np.int64)
 
 
 def chain_blocks(arr):
+    # the chain's per-block 4-tuples (written by the two pairs, so not a
+    # single monotone timeline) come first; each is internally ordered and
+    # short; the worker records that follow are triples
     k = 0
-    while 4 * k + 3 < len(arr) and arr[4 * k] > 0 and arr[4 * k + 3] >= arr[4 * k + 2] >= arr[4 * k + 1] >= arr[4 * k] \
-            and (k == 0 or arr[4 * k] >= arr[4 * k - 1]):
+    while 4 * k + 3 < len(arr):
+        t = arr[4 * k: 4 * k + 4]
+        if not (t[0] > 0 and t[0] <= t[1] <= t[2] <= t[3] and t[3] - t[0] < 50_000):
+            break
         k += 1
     return k
 
@@ -44,12 +49,12 @@ for name, arr in (("L", nt[:3 * n]), ("U", nt[3 * n:])):
     if nb == 0:
         continue
     tr = arr[:4 * nb].reshape(nb, 4)
-    tw, tm, ts, te = tr[:, 0], tr[:, 1], tr[:, 2], tr[:, 3]  # stage full, pre done, x_{k-1} in, published
-    prev_e = np.concatenate([[tw[0]], te[:-1]])
+    tw, tm, ts, te = tr[:, 0], tr[:, 1], tr[:, 2], tr[:, 3]  # stage + s staged, pre done, x_{k-1} in, published
+    prev_e = np.concatenate([[tw[0]], te[:-1]])  # block k-1 (the other pair)
     span = (te[-1] - tw[0]) / 1e3
     med = lambda v: float(np.median(v))  # noqa: E731
-    print(f"{name}: chain blocks {nb}, span {span:.1f} us; per block median ns: wait stage {med(tw - prev_e):.0f}, "
-          f"Dinv s - F2 x {med(tm - tw):.0f}, wait x(k-1) {med(ts - tm):.0f}, F1 gemv + publish {med(te - ts):.0f}; "
+    print(f"{name}: chain blocks {nb}, span {span:.1f} us; per block median ns: stage + s {med(tw - prev_e):.0f}, "
+          f"Dinv s {med(tm - tw):.0f}, wait x(k-1) {med(ts - tm):.0f}, F1 + publish {med(te - ts):.0f}; "
           f"total {med(te - prev_e):.0f}")
     rows = nb * 64
     w = arr[4 * nb: 4 * nb + 3 * rows].reshape(rows, 3)

@@ -538,7 +538,7 @@ void plan_triangle(exg_ctx* c, TriPlan& P, bool upper_tri, const std::vector<int
     int slot_total = 0;
     std::vector<int4> ctasks;
     const char* ko = getenv("EXG_CHAIN_OLD");
-    const int kOld = ko ? std::max(atoi(ko), 4) : 7;  // recent window k-7..k-4: <= 256 entries, one prefetched batch
+    const int kOld = ko ? std::max(atoi(ko), 5) : 8;  // recent window k-8..k-5: <= 256 entries, one prefetched batch
     std::vector<ChainRun> cruns;
     std::vector<int> crows, cnptr, cncol;
     std::vector<int4> cblocks;
@@ -548,7 +548,7 @@ void plan_triangle(exg_ctx* c, TriPlan& P, bool upper_tri, const std::vector<int
     std::vector<int> rows, nptr{0}, nmid, ncol;
     std::vector<double> nval, pool;
     constexpr int kB = 64;
-    std::vector<double> Dm(kB * kB), Em(kB * kB), E2(kB * kB), E3(kB * kB), Di(kB * kB), Fm(kB * kB);
+    std::vector<double> Dm(kB * kB), Em(kB * kB), E2(kB * kB), E3(kB * kB), E4(kB * kB), Di(kB * kB), Fm(kB * kB);
     auto diag_of = [&](int r) { return udiag ? (*udiag)[r] : 1.0; };
     // level classes, then absorb short wide stretches into the narrow runs
     // (a launch costs more than a few fat levels on the cluster)
@@ -597,11 +597,13 @@ void plan_triangle(exg_ctx* c, TriPlan& P, bool upper_tri, const std::vector<int
                 const int ps1 = kb >= 1 ? bs - kB : bs;
                 const int ps2 = kb >= 2 ? bs - 2 * kB : ps1;
                 const int ps3 = kb >= 3 ? bs - 3 * kB : ps2;
+                const int ps4 = kb >= 4 ? bs - 4 * kB : ps3;
                 std::fill(Dm.begin(), Dm.end(), 0.0);
                 std::fill(Em.begin(), Em.end(), 0.0);
                 std::fill(E2.begin(), E2.end(), 0.0);
                 std::fill(E3.begin(), E3.end(), 0.0);
-                bool d_ident = true, e1_zero = true, e2_zero = true, e3_zero = true;
+                std::fill(E4.begin(), E4.end(), 0.0);
+                bool d_ident = true, e1_zero = true, e2_zero = true, e3_zero = true, e4_zero = true;
                 const int pso = kb >= kOld ? bs - kOld * kB : p0;  // first position of block k-kOld
                 for (int i = 0; i < bc; ++i) {
                     const int p = bs + i;
@@ -616,8 +618,11 @@ void plan_triangle(exg_ctx* c, TriPlan& P, bool upper_tri, const std::vector<int
                         const int pq = pos_of[col[k]];
                         if (pq < pso) {
                             oldk.push_back({pq, k});
-                        } else if (pq < ps3) {
+                        } else if (pq < ps4) {
                             recv.push_back({col[k], val[k]});
+                        } else if (pq < ps3) {
+                            E4[i * kB + (pq - ps4)] = val[k];
+                            e4_zero = false;
                         } else if (pq < ps2) {
                             E3[i * kB + (pq - ps3)] = val[k];
                             e3_zero = false;
@@ -659,7 +664,7 @@ void plan_triangle(exg_ctx* c, TriPlan& P, bool upper_tri, const std::vector<int
                         cnval.push_back(e.second);
                     }
                     const int e2 = (int)cncol.size() - cr.ent0;
-                    wt.push_back({std::max(0, kb - 4), make_int4(pl, e1, e2, 1 | (nch << 8))});
+                    wt.push_back({std::max(0, kb - 5), make_int4(pl, e1, e2, 1 | (nch << 8))});
                     cnptr.push_back(e2);
                 }
                 std::fill(Di.begin(), Di.end(), 0.0);
@@ -677,12 +682,12 @@ void plan_triangle(exg_ctx* c, TriPlan& P, bool upper_tri, const std::vector<int
                 // (conflict-free shared-memory reads).  Absent matrices are
                 // zeros and flagged -1 in the block descriptor.
                 const int rec = (int)pool.size();
-                pool.resize(pool.size() + 4 * kB * kB, 0.0);
+                pool.resize(pool.size() + 5 * kB * kB, 0.0);
                 auto put_mat = [&](const std::vector<double>& M, int q) {
                     for (int c2 = 0; c2 < 2; ++c2)
                         for (int j = 0; j < 8; ++j)
                             for (int t = 0; t < 256; ++t)
-                                pool[rec + c2 * 4 * 2048 + q * 2048 + j * 256 + t] =
+                                pool[rec + c2 * 5 * 2048 + q * 2048 + j * 256 + t] =
                                     M[(32 * c2 + (t >> 3)) * kB + (t & 7) * 8 + j];
                     return rec;
                 };
@@ -700,7 +705,8 @@ void plan_triangle(exg_ctx* c, TriPlan& P, bool upper_tri, const std::vector<int
                 const int f1 = e1_zero ? -1 : times_dinv(Em, 1);
                 const int f2 = e2_zero ? -1 : times_dinv(E2, 2);
                 const int f3 = e3_zero ? -1 : times_dinv(E3, 3);
-                cblocks.push_back(make_int4(kb * kB, bc, f3, 0));  // .z: F3 present (>= 0)
+                const int f4 = e4_zero ? -1 : times_dinv(E4, 4);
+                cblocks.push_back(make_int4(kb * kB, bc, f3, f4));  // .z / .w: F3 / F4 present (>= 0)
                 cblocks.push_back(make_int4(dofs, f1, f2, rec));  // .w: record offset
                 cblocks.push_back(make_int4(0, 0, 0, 0));
             }

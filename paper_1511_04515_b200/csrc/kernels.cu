@@ -864,9 +864,10 @@ __global__ void __launch_bounds__(EXG_NARROW_THREADS, 1)
 // (DSMEM) and to global memory.
 // ---------------------------------------------------------------------------
 constexpr int kBlk = 64;
-constexpr int kChainStages = 3;  // TMA stages of the chain: block k+2 is in flight while k computes
+constexpr int kChainStages = 2;  // TMA stages per chain CTA (its pair's next block is in flight)
+constexpr int kChainMatsPerBlock = 5;  // Dinv, F1..F4 (the chain handles blocks k-1..k-4)
 constexpr int kChainThreads = 288;  // chain CTAs: 8 compute warps + 1 producer warp; workers use all 9
-constexpr size_t kChainMats = kChainStages * 4 * (kBlk * kBlk / 2) * sizeof(double);  // half of (Dinv, F1, F2, F3) per stage
+constexpr size_t kChainMats = kChainStages * kChainMatsPerBlock * (kBlk * kBlk / 2) * sizeof(double);  // half of (Dinv, F1..F4) per stage
 // launched with more than half an SM's shared memory so that no worker CTA
 // shares an SM with a chain CTA (one CTA per SM)
 constexpr size_t kChainSmem = kChainMats > 120 * 1024 ? kChainMats : 120 * 1024;  // > half an SM: one CTA per SM
@@ -1090,9 +1091,11 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
         constexpr int kXs = 72;   // padded x slot: column c at c + c/8
         constexpr int kHalf = kBlk * kBlk / 2;
         constexpr int kS = kChainStages;
-        constexpr unsigned kMatBytes = 4u * kHalf * sizeof(double);
+        constexpr int kNM = kChainMatsPerBlock;
+        constexpr int kR = kNM;  // x ring slots: blocks k-4..k
+        constexpr unsigned kMatBytes = (unsigned)kNM * kHalf * sizeof(double);
         extern __shared__ __align__(128) double smat[];  // [kS stages][4][kHalf]
-        __shared__ double xr[4 * kXs];                   // x of the last 4 blocks (both halves), slot k % 4
+        __shared__ double xr[kR * kXs];                  // x of the last 5 blocks (both halves), slot k % 5
         __shared__ double sst[kS][kXs];                  // staged s (padded layout)
         __shared__ int2 rqst[kS][32];                    // staged (row id, output position) of own rows
         __shared__ int4 mst[kS][2];                      // staged block descriptor (B, O)
@@ -1113,7 +1116,7 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
             for (int q = 0; q < 4; ++q) asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(xb0 + 8 * q));
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
-        for (int i = tid; i < 4 * kXs; i += blockDim.x) xr[i] = 0.0;
+        for (int i = tid; i < kR * kXs; i += blockDim.x) xr[i] = 0.0;
         unsigned xr_rem[3], xb_rem[3];  // the other three CTAs' rings and x barriers (DSMEM)
         {
             const unsigned xl = (unsigned)__cvta_generic_to_shared(xr);
@@ -1177,10 +1180,10 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
                 const int st = u % kS;
                 if (u >= kS) mb_wait(eb0 + 8 * st, (unsigned)(((u / kS) - 1) & 1));
                 if (lane == 0) {
-                    const unsigned dst = (unsigned)__cvta_generic_to_shared(smat + st * 4 * kHalf);
+                    const unsigned dst = (unsigned)__cvta_generic_to_shared(smat + st * kNM * kHalf);
                     asm volatile(
                         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(dst),
-                        "l"(a.pool + O0.w + hf * 4 * kHalf), "r"(kMatBytes), "r"(fb0 + 8 * st), "l"(pol)
+                        "l"(a.pool + O0.w + hf * kNM * kHalf), "r"(kMatBytes), "r"(fb0 + 8 * st), "l"(pol)
                         : "memory");
                     mst[st][0] = B0;
                     mst[st][1] = O0;
@@ -1232,11 +1235,18 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
             mb_wait(fb0 + 8 * st, (unsigned)((u / kS) & 1));
             const int4 Bc = mst[st][0], Oc = mst[st][1];
             const int nb = Bc.y;
-            const double* Ms = smat + st * 4 * kHalf;
+            const double* Ms = smat + st * kNM * kHalf;
             double q = 0.0;
-            // x_{k-3} (other pair) was waited for at the previous block
+            // x_{k-4} (own pair) and x_{k-3} (other pair) were waited for at
+            // earlier blocks
+            if (Bc.w >= 0) {
+                const double* xg = xr + ((kb + 1) % kR) * kXs + oc * 9;  // slot of block k-4
+                const double* M = Ms + 4 * kHalf + tid;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) q = __fma_rn(-M[j * 256], xg[j], q);
+            }
             if (Bc.z >= 0) {
-                const double* xg = xr + ((kb + 1) % 4) * kXs + oc * 9;  // slot of block k-3
+                const double* xg = xr + ((kb + 2) % kR) * kXs + oc * 9;  // slot of block k-3
                 const double* M = Ms + 3 * kHalf + tid;
 #pragma unroll
                 for (int j = 0; j < 8; ++j) q = __fma_rn(-M[j * 256], xg[j], q);
@@ -1248,7 +1258,7 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
                 if (tid == 0 && kb + 2 < nbk) expect_x(kb + 2);
             }
             if (Oc.z >= 0) {
-                const double* xg = xr + ((kb + 2) % 4) * kXs + oc * 9;  // slot of block k-2
+                const double* xg = xr + ((kb + 3) % kR) * kXs + oc * 9;  // slot of block k-2
                 const double* M = Ms + 2 * kHalf + tid;
 #pragma unroll
                 for (int j = 0; j < 8; ++j) q = __fma_rn(-M[j * 256], xg[j], q);
@@ -1275,7 +1285,7 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
             unsigned long long t_s = 0;
             if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_s));
             if (Oc.y >= 0) {
-                const double* xg = xr + ((kb + 3) % 4) * kXs + oc * 9;  // slot of block k-1
+                const double* xg = xr + ((kb + 4) % kR) * kXs + oc * 9;  // slot of block k-1
                 const double* M = Ms + kHalf + tid;
 #pragma unroll
                 for (int j = 0; j < 8; ++j) q = __fma_rn(-M[j * 256], xg[j], q);
@@ -1287,7 +1297,7 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
             // publish x_k: own ring, the other three rings, global, epilogue
             if (oc == 0) {
                 const double xv = row < nb ? cx : 0.0;
-                const int xi = (kb % 4) * kXs + row + (row >> 3);
+                const int xi = (kb % kR) * kXs + row + (row >> 3);
                 xr[xi] = xv;
 #pragma unroll
                 for (int r2 = 0; r2 < 3; ++r2)

@@ -866,6 +866,12 @@ __global__ void __launch_bounds__(EXG_NARROW_THREADS, 1)
 constexpr int kBlk = 64;
 constexpr int kChainStages = 2;  // TMA stages per chain CTA (its pair's next block is in flight)
 constexpr int kChainMatsPerBlock = 5;  // Dinv, F1..F4 (the chain handles blocks k-1..k-4)
+#ifndef EXG_CHAIN_PAIRS
+#define EXG_CHAIN_PAIRS 3
+#endif
+constexpr int kNP = EXG_CHAIN_PAIRS;     // CTA pairs of the chain cluster (blocks k == p mod kNP)
+constexpr int kCC = 2 * kNP;             // chain CTAs
+static_assert(kNP >= 2 && kNP <= 3, "x barrier ring of 4 assumes 2 <= pairs <= 3");
 constexpr int kChainThreads = 288;  // chain CTAs: 8 compute warps + 1 producer warp; workers use all 9
 constexpr size_t kChainMats = kChainStages * kChainMatsPerBlock * (kBlk * kBlk / 2) * sizeof(double);  // half of (Dinv, F1..F4) per stage
 // launched with more than half an SM's shared memory so that no worker CTA
@@ -1071,8 +1077,8 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
     if (a.ctrl && (a.ctrl->converged || a.ctrl->status)) return;
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (blockIdx.x < 4) {
-        // ===================== chain: two pairs =====================
+    if (blockIdx.x < kCC) {
+        // ===================== chain: kNP pairs =====================
         // The chain is a 4-CTA thread-block cluster on four SMs: pair p
         // (CTAs 2p, 2p+1) takes the blocks k == p (mod 2), and CTA h of a pair
         // owns rows 32h..32h+31 of each of them, so the per-block work that
@@ -1117,12 +1123,12 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
         for (int i = tid; i < kR * kXs; i += blockDim.x) xr[i] = 0.0;
-        unsigned xr_rem[3], xb_rem[3];  // the other three CTAs' rings and x barriers (DSMEM)
+        unsigned xr_rem[kCC - 1], xb_rem[kCC - 1];  // the other CTAs' rings and x barriers (DSMEM)
         {
             const unsigned xl = (unsigned)__cvta_generic_to_shared(xr);
 #pragma unroll
-            for (int q = 0; q < 3; ++q) {
-                const int other = (cr + 1 + q) & 3;
+            for (int q = 0; q < kCC - 1; ++q) {
+                const int other = (cr + 1 + q) % kCC;
                 asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(xr_rem[q]) : "r"(xl), "r"(other));
                 asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(xb_rem[q]) : "r"(xb0), "r"(other));
             }
@@ -1130,7 +1136,7 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
         const int nbk = a.n_blocks;
         // bytes block j brings to this CTA: the mate's half (own pair) or
         // both halves (other pair)
-        auto xbytes = [&](int j) { return (j & 1) == pr ? 32u * 8u : 64u * 8u; };
+        auto xbytes = [&](int j) { return j % kNP == pr ? 32u * 8u : 64u * 8u; };
         auto expect_x = [&](int j) {
             asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(xb0 + 8 * (j & 3)),
                          "r"(xbytes(j)) : "memory");
@@ -1157,12 +1163,12 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
                     : "=r"(done) : "r"(mb), "r"(par) : "memory");
             }
         };
-        const int nmine = nbk > pr ? (nbk - pr + 1) / 2 : 0;  // blocks of this pair
+        const int nmine = nbk > pr ? (nbk - pr + kNP - 1) / kNP : 0;  // blocks of this pair
         if (warp == 8) {
             // ---------------- producer ----------------
             unsigned long long pol;
             asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-            auto blk = [&](int u) { return pr + 2 * u; };
+            auto blk = [&](int u) { return pr + kNP * u; };
             int4 B0 = make_int4(0, 0, 0, 0), O0 = make_int4(-1, -1, -1, 0);
             int4 B1 = B0, O1 = O0;
             if (nmine > 0) {
@@ -1230,32 +1236,33 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
         const int rl = tid >> 3, oc = tid & 7;
         const int row = 32 * hf + rl;  // row of the block owned by this thread group
         for (int u = 0; u < nmine; ++u) {
-            const int kb = pr + 2 * u;
+            const int kb = pr + kNP * u;
             const int st = u % kS;
             mb_wait(fb0 + 8 * st, (unsigned)((u / kS) & 1));
             const int4 Bc = mst[st][0], Oc = mst[st][1];
             const int nb = Bc.y;
             const double* Ms = smat + st * kNM * kHalf;
             double q = 0.0;
-            // x_{k-4} (own pair) and x_{k-3} (other pair) were waited for at
-            // earlier blocks
+            // x_{k-4} was waited for at an earlier block (kNP <= 3)
             if (Bc.w >= 0) {
                 const double* xg = xr + ((kb + 1) % kR) * kXs + oc * 9;  // slot of block k-4
                 const double* M = Ms + 4 * kHalf + tid;
 #pragma unroll
                 for (int j = 0; j < 8; ++j) q = __fma_rn(-M[j * 256], xg[j], q);
             }
+            // blocks k-kNP .. k-2 (own pair's previous block: the mate's half;
+            // the others: both halves), each waited once and its barrier
+            // re-armed for block j+4 (cannot be produced before our x_k)
+            for (int j = kb - kNP; j <= kb - 2; ++j) {
+                if (j < 0) continue;
+                wait_x(j);
+                if (tid == 0 && j + 4 < nbk) expect_x(j + 4);
+            }
             if (Bc.z >= 0) {
                 const double* xg = xr + ((kb + 2) % kR) * kXs + oc * 9;  // slot of block k-3
                 const double* M = Ms + 3 * kHalf + tid;
 #pragma unroll
                 for (int j = 0; j < 8; ++j) q = __fma_rn(-M[j * 256], xg[j], q);
-            }
-            // x_{k-2} (own pair): own half from the block barrier at the end of
-            // the previous block, the mate's half by DSMEM; re-arm for k+2
-            if (kb >= 2) {
-                wait_x(kb - 2);
-                if (tid == 0 && kb + 2 < nbk) expect_x(kb + 2);
             }
             if (Oc.z >= 0) {
                 const double* xg = xr + ((kb + 3) % kR) * kXs + oc * 9;  // slot of block k-2
@@ -1300,7 +1307,7 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
                 const int xi = (kb % kR) * kXs + row + (row >> 3);
                 xr[xi] = xv;
 #pragma unroll
-                for (int r2 = 0; r2 < 3; ++r2)
+                for (int r2 = 0; r2 < kCC - 1; ++r2)
                     asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(
                                      xr_rem[r2] + 8u * (unsigned)xi),
                                  "l"(__double_as_longlong(xv)), "r"(xb_rem[r2] + 8u * (unsigned)(kb & 3))
@@ -1329,9 +1336,11 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
         }
         // x blocks that arrive but are never consumed (the last ones) must
         // land before the CTA exits
-        for (int j = nbk - 2 > 0 ? nbk - 2 : 0; j < nbk; ++j) {
-            const bool waited = ((j & 1) != pr) ? (j + 1 < nbk) : (j + 2 < nbk);
-            if (!waited) wait_x(j);
+        {
+            const int last = nmine > 0 ? pr + kNP * (nmine - 1) : -1;  // this pair's last block
+            // waited so far: blocks < last (each at the pair's next block);
+            // our own last block's mate half and everything after it were not
+            for (int j = last > 0 ? last : 0; j < nbk; ++j) wait_x(j);
         }
         asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
         asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -1346,8 +1355,8 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
     // and (recent tasks) right-hand side and chunk partials are loaded while
     // the current task waits, so a task costs one L2 round trip, not three
     // dependent HBM loads.
-    const int gw = (blockIdx.x - 4) * (blockDim.x >> 5) + warp;
-    const int W = (gridDim.x - 4) * (blockDim.x >> 5);
+    const int gw = (blockIdx.x - kCC) * (blockDim.x >> 5) + warp;
+    const int W = (gridDim.x - kCC) * (blockDim.x >> 5);
     struct Stage {
         int4 T;
         int cc[8];
@@ -2704,7 +2713,7 @@ cudaError_t trsv_chain(const Launch& L, bool upper, const ChainArgs& a) {
     cfg.stream = L.stream;
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 4;
+    at[0].val.clusterDim.x = kCC;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     at[1].id = cudaLaunchAttributeCooperative;
@@ -2713,9 +2722,9 @@ cudaError_t trsv_chain(const Launch& L, bool upper, const ChainArgs& a) {
     if (!attr[upper]) {
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kChainSmem);
         cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        // how many 4-CTA clusters fit at once (not every GPC holds a
-        // multiple of 4 SMs: 33 clusters on a 148-SM B200)
-        cfg.gridDim = dim3(4 * (unsigned)L.num_sms);
+        // how many kCC-CTA clusters fit at once (not every GPC holds a
+        // multiple of kCC SMs)
+        cfg.gridDim = dim3(kCC * (unsigned)L.num_sms);
         cfg.numAttrs = 1;
         int mc = 0;
         if (upper)
@@ -2725,11 +2734,11 @@ cudaError_t trsv_chain(const Launch& L, bool upper, const ChainArgs& a) {
         max_clusters[upper] = mc > 1 ? mc : 2;
         attr[upper] = true;
     }
-    // clusters of 4 (CTAs 0-3 = the chain, the rest workers); cooperative so
+    // clusters of kCC (the first = the chain, the rest workers); cooperative so
     // every worker is resident while the chain waits on them
-    const long long want = 1 + ((long long)a.n_rows + 8) / 9 / 4 + 1;
+    const long long want = 1 + ((long long)a.n_rows + 8) / 9 / kCC + 1;
     const long long nclu = std::max<long long>(2, std::min<long long>(max_clusters[upper], want));
-    cfg.gridDim = dim3((unsigned)(4 * nclu));
+    cfg.gridDim = dim3((unsigned)(kCC * nclu));
     // EXG_NO_COOP: plain cluster launch (ncu cannot replay a cooperative
     // cluster launch); co-residency then rests on the occupancy sizing above
     static const bool no_coop = getenv("EXG_NO_COOP") != nullptr;

@@ -515,7 +515,7 @@ void plan_triangle(exg_ctx* c, TriPlan& P, bool upper_tri, const std::vector<int
     P.runs.clear();
     const char* env_t = getenv(upper_tri ? "EXG_NARROW_T_U" : "EXG_NARROW_T_L");
     if (!env_t) env_t = getenv("EXG_NARROW_T");
-    const int T = env_t ? atoi(env_t) : (upper_tri ? 48 : 32);  // swept at 1M (profiles/r01)
+    const int T = env_t ? atoi(env_t) : (upper_tri ? 64 : 48);  // swept at 1M (profiles/r01)
     const char* env_r = getenv("EXG_ABSORB_ROWS");
     const long long absorb_rows = env_r ? atoll(env_r) : 8192;
     const int CAP = TriPlan::kCap;

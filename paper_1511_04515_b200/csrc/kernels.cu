@@ -1244,11 +1244,17 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
             const double* Ms = smat + st * kNM * kHalf;
             double q = 0.0;
             // x_{k-4} was waited for at an earlier block (kNP <= 3)
+            // independent accumulators per matrix and per half of the slice:
+            // a dependent FP64 FMA chain is the latency that matters here
+            double qa = 0.0, qb = 0.0, qc = 0.0, qd = 0.0, qe = 0.0, qf = 0.0;
             if (Bc.w >= 0) {
                 const double* xg = xr + ((kb + 1) % kR) * kXs + oc * 9;  // slot of block k-4
                 const double* M = Ms + 4 * kHalf + tid;
 #pragma unroll
-                for (int j = 0; j < 8; ++j) q = __fma_rn(-M[j * 256], xg[j], q);
+                for (int j = 0; j < 8; j += 2) {
+                    qa = __fma_rn(-M[j * 256], xg[j], qa);
+                    qb = __fma_rn(-M[(j + 1) * 256], xg[j + 1], qb);
+                }
             }
             // blocks k-kNP .. k-2 (own pair's previous block: the mate's half;
             // the others: both halves), each waited once and its barrier
@@ -1262,26 +1268,37 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
                 const double* xg = xr + ((kb + 2) % kR) * kXs + oc * 9;  // slot of block k-3
                 const double* M = Ms + 3 * kHalf + tid;
 #pragma unroll
-                for (int j = 0; j < 8; ++j) q = __fma_rn(-M[j * 256], xg[j], q);
+                for (int j = 0; j < 8; j += 2) {
+                    qc = __fma_rn(-M[j * 256], xg[j], qc);
+                    qd = __fma_rn(-M[(j + 1) * 256], xg[j + 1], qd);
+                }
             }
             if (Oc.z >= 0) {
                 const double* xg = xr + ((kb + 3) % kR) * kXs + oc * 9;  // slot of block k-2
                 const double* M = Ms + 2 * kHalf + tid;
 #pragma unroll
-                for (int j = 0; j < 8; ++j) q = __fma_rn(-M[j * 256], xg[j], q);
+                for (int j = 0; j < 8; j += 2) {
+                    qe = __fma_rn(-M[j * 256], xg[j], qe);
+                    qf = __fma_rn(-M[(j + 1) * 256], xg[j + 1], qf);
+                }
             }
             mb_wait(sb0 + 8 * st, (unsigned)((u / kS) & 1));
             unsigned long long t_w = 0;
             if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_w));
             const double ad = (oc == 0 && row < nb && a.final_out && a.add) ? a.add[rqst[st][rl].y] : 0.0;
+            double sa = 0.0, sb = 0.0;
             if (Oc.x >= 0) {
                 const double* M = Ms + tid;
                 const double* sg = sst[st] + oc * 9;
 #pragma unroll
-                for (int j = 0; j < 8; ++j) q = __fma_rn(M[j * 256], sg[j], q);
+                for (int j = 0; j < 8; j += 2) {
+                    sa = __fma_rn(M[j * 256], sg[j], sa);
+                    sb = __fma_rn(M[(j + 1) * 256], sg[j + 1], sb);
+                }
             } else if (oc == (row >> 3) && row < nb) {
-                q += sst[st][row + (row >> 3)];  // identity Dinv: s_row
+                sa = sst[st][row + (row >> 3)];  // identity Dinv: s_row
             }
+            q = ((sa + sb) + ((qa + qb) + (qc + qd))) + (qe + qf);
             unsigned long long t_m = 0;
             if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_m));
             // x_{k-1}: both halves from the other pair; re-arm for k+3
@@ -1294,8 +1311,13 @@ __global__ void __launch_bounds__(kChainThreads, EXG_CHAIN_MINB)
             if (Oc.y >= 0) {
                 const double* xg = xr + ((kb + 4) % kR) * kXs + oc * 9;  // slot of block k-1
                 const double* M = Ms + kHalf + tid;
+                double pa = 0.0, pb = 0.0;
 #pragma unroll
-                for (int j = 0; j < 8; ++j) q = __fma_rn(-M[j * 256], xg[j], q);
+                for (int j = 0; j < 8; j += 2) {
+                    pa = __fma_rn(-M[j * 256], xg[j], pa);
+                    pb = __fma_rn(-M[(j + 1) * 256], xg[j + 1], pb);
+                }
+                q = q + (pa + pb);
             }
             q += __shfl_xor_sync(FULL, q, 1);
             q += __shfl_xor_sync(FULL, q, 2);

@@ -36,6 +36,21 @@ FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
 METRIC = "time-steps/s (ER, config 1: 1M-node RC mesh)"
 
 
+WORKLOADS = {0: "config0_rc_mesh_32x32", 2: "config2_rlc_grid_500x500",
+             3: "config3_matrix_defined_n11417", 4: "config4_inverter_chains_4096"}
+
+
+def workload_name(config: int, width: int) -> str:
+    """The workload key for `config`; config 1 carries its mesh width."""
+    return WORKLOADS.get(config, f"config1_rc_mesh_{width}x{width}")
+
+
+def l2_note(factor_bytes: float) -> str:
+    if factor_bytes > 126e6:
+        return f"inputs larger than L2 (factors {factor_bytes / 1e9:.2f} GB)"
+    return f"inputs L2-resident (factors {factor_bytes / 1e6:.1f} MB, no flush: small config)"
+
+
 def CFG_FIXED_STEP(s) -> bool:
     """BASELINE.json runs configs 0 and 3 with fixed 1 ps steps."""
     return getattr(s, "config", None) in (0, 3)
@@ -398,12 +413,12 @@ def run_ours(args, rank, world, local):
         "metric": METRIC, "value": round(value, 4), "unit": "steps/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded config-1 generator, DESIGN.md §4)",
-        "config": {"workload": f"config{args.config}_rc_mesh_{args.width}x{args.width}", "n": n,
+        "data": f"synthetic (seeded config-{args.config} generator, DESIGN.md §8)",
+        "config": {"workload": workload_name(args.config, args.width), "n": n,
                    "nnz_C": s.C.nnz, "nnz_G": s.G.nnz, "nnz_LU": int(f.fill_nnz),
                    "n_inputs": ni, "trsv_mode": args.trsv, "weight_mode": args.weight, "loop": args.loop,
                    "parallelism": f"replicas{world}",
-                   "l2": "inputs larger than L2 (factors ~1.4 GB, basis 328 MB)"},
+                   "l2": l2_note(12.0 * float(f.fill_nnz))},
         "arnoldi_iters_per_s": round(allsum(world, float(iters)) / (ms_max / 1e3), 3),
         "m_per_step": m_seq, "gpu_launches": int(launches),
         "roofline": roofline, "cpu_baseline": cpu,
@@ -450,8 +465,8 @@ def run_reference(args, rank, world):
         "metric": METRIC, "value": round(value, 6), "unit": "steps/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(timed / args.steps * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded config-1 generator, DESIGN.md §4)", "impl": "reference",
-        "config": {"workload": f"config{args.config}_rc_mesh_{args.width}x{args.width}", "n": s.n},
+        "data": f"synthetic (seeded config-{args.config} generator, DESIGN.md §8)", "impl": "reference",
+        "config": {"workload": workload_name(args.config, args.width), "n": s.n},
         "cpu_baseline": {"value": round(value, 6), "unit": "steps/s", "cores": 1, "kind": "reference",
                          "sample": f"steps {args.warmup}..{n_total - 1} of the config-1 transient, "
                                    "unmodified exsim_core restated ER loop (cached factorization "

@@ -1571,8 +1571,14 @@ exg_status exg_gather(exg_ctx* c, const int* idx, int k, double* out) {
         c->probe_idx = dalloc<int>(k);
         c->probe_out = dalloc<double>(k);
         c->probe_cap = k;
+        c->probe_host.clear();
     }
-    ck(cudaMemcpyAsync(c->probe_idx, idx, sizeof(int) * k, cudaMemcpyHostToDevice, c->stream), "idx");
+    // a transient probes the same nodes every step: upload the list only when
+    // it changed (a pageable upload is a stream sync)
+    if (c->probe_host.size() != (size_t)k || std::memcmp(c->probe_host.data(), idx, sizeof(int) * k) != 0) {
+        ck(cudaMemcpyAsync(c->probe_idx, idx, sizeof(int) * k, cudaMemcpyHostToDevice, c->stream), "idx");
+        c->probe_host.assign(idx, idx + k);
+    }
     k_gather<<<(k + 255) / 256, 256, 0, c->stream>>>(c->xnext, c->probe_idx, k, c->probe_out);
     c->launches++;
     ck(cudaMemcpyAsync(out, c->probe_out, sizeof(double) * k, cudaMemcpyDeviceToHost, c->stream), "d2h");

@@ -158,6 +158,7 @@ struct exg_ctx {
     double *probe_out = nullptr;
     int* probe_idx = nullptr;
     int probe_cap = 0;
+    std::vector<int> probe_host;  // the index list last uploaded to probe_idx
 
     // profiling: event pairs per kernel class, resolved in exg_profile_get
     bool profiling = false;

@@ -49,6 +49,17 @@ struct Fail {
     std::string msg;
 };
 
+void cuda_chk(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw Fail{EXG_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e)};
+}
+
+struct PinnedDoubles {
+    double* p = nullptr;
+    ~PinnedDoubles() {
+        if (p) cudaFreeHost(p);
+    }
+};
+
 void chk(exg_ctx* ctx, exg_status st) {
     if (st != EXG_OK) {
         char buf[512];
@@ -304,6 +315,8 @@ exg_status exg_transient(exg_ctx* ctx, const exg_system* sp, const exg_step_cont
         const int n = sys.n;
         const int ni = sys.n_inputs();
         chk(ctx, exg_memcpy(ctx, ctx->xnext, x.data(), sizeof(double) * n, cudaMemcpyHostToDevice));
+        PinnedDoubles u_pin;
+        if (ni) cuda_chk(cudaMallocHost(&u_pin.p, sizeof(double) * 2 * ni), "cudaMallocHost");
         double t = 0.0;
         while (t < t_stop - t_tiny) {
             const double seg_end = std::min(next_breakpoint_after(bps, t), t_stop);
@@ -314,8 +327,14 @@ exg_status exg_transient(exg_ctx* ctx, const exg_system* sp, const exg_step_cont
             const std::vector<double> u_k = exg::eval_sources(sys, t);
             const std::vector<double> u_k1 = exg::eval_sources(sys, t + h_try);
             if (ni) {
-                chk(ctx, exg_memcpy(ctx, ctx->u_k, u_k.data(), sizeof(double) * ni, cudaMemcpyHostToDevice));
-                chk(ctx, exg_memcpy(ctx, ctx->u_k1, u_k1.data(), sizeof(double) * ni, cudaMemcpyHostToDevice));
+                // pinned staging, stream-ordered before er_begin; the previous
+                // step's gather synchronised, so its copies have completed
+                std::memcpy(u_pin.p, u_k.data(), sizeof(double) * ni);
+                std::memcpy(u_pin.p + ni, u_k1.data(), sizeof(double) * ni);
+                cuda_chk(cudaMemcpyAsync(ctx->u_k, u_pin.p, sizeof(double) * ni, cudaMemcpyHostToDevice,
+                                         ctx->stream), "u_k upload");
+                cuda_chk(cudaMemcpyAsync(ctx->u_k1, u_pin.p + ni, sizeof(double) * ni,
+                                         cudaMemcpyHostToDevice, ctx->stream), "u_k1 upload");
             }
             // x_k <- previous x_next (device to device)
             chk(ctx, exg_er_begin(ctx, ctx->xnext, ctx->u_k, ctx->u_k1, h_try, EXG_PTR_DEVICE));

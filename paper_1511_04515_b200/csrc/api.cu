@@ -1565,6 +1565,21 @@ exg_status exg_er_nonlinear(exg_ctx* c, double h, const exg_mevp_cfg* cfg, int e
 exg_status exg_gather(exg_ctx* c, const int* idx, int k, double* out) {
     API_BEGIN
     if (k <= 0) return EXG_OK;
+    const exg_status st = exg_gather_async(c, idx, k, nullptr, true);
+    if (st != EXG_OK) return st;
+    ck(cudaMemcpyAsync(out, c->probe_out, sizeof(double) * k, cudaMemcpyDeviceToHost, c->stream), "d2h");
+    ck(cudaStreamSynchronize(c->stream), "gather sync");
+    API_END(c)
+}
+
+}  // extern "C"
+
+// x_next[idx] -> dev_out (probe_out when null), stream-ordered, no host sync.
+// A transient probes the same nodes every step: the index list is uploaded
+// only when it changed (check) or on the first call.
+exg_status exg_gather_async(exg_ctx* c, const int* idx, int k, double* dev_out, bool check) {
+    API_BEGIN
+    if (k <= 0) return EXG_OK;
     if (k > c->probe_cap) {
         dfree(c->probe_idx);
         dfree(c->probe_out);
@@ -1573,18 +1588,18 @@ exg_status exg_gather(exg_ctx* c, const int* idx, int k, double* out) {
         c->probe_cap = k;
         c->probe_host.clear();
     }
-    // a transient probes the same nodes every step: upload the list only when
-    // it changed (a pageable upload is a stream sync)
-    if (c->probe_host.size() != (size_t)k || std::memcmp(c->probe_host.data(), idx, sizeof(int) * k) != 0) {
+    if (c->probe_host.size() != (size_t)k ||
+        (check && std::memcmp(c->probe_host.data(), idx, sizeof(int) * k) != 0)) {
         ck(cudaMemcpyAsync(c->probe_idx, idx, sizeof(int) * k, cudaMemcpyHostToDevice, c->stream), "idx");
         c->probe_host.assign(idx, idx + k);
     }
-    k_gather<<<(k + 255) / 256, 256, 0, c->stream>>>(c->xnext, c->probe_idx, k, c->probe_out);
+    k_gather<<<(k + 255) / 256, 256, 0, c->stream>>>(c->xnext, c->probe_idx, k, dev_out ? dev_out : c->probe_out);
     c->launches++;
-    ck(cudaMemcpyAsync(out, c->probe_out, sizeof(double) * k, cudaMemcpyDeviceToHost, c->stream), "d2h");
-    ck(cudaStreamSynchronize(c->stream), "gather sync");
+    ck(cudaGetLastError(), "gather launch");
     API_END(c)
 }
+
+extern "C" {
 
 // debug: one triangular-solve pair with per-row (start, end) timestamps of the
 // L and U sweeps (ns, %globaltimer), 4n values: L pairs then U pairs

@@ -225,3 +225,8 @@ struct exg_ctx {
     }
 };
 
+
+// internal (api.cu): x_next[idx] -> dev_out (the probe buffer when null) on the
+// context stream without a host sync; the index list is re-uploaded when its
+// length changes, or, with check, when its contents do
+exg_status exg_gather_async(exg_ctx* c, const int* idx, int k, double* dev_out, bool check);

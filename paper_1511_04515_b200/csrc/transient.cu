@@ -60,6 +60,13 @@ struct PinnedDoubles {
     }
 };
 
+struct DeviceDoubles {
+    double* p = nullptr;
+    ~DeviceDoubles() {
+        if (p) cudaFree(p);
+    }
+};
+
 void chk(exg_ctx* ctx, exg_status st) {
     if (st != EXG_OK) {
         char buf[512];
@@ -317,6 +324,26 @@ exg_status exg_transient(exg_ctx* ctx, const exg_system* sp, const exg_step_cont
         chk(ctx, exg_memcpy(ctx, ctx->xnext, x.data(), sizeof(double) * n, cudaMemcpyHostToDevice));
         PinnedDoubles u_pin;
         if (ni) cuda_chk(cudaMallocHost(&u_pin.p, sizeof(double) * 2 * ni), "cudaMallocHost");
+        // recorded samples: a device ring of up to 256 steps (<= 64 MB) and a
+        // pinned host mirror; one read-back per ring instead of a sync per step
+        const int k_rec = static_cast<int>(rec.size());
+        const int ring_steps = static_cast<int>(
+            std::max<size_t>(1, std::min<size_t>(256, (size_t(64) << 20) / (sizeof(double) * k_rec))));
+        DeviceDoubles ring;
+        PinnedDoubles ring_pin;
+        cuda_chk(cudaMalloc(&ring.p, sizeof(double) * k_rec * ring_steps), "cudaMalloc");
+        cuda_chk(cudaMallocHost(&ring_pin.p, sizeof(double) * k_rec * ring_steps), "cudaMallocHost");
+        int filled = 0;
+        bool first_gather = true;  // a user exg_gather may have left another list
+        auto flush_ring = [&]() {
+            if (!filled) return;
+            const size_t cnt = (size_t)filled * k_rec;
+            cuda_chk(cudaMemcpyAsync(ring_pin.p, ring.p, sizeof(double) * cnt, cudaMemcpyDeviceToHost,
+                                     ctx->stream), "samples d2h");
+            cuda_chk(cudaStreamSynchronize(ctx->stream), "samples sync");
+            res->samples.insert(res->samples.end(), ring_pin.p, ring_pin.p + cnt);
+            filled = 0;
+        };
         double t = 0.0;
         while (t < t_stop - t_tiny) {
             const double seg_end = std::min(next_breakpoint_after(bps, t), t_stop);
@@ -351,9 +378,11 @@ exg_status exg_transient(exg_ctx* ctx, const exg_system* sp, const exg_step_cont
             res->dims_off.push_back(static_cast<int>(res->dims.size()));
 
             t += h_try;
-            chk(ctx, exg_gather(ctx, rec.data(), static_cast<int>(rec.size()), row.data()));
+            // samples gathered into a device ring, read back in batches
+            chk(ctx, exg_gather_async(ctx, rec.data(), k_rec, ring.p + (size_t)filled * k_rec, first_gather));
+            first_gather = false;
             res->times.push_back(t);
-            res->samples.insert(res->samples.end(), row.begin(), row.end());
+            if (++filled == ring_steps) flush_ring();
 
             const bool grow = !ctl->fixed_step &&
                               (ctl->grow_only_on_clean ? rejects == 0 : rejects < ctl->grow_threshold);
@@ -362,6 +391,7 @@ exg_status exg_transient(exg_ctx* ctx, const exg_system* sp, const exg_step_cont
             if (grow)
                 h_nominal = std::min(ctl->beta * (clamped && rejects == 0 ? h_nominal : h_try), ctl->hmax);
         }
+        flush_ring();
         // the linear factorization is shared by every step: report it once
         if (!res->lu.empty()) res->lu[0] = 1;
         res->loop_s = std::chrono::duration<double>(clock::now() - t2).count();

@@ -261,7 +261,16 @@ void lu_factor(const Csr& A, double pivot_tol, Factor& f) {
 
     Csc a = to_csc(A);
     const auto t0 = clock::now();
-    const std::vector<int> col_order = min_degree_order(A);
+    // The ordering is a function of the pattern alone: a nonlinear transient
+    // refactors the same pattern every attempt, so the last one is reused
+    // when rowptr and col match exactly (same order, bit for bit).
+    static thread_local std::vector<int> cached_rowptr, cached_col, cached_order;
+    if (cached_rowptr != A.rowptr || cached_col != A.col) {
+        cached_order = min_degree_order(A);
+        cached_rowptr = A.rowptr;
+        cached_col = A.col;
+    }
+    const std::vector<int> col_order = cached_order;
     const auto t1 = clock::now();
     // Work in relabelled row coordinates: row i gets the label of its column
     // position in col_order (the diagonal row of column j is label j).  The

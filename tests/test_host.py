@@ -61,6 +61,30 @@ def test_lu_bit_identical_to_reference(ref, cfg, kw):
     assert bit_equal(e["Lx"], f.L.val) and bit_equal(e["Ux"], f.U.val)
 
 
+def _assert_factor_equals_reference(ref, A, f):
+    fh = ref.lu_factor(A)
+    try:
+        e = ref.factor_export(fh)
+    finally:
+        ref.factor_free(fh)
+    assert np.array_equal(e["col_perm"], f.col_perm) and np.array_equal(e["row_perm"], f.row_perm)
+    assert np.array_equal(e["Li"], f.L.col) and np.array_equal(e["Ui"], f.U.col)
+    assert bit_equal(e["Lx"], f.L.val) and bit_equal(e["Ux"], f.U.val)
+
+
+def test_lu_ordering_reuse_across_patterns(ref):
+    """lu_factor reuses the ordering while the pattern is unchanged (a nonlinear
+    transient's refactorisations): same pattern with new values, a different
+    pattern in between, then the first pattern again -- all bit-identical to
+    the reference's lu_factor."""
+    a = ex.System.generate(4, width=10, chains=4, stages=4).G
+    b = ex.System.generate(0).G
+    rng = np.random.default_rng(7)
+    a2 = ex.Csr(a.n_rows, a.n_cols, a.rowptr, a.col, a.val * (1.0 + 0.25 * rng.random(a.val.size)))
+    for A in (a, a2, b, a, a2):
+        _assert_factor_equals_reference(ref, A, ex.lu_factor(A))
+
+
 def test_lu_singular_raises():
     """test_sparse.cpp:104-110."""
     A = ex.Csr(2, 2, np.array([0, 2, 4], np.int32), np.array([0, 1, 0, 1], np.int32), np.ones(4))

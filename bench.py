@@ -339,7 +339,7 @@ def run_ours(args, rank, world, local):
     bytes_spmv = 12 * Cm.nnz + 4 * (n + 1) + 8 * n + 8 * n
     alg = {"trsv_l": bytes_l, "trsv_u": bytes_u, "spmv": bytes_spmv,
            "mgs": None, "dense": None, "weight": None}
-    dom = max(ktimes, key=lambda k: ktimes[k]["ms"])
+    dom = max(ktimes, key=lambda k: ktimes[k]["ms"]) if ktimes else "trsv_u"
     peak, peak_kind = hbm_peak()
     roof = {}
     for k in ("trsv_l", "trsv_u", "spmv"):
@@ -348,7 +348,7 @@ def run_ours(args, rank, world, local):
             ach = alg[k] / per / 1e9
             roof[k] = {"achieved": round(ach, 1), "frac": round(ach / peak, 4),
                        "ms_per_launch": round(per * 1e3, 4), "bytes_per_launch": alg[k]}
-    dom_roof = dom if dom in roof else "trsv_u" if "trsv_u" in roof else next(iter(roof))
+    dom_roof = dom if dom in roof else "trsv_u" if "trsv_u" in roof else next(iter(roof), None)
     traffic = None
     tf = ROOT / "profiles" / "traffic_config1.json"
     if tf.exists():
@@ -356,9 +356,9 @@ def run_ours(args, rank, world, local):
             traffic = json.loads(tf.read_text()).get(dom_roof)
         except Exception:  # noqa: BLE001
             traffic = None
-    roofline = {"bound": "hbm", "kernel": dom_roof, "achieved": roof[dom_roof]["achieved"],
+    roofline = {"bound": "hbm", "kernel": dom_roof, "achieved": roof[dom_roof]["achieved"] if dom_roof else None,
                 "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                "frac": roof[dom_roof]["frac"], "traffic": traffic,
+                "frac": roof[dom_roof]["frac"] if dom_roof else None, "traffic": traffic,
                 "per_kernel": roof, "l_levels": cn.l_levels, "u_levels": cn.u_levels,
                 "kernel_ms": ktimes}
 

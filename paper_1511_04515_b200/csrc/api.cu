@@ -207,6 +207,30 @@ void solve_dev(exg_ctx* c, const double* b, double* final_out, double coef, cons
                     cudaEventRecord(e, c->stream);
                     rev.push_back(e);
                 }
+                if (run.narrow == 3) {
+                    exg::dev::SubArgs sa{};
+                    sa.n_comps = P.sub.n_comps;
+                    sa.max_rows = P.sub.max_rows;
+                    sa.max_tasks = P.sub.max_tasks;
+                    sa.max_levels = P.sub.max_levels;
+                    sa.clev = P.sub.clev;
+                    sa.ltp = P.sub.ltp;
+                    sa.comps = P.sub.comps;
+                    sa.tasks = P.sub.tasks;
+                    sa.meta = P.sub.meta;
+                    sa.ecol = P.sub.ecol;
+                    sa.eval = P.sub.eval;
+                    sa.in = a.in;
+                    sa.diag = a.diag;
+                    sa.out = a.out;
+                    sa.final_out = a.final_out;
+                    sa.out_perm = a.out_perm;
+                    sa.add = a.add;
+                    sa.coef = a.coef;
+                    sa.ctrl = ctrl;
+                    ck(exg::dev::trsv_sub(c->L(), upper, sa), "subtree solve launch");
+                    continue;
+                }
                 if (run.narrow == 2) {
                     const TriPlan::Chain& ch = P.chains[run.a];
                     exg::dev::ChainArgs ca{};
@@ -241,43 +265,11 @@ void solve_dev(exg_ctx* c, const double* b, double* final_out, double coef, cons
                     sbuf_dev += ch.n_rows;
                     continue;
                 }
-                if (!run.narrow) {
-                    if (run.b <= run.a) continue;
-                    a.tasks = tasks + run.a;
-                    a.n_tasks = run.b - run.a;
-                    a.meta = c->meta[tri];
-                    static const bool v2 = getenv("EXG_WIDE_V2") != nullptr;
-                    if (v2) {
-                        if (next_ticket >= kMaxTickets) throw ApiError{EXG_E_CONTRACT, "too many solve runs"};
-                        a.ticket = tickets + next_ticket++;
-                        exg::dev::trsv(c->L(), upper, true, a);
-                    } else {
-                        exg::dev::trsv_wide(c->L(), upper, a);
-                    }
-                } else {
-                    exg::dev::NarrowArgs na{};
-                    na.regions = P.regions + run.a;
-                    na.n_regions = run.b - run.a;
-                    na.rows = P.rows;
-                    na.nptr = P.nptr;
-                    na.nmid = P.nmid;
-                    na.ncol = P.ncol;
-                    na.nval = P.nval;
-                    na.in = a.in;
-                    na.in_perm = a.in_perm;
-                    na.diag = a.diag;
-                    na.out = a.out;
-                    na.final_out = a.final_out;
-                    na.out_perm = a.out_perm;
-                    na.add = a.add;
-                    na.coef = a.coef;
-                    na.ctrl = ctrl;
-                    na.trace = upper ? c->ntrace_u : c->ntrace_l;
-                    na.regions4 = P.regions4 + run.a;
-                    na.blocks = P.blocks;
-                    na.pool = P.pool;
-                    exg::dev::trsv_blk(c->L(), upper, na, c->cluster, P.smem);
-                }
+                if (run.b <= run.a) continue;
+                a.tasks = tasks + run.a;
+                a.n_tasks = run.b - run.a;
+                a.meta = c->meta[tri];
+                ck(exg::dev::trsv_wide(c->L(), upper, a), "wide solve launch");
             }
             if (run_timing) {
                 cudaEvent_t e;
@@ -290,7 +282,14 @@ void solve_dev(exg_ctx* c, const double* b, double* final_out, double coef, cons
                     float ms = 0.f;
                     cudaEventElapsedTime(&ms, rev[i], rev[i + 1]);
                     const TriPlan::Run& run = P.runs[i];
-                    fprintf(stderr, " %s[%d,%d):%.3fms", run.narrow ? "N" : "W", run.a, run.b, ms);
+                    if (run.narrow == 3)
+                        fprintf(stderr, " S[%d comps, %lld rows, depth<=%d]:%.3fms", P.sub.n_comps, P.sub.rows,
+                                P.sub.max_levels, ms);
+                    else if (run.narrow == 2)
+                        fprintf(stderr, " C[%d rows, %d blocks]:%.3fms", P.chains[run.a].n_rows,
+                                P.chains[run.a].n_blocks, ms);
+                    else
+                        fprintf(stderr, " W[%d tasks]:%.3fms", run.b - run.a, ms);
                 }
                 fprintf(stderr, "\n");
                 for (auto e : rev) cudaEventDestroy(e);
@@ -509,7 +508,7 @@ void plan_triangle(exg_ctx* c, TriPlan& P, bool upper_tri, const std::vector<int
                    const std::vector<int>& level, int nl, const std::vector<int>& ptr,
                    const std::vector<int>& col, const std::vector<double>& val,
                    const std::vector<int2>& tasks, const std::vector<double>* udiag,
-                   const int* out_perm) {
+                   const int* out_perm, int sub_level) {
     const int n = (int)ord.size();
     P.free_dev();
     P.runs.clear();
@@ -518,7 +517,6 @@ void plan_triangle(exg_ctx* c, TriPlan& P, bool upper_tri, const std::vector<int
     const int T = env_t ? atoi(env_t) : (upper_tri ? 64 : 48);  // swept at 1M (profiles/r01)
     const char* env_r = getenv("EXG_ABSORB_ROWS");
     const long long absorb_rows = env_r ? atoll(env_r) : 8192;
-    const int CAP = TriPlan::kCap;
     std::vector<int> cnt(nl, 0), lpos(nl + 1, 0);
     for (int r = 0; r < n; ++r) cnt[level[r]]++;
     for (int l = 0; l < nl; ++l) lpos[l + 1] = lpos[l] + cnt[l];
@@ -527,8 +525,6 @@ void plan_triangle(exg_ctx* c, TriPlan& P, bool upper_tri, const std::vector<int
     for (int l = nl - 1; l >= 0; --l) tfirst[l] = std::min(tfirst[l], tfirst[l + 1]);
     std::vector<int> pos_of(n);
     for (int p = 0; p < n; ++p) pos_of[ord[p]] = p;
-    std::vector<int2> regions;
-    std::vector<int4> regions4, blocks;
     struct ChainRun {
         int pos0, rows, blk0, nblocks, ent0, task0 = 0, ntasks = 0, slot0 = 0, slots = 0;
     };
@@ -542,11 +538,7 @@ void plan_triangle(exg_ctx* c, TriPlan& P, bool upper_tri, const std::vector<int
     std::vector<ChainRun> cruns;
     std::vector<int> crows, cnptr, cncol;
     std::vector<int4> cblocks;
-    std::vector<double> cnval;
-    const char* nm = getenv("EXG_NARROW_MODE");
-    const bool chain_mode = !nm || std::string(nm) == "chain";
-    std::vector<int> rows, nptr{0}, nmid, ncol;
-    std::vector<double> nval, pool;
+    std::vector<double> cnval, pool;
     constexpr int kB = 64;
     std::vector<double> Dm(kB * kB), Em(kB * kB), E2(kB * kB), E3(kB * kB), E4(kB * kB), Di(kB * kB), Fm(kB * kB);
     auto diag_of = [&](int r) { return udiag ? (*udiag)[r] : 1.0; };
@@ -554,6 +546,7 @@ void plan_triangle(exg_ctx* c, TriPlan& P, bool upper_tri, const std::vector<int
     // (a launch costs more than a few fat levels on the cluster)
     std::vector<char> is_narrow(nl);
     for (int q = 0; q < nl; ++q) is_narrow[q] = T > 0 && cnt[q] <= T;
+    if (sub_level >= 0) is_narrow[sub_level] = 2;  // the subtree phase: a run of its own
     {
         int q = 0;
         while (q < nl) {
@@ -570,12 +563,19 @@ void plan_triangle(exg_ctx* c, TriPlan& P, bool upper_tri, const std::vector<int
         const bool narrow = is_narrow[l];
         int l1 = l;
         while (l1 < nl && is_narrow[l1] == narrow) ++l1;
+        if (is_narrow[l] != 2 && lpos[l1] == lpos[l]) {  // empty stretch (no rows)
+            l = l1;
+            continue;
+        }
         TriPlan::Run run{};
         run.narrow = narrow;
-        if (!narrow) {
+        if (is_narrow[l] == 2) {
+            run.narrow = 3;  // subtree phase (P.sub)
+            l1 = l + 1;
+        } else if (!narrow) {
             run.a = tfirst[l];
             run.b = tfirst[l1];
-        } else if (chain_mode) {
+        } else {
             // chain + workers: blocks of kB positions over the whole run
             run.narrow = 2;
             run.a = (int)cruns.size();
@@ -719,117 +719,9 @@ void plan_triangle(exg_ctx* c, TriPlan& P, bool upper_tri, const std::vector<int
             slot_total += cr.slots;
             cruns.push_back(cr);
             run.b = run.a + 1;
-        } else {
-            run.a = (int)regions.size();
-            for (int p0 = lpos[l]; p0 < lpos[l1]; p0 += CAP) {
-                const int pc = std::min(CAP, lpos[l1] - p0);
-                const int np0 = (int)rows.size();
-                const int nblk = (pc + kB - 1) / kB;
-                regions.push_back(make_int2(np0, pc));
-                regions4.push_back(make_int4(np0, pc, (int)blocks.size() / 3, nblk));
-                for (int kb = 0; kb < nblk; ++kb) {
-                    const int bs = p0 + kb * kB;                 // first position of the block
-                    const int bc = std::min(kB, p0 + pc - bs);   // rows
-                    const int ps1 = kb >= 1 ? bs - kB : bs;       // first position of block k-1
-                    const int ps2 = kb >= 2 ? bs - 2 * kB : ps1;  // first position of block k-2
-                    std::fill(Dm.begin(), Dm.end(), 0.0);
-                    std::fill(Em.begin(), Em.end(), 0.0);
-                    std::fill(E2.begin(), E2.end(), 0.0);
-                    bool d_ident = true, e1_zero = true, e2_zero = true;
-                    for (int i = 0; i < bc; ++i) {
-                        const int p = bs + i;
-                        const int r = ord[p];
-                        rows.push_back(r);
-                        Dm[i * kB + i] = diag_of(r);
-                        if (Dm[i * kB + i] != 1.0) d_ident = false;
-                        std::vector<std::pair<int, int>> near;  // (slot, k)
-                        for (int k = ptr[r]; k < ptr[r + 1]; ++k) {
-                            const int pq = pos_of[col[k]];
-                            if (pq < p0) {  // earlier region / launch: global
-                                ncol.push_back(col[k]);
-                                nval.push_back(val[k]);
-                            } else if (pq < ps2) {  // this region, blocks <= k-3
-                                near.push_back({pq - p0, k});
-                            } else if (pq < ps1) {  // block k-2 -> E2
-                                E2[i * kB + (pq - ps2)] = val[k];
-                                e2_zero = false;
-                            } else if (pq < bs) {  // block k-1 -> E1
-                                Em[i * kB + (pq - ps1)] = val[k];
-                                e1_zero = false;
-                            } else {  // inside the block -> D
-                                Dm[i * kB + (pq - bs)] = val[k];
-                                d_ident = false;
-                            }
-                        }
-                        std::sort(near.begin(), near.end());
-                        nmid.push_back((int)ncol.size());
-                        for (auto& e : near) {
-                            ncol.push_back(-1 - e.first);
-                            nval.push_back(val[e.second]);
-                        }
-                        nptr.push_back((int)ncol.size());
-                    }
-                    // Dinv by forward substitution on the identity
-                    std::fill(Di.begin(), Di.end(), 0.0);
-                    for (int jc = 0; jc < bc; ++jc)
-                        for (int i = jc; i < bc; ++i) {
-                            double sacc = (i == jc) ? 1.0 : 0.0;
-                            for (int m2 = jc; m2 < i; ++m2) sacc -= Dm[i * kB + m2] * Di[m2 * kB + jc];
-                            Di[i * kB + jc] = sacc / Dm[i * kB + i];
-                        }
-                    auto push_mat = [&](const std::vector<double>& M) {
-                        const int o = (int)pool.size();
-                        pool.insert(pool.end(), M.begin(), M.end());
-                        return o;
-                    };
-                    auto times_dinv = [&](const std::vector<double>& E) {
-                        std::fill(Fm.begin(), Fm.end(), 0.0);
-                        for (int i = 0; i < bc; ++i)
-                            for (int j = 0; j < kB; ++j) {
-                                double sacc = 0.0;
-                                for (int m2 = 0; m2 <= i; ++m2) sacc += Di[i * kB + m2] * E[m2 * kB + j];
-                                Fm[i * kB + j] = sacc;
-                            }
-                        return push_mat(Fm);
-                    };
-                    const int dofs = d_ident ? -1 : push_mat(Di);
-                    const int f1 = e1_zero ? -1 : times_dinv(Em);
-                    const int f2 = e2_zero ? -1 : times_dinv(E2);
-                    blocks.push_back(make_int4(bs - p0, bc, 0, 0));
-                    blocks.push_back(make_int4(dofs, f1, f2, 0));
-                    blocks.push_back(make_int4(0, 0, 0, 0));
-                }
-            }
-            run.b = (int)regions.size();
         }
         P.runs.push_back(run);
         l = l1;
-    }
-    if (!regions.empty()) {
-        P.regions = dalloc<int2>(regions.size());
-        P.rows = dalloc<int>(rows.size());
-        P.nptr = dalloc<int>(nptr.size());
-        P.nmid = dalloc<int>(nmid.size());
-        ck(cudaMemcpy(P.nmid, nmid.data(), nmid.size() * sizeof(int), cudaMemcpyHostToDevice), "plan");
-        P.ncol = dalloc<int>(ncol.size());
-        P.nval = dalloc<double>(nval.size());
-        ck(cudaMemcpy(P.regions, regions.data(), regions.size() * sizeof(int2), cudaMemcpyHostToDevice), "plan");
-        ck(cudaMemcpy(P.rows, rows.data(), rows.size() * sizeof(int), cudaMemcpyHostToDevice), "plan");
-        ck(cudaMemcpy(P.nptr, nptr.data(), nptr.size() * sizeof(int), cudaMemcpyHostToDevice), "plan");
-        if (!ncol.empty()) {
-            ck(cudaMemcpy(P.ncol, ncol.data(), ncol.size() * sizeof(int), cudaMemcpyHostToDevice), "plan");
-            ck(cudaMemcpy(P.nval, nval.data(), nval.size() * sizeof(double), cudaMemcpyHostToDevice), "plan");
-        }
-        P.regions4 = dalloc<int4>(regions4.size());
-        ck(cudaMemcpy(P.regions4, regions4.data(), regions4.size() * sizeof(int4), cudaMemcpyHostToDevice), "plan");
-        P.blocks = dalloc<int4>(blocks.size());
-        ck(cudaMemcpy(P.blocks, blocks.data(), blocks.size() * sizeof(int4), cudaMemcpyHostToDevice), "plan");
-        P.pool = dalloc<double>(std::max<size_t>(pool.size(), 1));
-        if (!pool.empty())
-            ck(cudaMemcpy(P.pool, pool.data(), pool.size() * sizeof(double), cudaMemcpyHostToDevice), "plan");
-        int mx = 0;
-        for (auto& R : regions) mx = std::max(mx, R.y);
-        P.smem = (size_t)mx * sizeof(double);
     }
     if (!cruns.empty()) {
         P.crows = dalloc<int>(crows.size());
@@ -850,11 +742,9 @@ void plan_triangle(exg_ctx* c, TriPlan& P, bool upper_tri, const std::vector<int
         ck(cudaMemcpy(P.crq, crq.data(), crq.size() * sizeof(int2), cudaMemcpyHostToDevice), "chain");
         P.cpslot = dalloc<int>(std::max<size_t>(cpslot.size(), 1));
         ck(cudaMemcpy(P.cpslot, cpslot.data(), cpslot.size() * sizeof(int), cudaMemcpyHostToDevice), "chain");
-        if (!P.pool) {
-            P.pool = dalloc<double>(std::max<size_t>(pool.size(), 1));
-            if (!pool.empty())
-                ck(cudaMemcpy(P.pool, pool.data(), pool.size() * sizeof(double), cudaMemcpyHostToDevice), "chain");
-        }
+        P.pool = dalloc<double>(std::max<size_t>(pool.size(), 1));
+        if (!pool.empty())
+            ck(cudaMemcpy(P.pool, pool.data(), pool.size() * sizeof(double), cudaMemcpyHostToDevice), "chain");
         // run-local views: the nptr index of position j of run q is pos0 + q + j
         for (size_t q = 0; q < cruns.size(); ++q) {
             TriPlan::Chain ch;
@@ -872,10 +762,191 @@ void plan_triangle(exg_ctx* c, TriPlan& P, bool upper_tri, const std::vector<int
             P.chain_rows += cruns[q].rows;
         }
     }
-    P.narrow_rows = (long long)rows.size();
-    P.narrow_nnz = (long long)ncol.size();
     P.chain_slots = slot_total;
     (void)c;
+}
+
+// ---- FAST subtree phase (k_trsv_sub) ----------------------------------------
+// Greedy selection on a strictly-lower pattern (row i lists the rows it must
+// come after): in increasing index, a row joins the phase when every row it
+// lists is already in it and the union of their components plus itself stays
+// within `budget` rows.  The result is closed under the listed relation and
+// split into components with no edge between them.  For L the relation is
+// "depends on" (L itself); for U it is "is depended on by" (U^T), so the U
+// phase is closed under dependents and runs last.  Returns the component
+// count; comp[r] = component id or -1.
+int select_subtrees(int n, const std::vector<int>& ptr, const std::vector<int>& col, int budget,
+                    std::vector<int>& comp) {
+    comp.assign(n, -1);
+    if (budget <= 0) return 0;
+    std::vector<int> par(n), sz(n, 1);
+    std::vector<char> in(n, 0);
+    for (int i = 0; i < n; ++i) par[i] = i;
+    auto find = [&](int x) {
+        while (par[x] != x) {
+            par[x] = par[par[x]];
+            x = par[x];
+        }
+        return x;
+    };
+    std::vector<int> roots;
+    for (int r = 0; r < n; ++r) {
+        bool ok = true;
+        long long tot = 1;
+        roots.clear();
+        for (int k = ptr[r]; k < ptr[r + 1] && ok; ++k) {
+            const int c = col[k];
+            if (!in[c]) {
+                ok = false;
+                break;
+            }
+            const int q = find(c);
+            if (std::find(roots.begin(), roots.end(), q) == roots.end()) {
+                roots.push_back(q);
+                tot += sz[q];
+            }
+        }
+        if (!ok || tot > budget) continue;
+        in[r] = 1;
+        for (int q : roots) par[q] = r;
+        sz[r] = (int)tot;
+    }
+    std::vector<int> id(n, -1);
+    int nc = 0;
+    for (int r = 0; r < n; ++r)
+        if (in[r]) {
+            const int q = find(r);
+            if (id[q] < 0) id[q] = nc++;
+            comp[r] = id[q];
+        }
+    return nc;
+}
+
+void transpose_pattern(int n, const std::vector<int>& ptr, const std::vector<int>& col,
+                       std::vector<int>& tp, std::vector<int>& tc) {
+    tp.assign(n + 1, 0);
+    for (int k = 0; k < ptr[n]; ++k) tp[col[k] + 1]++;
+    for (int i = 0; i < n; ++i) tp[i + 1] += tp[i];
+    tc.resize(ptr[n]);
+    std::vector<int> next(tp.begin(), tp.end() - 1);
+    for (int r = 0; r < n; ++r)
+        for (int k = ptr[r]; k < ptr[r + 1]; ++k) tc[next[col[k]]++] = r;
+}
+
+// Device arrays of the subtree phase: per component its rows by local level
+// (L: ascending row, U: descending), warp tasks within one local level, and
+// each row's entries re-encoded (earlier-phase rows first as global ids, then
+// component slots ascending as ~slot).  Components are issued largest first.
+void build_sub(SubPlan& P, bool upper, const std::vector<int>& comp, int ncomp,
+               const std::vector<int>& ptr, const std::vector<int>& col,
+               const std::vector<double>& val, const int* row_perm) {
+    P.free_dev();
+    if (ncomp == 0) return;
+    const int n = (int)comp.size();
+    std::vector<std::vector<int>> rows(ncomp);
+    for (int i = 0; i < n; ++i) {
+        const int r = upper ? n - 1 - i : i;  // dependencies before dependents
+        if (comp[r] >= 0) rows[comp[r]].push_back(r);
+    }
+    std::vector<int> order(ncomp);
+    for (int q = 0; q < ncomp; ++q) order[q] = q;
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int x, int y) { return rows[x].size() > rows[y].size(); });
+    std::vector<int4> comps, meta;
+    std::vector<int2> tasks, clev;
+    std::vector<int> ltp;
+    std::vector<int> ecol, llev(n, 0), slot(n, -1);
+    std::vector<double> eval;
+    int max_rows = 0, max_lev = 0, max_tasks = 0;
+    for (int q : order) {
+        const std::vector<int>& R = rows[q];
+        int nl = 0;
+        for (int r : R) {
+            int v = 0;
+            for (int k = ptr[r]; k < ptr[r + 1]; ++k)
+                if (comp[col[k]] == q) v = std::max(v, llev[col[k]] + 1);
+            llev[r] = v;
+            nl = std::max(nl, v + 1);
+        }
+        std::vector<int> byl(R);
+        std::stable_sort(byl.begin(), byl.end(), [&](int x, int y) { return llev[x] < llev[y]; });
+        const int pos0 = (int)meta.size();
+        for (size_t i = 0; i < byl.size(); ++i) slot[byl[i]] = (int)i;
+        const int task0 = (int)tasks.size();
+        int g0 = -1, gc = 0, glev = -1, glg = -1;
+        auto flush = [&]() {
+            if (gc) tasks.push_back(make_int2(g0, gc | (glg << 8)));
+            gc = 0;
+        };
+        clev.push_back(make_int2((int)ltp.size(), nl));
+        for (size_t i = 0; i < byl.size(); ++i) {
+            const int r = byl[i];
+            if (i == 0 || llev[r] != llev[byl[i - 1]]) {
+                flush();
+                ltp.push_back((int)tasks.size());
+            }
+            std::vector<std::pair<int, int>> loc;  // (slot, k)
+            const int k0 = (int)ecol.size();
+            for (int k = ptr[r]; k < ptr[r + 1]; ++k) {
+                if (comp[col[k]] == q) {
+                    loc.push_back({slot[col[k]], k});
+                } else {
+                    ecol.push_back(col[k]);
+                    eval.push_back(val[k]);
+                }
+            }
+            std::sort(loc.begin(), loc.end());
+            for (auto& e : loc) {
+                ecol.push_back(~e.first);
+                eval.push_back(val[e.second]);
+            }
+            const int k1 = (int)ecol.size();
+            meta.push_back(make_int4(r, upper ? r : row_perm[r], k0, k1));
+            const int len = k1 - k0;
+            const int p = pos0 + (int)i;
+            if (len > 32) {
+                flush();
+                tasks.push_back(make_int2(p, 1 | (1 << 30)));
+                continue;
+            }
+            const int lg = len <= 4 ? 0 : len <= 8 ? 1 : len <= 16 ? 2 : 3;
+            if (gc && (llev[r] != glev || lg != glg || (gc + 1) << lg > 32)) flush();
+            if (!gc) {
+                g0 = p;
+                glev = llev[r];
+                glg = lg;
+            }
+            ++gc;
+        }
+        flush();
+        ltp.push_back((int)tasks.size());
+        comps.push_back(make_int4(task0, (int)tasks.size() - task0, pos0, (int)R.size()));
+        max_rows = std::max(max_rows, (int)R.size());
+        max_tasks = std::max(max_tasks, (int)tasks.size() - task0);
+        max_lev = std::max(max_lev, nl);
+    }
+    P.n_comps = ncomp;
+    P.max_rows = (max_rows + 1) & ~1;  // keeps the int4 metadata after the slots 16-B aligned
+    P.max_tasks = max_tasks;
+    P.max_levels = max_lev;
+    P.rows = (long long)meta.size();
+    P.nnz = (long long)ecol.size();
+    P.comps = dalloc<int4>(comps.size());
+    P.clev = dalloc<int2>(clev.size());
+    P.ltp = dalloc<int>(ltp.size());
+    ck(cudaMemcpy(P.clev, clev.data(), clev.size() * sizeof(int2), cudaMemcpyHostToDevice), "sub plan");
+    ck(cudaMemcpy(P.ltp, ltp.data(), ltp.size() * sizeof(int), cudaMemcpyHostToDevice), "sub plan");
+    P.tasks = dalloc<int2>(tasks.size());
+    P.meta = dalloc<int4>(meta.size());
+    P.ecol = dalloc<int>(std::max<size_t>(ecol.size(), 1));
+    P.eval = dalloc<double>(std::max<size_t>(eval.size(), 1));
+    ck(cudaMemcpy(P.comps, comps.data(), comps.size() * sizeof(int4), cudaMemcpyHostToDevice), "sub plan");
+    ck(cudaMemcpy(P.tasks, tasks.data(), tasks.size() * sizeof(int2), cudaMemcpyHostToDevice), "sub plan");
+    ck(cudaMemcpy(P.meta, meta.data(), meta.size() * sizeof(int4), cudaMemcpyHostToDevice), "sub plan");
+    if (!ecol.empty()) {
+        ck(cudaMemcpy(P.ecol, ecol.data(), ecol.size() * sizeof(int), cudaMemcpyHostToDevice), "sub plan");
+        ck(cudaMemcpy(P.eval, eval.data(), eval.size() * sizeof(double), cudaMemcpyHostToDevice), "sub plan");
+    }
 }
 
 }  // namespace
@@ -1043,6 +1114,11 @@ exg_status exg_set_factors(exg_ctx* c, int n, const int* Lp, const int* Li, cons
     // With a symmetric pattern ALAP of U mirrors ASAP of L: the separator
     // chains become one long thin stretch (handled on one CTA, pick_schedule)
     // instead of thin levels interleaved with thousands of half-wide ones.
+    // mask: component id per row (>= 0: the row belongs to the FAST subtree
+    // phase, scheduled separately), or null; masked rows and every entry
+    // touching them are left out of the level analysis
+    const std::vector<int>* mask = nullptr;
+    auto masked = [&](int r) { return mask && (*mask)[r] >= 0; };
     auto asap = [&](bool upper_tri, std::vector<int>& lv_) {
         const std::vector<int>& p_ = upper_tri ? up : lp;
         const std::vector<int>& c_ = upper_tri ? uc : lc;
@@ -1050,8 +1126,10 @@ exg_status exg_set_factors(exg_ctx* c, int n, const int* Lp, const int* Li, cons
         int nl = 0;
         for (int i = 0; i < n; ++i) {
             const int r = upper_tri ? n - 1 - i : i;
+            if (masked(r)) continue;
             int v = 0;
-            for (int k = p_[r]; k < p_[r + 1]; ++k) v = std::max(v, lv_[c_[k]] + 1);
+            for (int k = p_[r]; k < p_[r + 1]; ++k)
+                if (!masked(c_[k])) v = std::max(v, lv_[c_[k]] + 1);
             lv_[r] = v;
             nl = std::max(nl, v + 1);
         }
@@ -1064,11 +1142,13 @@ exg_status exg_set_factors(exg_ctx* c, int n, const int* Lp, const int* Li, cons
         int H = 0;
         for (int i = 0; i < n; ++i) {
             const int r = upper_tri ? i : n - 1 - i;  // dependents of r are already final
+            if (masked(r)) continue;
             H = std::max(H, h[r]);
-            for (int k = p_[r]; k < p_[r + 1]; ++k) h[c_[k]] = std::max(h[c_[k]], h[r] + 1);
+            for (int k = p_[r]; k < p_[r + 1]; ++k)
+                if (!masked(c_[k])) h[c_[k]] = std::max(h[c_[k]], h[r] + 1);
         }
         lv_.resize(n);
-        for (int r = 0; r < n; ++r) lv_[r] = H - h[r];
+        for (int r = 0; r < n; ++r) lv_[r] = masked(r) ? 0 : H - h[r];
         return H + 1;
     };
     // schedule cost model (µs): a thin level (<= 16 rows) costs one on-chip
@@ -1077,6 +1157,7 @@ exg_status exg_set_factors(exg_ctx* c, int n, const int* Lp, const int* Li, cons
         const std::vector<int>& p_ = upper_tri ? up : lp;
         std::vector<long long> rows(nl, 0), nz(nl, 0);
         for (int r = 0; r < n; ++r) {
+            if (masked(r)) continue;
             rows[lv_[r]]++;
             nz[lv_[r]] += p_[r + 1] - p_[r];
         }
@@ -1136,6 +1217,10 @@ exg_status exg_set_factors(exg_ctx* c, int n, const int* Lp, const int* Li, cons
         };
         for (int i = 0; i < (int)ord.size(); ++i) {
             const int r = ord[i];
+            if (r < 0) {  // not scheduled here (subtree phase)
+                flush();
+                continue;
+            }
             const int len = ptr[r + 1] - ptr[r];
             if (len > 32) {
                 flush();
@@ -1157,8 +1242,42 @@ exg_status exg_set_factors(exg_ctx* c, int n, const int* Lp, const int* Li, cons
     };
     const std::vector<int2> ltasks = make_tasks(lord, lp, llev, false);
     const std::vector<int2> utasks = make_tasks(uord, up, lev, false);
-    const std::vector<int2> ltasks_f = make_tasks(lord, lp, llev, true);
-    const std::vector<int2> utasks_f = make_tasks(uord, up, lev, true);
+
+    // ---- FAST schedule: the subtree phase (k_trsv_sub) takes the bottom of
+    // the elimination DAG (L: first, U: last); the rest is levelled without it
+    const char* sr_env = getenv("EXG_SUB_ROWS");
+    const int sub_rows = sr_env ? atoi(sr_env) : 0;  // off by default: measured slower at 1M
+    std::vector<int> lcomp, ucomp;
+    const int lncomp = select_subtrees(n, lp, lc, sub_rows, lcomp);
+    std::vector<int> utp, utc;
+    transpose_pattern(n, up, uc, utp, utc);  // U^T: the rows that depend on each row
+    const int uncomp = select_subtrees(n, utp, utc, sub_rows, ucomp);
+    std::vector<int> lflev, uflev;
+    mask = &lcomp;
+    int lnl_f = pick_schedule(false, lflev);
+    mask = &ucomp;
+    int unl_f = pick_schedule(true, uflev);
+    mask = nullptr;
+    int l_sub = -1, u_sub = -1;
+    if (lncomp) {  // L: subtree phase = level 0, the rest after it
+        for (int r = 0; r < n; ++r) lflev[r] = lcomp[r] >= 0 ? 0 : lflev[r] + 1;
+        l_sub = 0;
+        ++lnl_f;
+    }
+    if (uncomp) {  // U: the rest first, subtree phase = the last level
+        for (int r = 0; r < n; ++r) uflev[r] = ucomp[r] >= 0 ? unl_f : uflev[r];
+        u_sub = unl_f;
+        ++unl_f;
+    }
+    const std::vector<int> lford = order_by(lflev, lnl_f, false);
+    const std::vector<int> uford = order_by(uflev, unl_f, true);
+    auto rest_only = [](const std::vector<int>& ord, const std::vector<int>& comp) {
+        std::vector<int> o(ord.size());
+        for (size_t i = 0; i < ord.size(); ++i) o[i] = comp[ord[i]] >= 0 ? -1 : ord[i];
+        return o;
+    };
+    const std::vector<int2> ltasks_f = make_tasks(rest_only(lford, lcomp), lp, lflev, true);
+    const std::vector<int2> utasks_f = make_tasks(rest_only(uford, ucomp), up, uflev, true);
 
     int* ip[] = {c->l_ptr, c->l_col, c->u_ptr, c->u_col, c->row_perm, c->col_perm, c->l_order, c->u_order};
     for (int* p : ip)
@@ -1189,15 +1308,16 @@ exg_status exg_set_factors(exg_ctx* c, int n, const int* Lp, const int* Li, cons
     up_i(c->u_order, uord.data(), n);
     // FAST-mode plan: runs of wide levels (warp tasks, all SMs) and of narrow
     // levels (one thread-block cluster, DSMEM hand-offs)
-    const int lnl = l_levels, unl = u_levels;
-    plan_triangle(c, c->plan[0], false, lord, llev, lnl, lp, lc, lv, ltasks_f, nullptr, nullptr);
-    plan_triangle(c, c->plan[1], true, uord, lev, unl, up, uc, uv, utasks_f, &ud, col_perm);
+    plan_triangle(c, c->plan[0], false, lford, lflev, lnl_f, lp, lc, lv, ltasks_f, nullptr, nullptr, l_sub);
+    plan_triangle(c, c->plan[1], true, uford, uflev, unl_f, up, uc, uv, utasks_f, &ud, col_perm, u_sub);
+    build_sub(c->plan[0].sub, false, lcomp, lncomp, lp, lc, lv, row_perm);
+    build_sub(c->plan[1].sub, true, ucomp, uncomp, up, uc, uv, row_perm);
     {
         std::vector<int4> lm(n), um(n);
         for (int p = 0; p < n; ++p) {
-            const int r = lord[p];
+            const int r = lford[p];
             lm[p] = make_int4(r, row_perm[r], lp[r], lp[r + 1]);
-            const int ru = uord[p];
+            const int ru = uford[p];
             um[p] = make_int4(ru, ru, up[ru], up[ru + 1]);
         }
         if (c->meta[0]) cudaFree(c->meta[0]);
@@ -1520,13 +1640,19 @@ exg_status exg_er_nonlinear(exg_ctx* c, double h, const exg_mevp_cfg* cfg, int e
     auto L = c->L();
     *err_norm = 0.0;
     *n_dims = 0;
+    // residual_F rejects a non-finite state (devices.cpp:205): ||x_next||_inf
+    // (NaN-propagating) is read back with ||deltaF||_inf
+    exg::dev::absmax(L, c->xnext, n, c->partials, c->done, c->weight + 3);
     // deltaF = residual_F(x_next) - F_k
     exg::dev::mos_residual(L, c->n_mos, c->mos_nodes, c->mos_par, c->mos_op, c->xnext, c->mos_r, n,
                            c->node_ptr, c->node_list, c->dF, c->Fk);
     exg::dev::absmax(L, c->dF, n, c->partials, c->done, c->weight + 2);
-    double dfinf = 0.0;
-    ck(cudaMemcpyAsync(&dfinf, c->weight + 2, sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
+    double norms[2] = {0.0, 0.0};  // ||deltaF||_inf, ||x_next||_inf
+    ck(cudaMemcpyAsync(norms, c->weight + 2, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
     ck(cudaStreamSynchronize(c->stream), "sync");
+    if (!std::isfinite(norms[1])) throw ApiError{EXG_E_NONFINITE, "residual_F: non-finite state entry"};
+    const double dfinf = norms[0];
+    if (!std::isfinite(dfinf)) throw ApiError{EXG_E_NONFINITE, "residual_F: non-finite device residual"};
     if (dfinf == 0.0) return EXG_OK;  // both error and correction vanish
     solve_dev(c, c->dF, c->nw, 1.0, nullptr, nullptr);  // w = G^{-1} deltaF
     c->swap_krylov();
@@ -1543,6 +1669,7 @@ exg_status exg_er_nonlinear(exg_ctx* c, double h, const exg_mevp_cfg* cfg, int e
         exg::dev::absmax(L, c->nu, n, c->partials, c->done, c->weight + 2);
         ck(cudaMemcpyAsync(err_norm, c->weight + 2, sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
         ck(cudaStreamSynchronize(c->stream), "sync");
+        if (!std::isfinite(*err_norm)) throw ApiError{EXG_E_NONFINITE, "error estimate: non-finite entry"};
     }
     if (erc && gamma != 0.0) {
         // u = G^{-1} C w ; d = gamma (w + (e^{hJ}u - u)/h) ; x_next += d

@@ -20,22 +20,44 @@ constexpr size_t kTrsvHdr = 1024;  // ticket counters ahead of the solve scratch
 constexpr int kMaxTickets = 256;
 
 // FAST-mode execution plan of one triangle (see plan_triangle, api.cu)
+// subtree phase of one triangle (k_trsv_sub): components of the bottom of
+// the elimination DAG, one CTA each (plan_subtrees, api.cu)
+struct SubPlan {
+    int n_comps = 0, max_rows = 0, max_tasks = 0;
+    long long rows = 0, nnz = 0;
+    int max_levels = 0;
+    int4* comps = nullptr;
+    int2* clev = nullptr;
+    int* ltp = nullptr;
+    int2* tasks = nullptr;
+    int4* meta = nullptr;
+    int* ecol = nullptr;
+    double* eval = nullptr;
+    void free_dev() {
+        void* ps[] = {comps, clev, ltp, tasks, meta, ecol, eval};
+        for (void* p : ps)
+            if (p) cudaFree(p);
+        comps = nullptr;
+        clev = nullptr;
+        ltp = nullptr;
+        tasks = nullptr;
+        meta = nullptr;
+        ecol = nullptr;
+        eval = nullptr;
+        n_comps = max_rows = max_tasks = max_levels = 0;
+        rows = nnz = 0;
+    }
+};
+
 struct TriPlan {
-    static constexpr int kCap = 26112;  // region rows per shared-memory replica (204 KB)
+    // run = wide levels (warp tasks [a, b) of k_trsv3), one chain run
+    // (narrow == 2, chains[a]) or the subtree phase (narrow == 3, sub)
     struct Run {
         int narrow;
-        int a, b;  // wide: task range; narrow: region range
+        int a, b;
     };
     std::vector<Run> runs;
-    int2* regions = nullptr;
-    int* rows = nullptr;
-    int* nptr = nullptr;
-    int* nmid = nullptr;
-    int* ncol = nullptr;
-    double* nval = nullptr;
-    int4* regions4 = nullptr;
-    int4* blocks = nullptr;
-    double* pool = nullptr;
+    double* pool = nullptr;  // chain block records (Dinv, F1..F4)
     // chain + workers runs
     struct Chain {
         int rows_off, nptr_off, ent0, n_rows, blk0, n_blocks, task0, ntasks, slot0, n_slots;
@@ -50,39 +72,19 @@ struct TriPlan {
     int* cpslot = nullptr;
     int2* crq = nullptr;
     long long chain_rows = 0, chain_slots = 0;  // scratch of the chain runs (s values, partial slots)
-    size_t smem = 0;
-    long long narrow_rows = 0, narrow_nnz = 0;
+    SubPlan sub;
     void free_dev() {
-        if (regions) cudaFree(regions);
-        if (rows) cudaFree(rows);
-        if (nptr) cudaFree(nptr);
-        if (nmid) cudaFree(nmid);
-        if (ncol) cudaFree(ncol);
-        if (nval) cudaFree(nval);
-        if (regions4) cudaFree(regions4);
-        if (blocks) cudaFree(blocks);
-        if (pool) cudaFree(pool);
-        if (crows) cudaFree(crows);
-        if (cnptr) cudaFree(cnptr);
-        if (cncol) cudaFree(cncol);
-        if (cnval) cudaFree(cnval);
-        if (cblocks) cudaFree(cblocks);
-        if (ctasks) cudaFree(ctasks);
-        if (cpslot) cudaFree(cpslot);
-        if (crq) cudaFree(crq);
-        crq = nullptr;
-        cpslot = nullptr;
-        chain_rows = chain_slots = 0;
-        ctasks = nullptr;
-        crows = cnptr = cncol = nullptr;
-        cnval = nullptr;
-        cblocks = nullptr;
-        chains.clear();
-        regions4 = blocks = nullptr;
+        sub.free_dev();
+        void* ps[] = {pool, crows, cnptr, cncol, cnval, cblocks, ctasks, cpslot, crq};
+        for (void* p : ps)
+            if (p) cudaFree(p);
         pool = nullptr;
-        regions = nullptr;
-        rows = nptr = nmid = ncol = nullptr;
-        nval = nullptr;
+        crows = cnptr = cncol = cpslot = nullptr;
+        cnval = nullptr;
+        cblocks = ctasks = nullptr;
+        crq = nullptr;
+        chain_rows = chain_slots = 0;
+        chains.clear();
     }
 };
 

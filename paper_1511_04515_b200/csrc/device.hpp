@@ -32,28 +32,26 @@ struct TrsvArgs {
     const int4* meta;   // v3: per level-order position {row, b index, k0, k1}
 };
 
-struct NarrowArgs {
-    const int2* regions;  // (first position, rows) per region of this run
-    int n_regions;
-    const int* rows;      // row id per level-order position (narrow runs)
-    const int* nptr;      // entry offsets per position
-    const int* nmid;      // first near entry per position (far entries come first)
-    const int* ncol;      // encoded: >= 0 far row id, < 0 -(1 + region slot)
-    const double* nval;
+struct SubArgs {
+    int n_comps;
+    int max_rows;         // shared-memory slots (largest component)
+    int max_tasks;        // largest component's task count
+    int max_levels;       // deepest component's level count
+    const int2* clev;     // per component: (first entry in ltp, levels)
+    const int* ltp;       // per component level: first task (ends with the component's task end)
+    const int4* comps;    // per component: (first task, tasks, first position, rows)
+    const int2* tasks;    // (first position, rows | log2(lanes per row) << 8 | long << 30)
+    const int4* meta;     // per position: (row, b index, first entry, end entry)
+    const int* ecol;      // >= 0: row of an earlier phase (global); < 0: ~component slot
+    const double* eval;
     const double* in;
-    const int* in_perm;
-    const double* diag;
-    double* out;          // pivot-coordinate solution (global)
+    const double* diag;   // U only
+    double* out;
     double* final_out;
     const int* out_perm;
     const double* add;
     double coef;
     const Ctrl* ctrl;
-    unsigned long long* trace;  // debug: per row (start, far done, end)
-    // block-recurrence mode (k_trsv_blk)
-    const int4* regions4;  // (first position, rows, first block, blocks)
-    const int4* blocks;    // (first region slot, rows, Dinv offset, F offset)
-    const double* pool;    // Dinv / F matrices, 64x64 row-major each
 };
 
 struct ChainArgs {
@@ -130,15 +128,9 @@ void axpby(const Launch& L, const double* a, double alpha, const double* b, doub
 void erc_update(const Launch& L, const double* w, const double* value, const double* u, int have_u,
                 double ih, double gamma, double* x, int n);
 void trsv(const Launch& L, bool upper, bool reverse, const TrsvArgs& a);
-void trsv_narrow(const Launch& L, bool upper, const NarrowArgs& a, int cluster, size_t smem);
-void trsv_wide(const Launch& L, bool upper, const TrsvArgs& a);
-void trsv_blk(const Launch& L, bool upper, const NarrowArgs& a, int cluster, size_t smem);
+cudaError_t trsv_wide(const Launch& L, bool upper, const TrsvArgs& a);
 cudaError_t trsv_chain(const Launch& L, bool upper, const ChainArgs& a);
-void apply_weight(const Launch& L, const int* uptr, const int* ucol, const double* uval,
-                  const double* udiag, const int* lptr, const int* lcol, const double* lval, int n,
-                  const int* col_perm, const int* row_perm, const double* x, double* t,
-                  double* y_out, double* partials, unsigned int* done, Ctrl* ctrl,
-                  const double* vbase, long long ldv, double* weight_out);
+cudaError_t trsv_sub(const Launch& L, bool upper, const SubArgs& a);
 void apply_tasks(const Launch& L, const int2* utasks, int n_utasks, const int* uorder,
                  const int2* ltasks, int n_ltasks, const int* lorder, const int* uptr,
                  const int* ucol, const double* uval, const double* udiag, const int* lptr,

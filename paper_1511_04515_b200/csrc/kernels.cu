@@ -158,84 +158,6 @@ __global__ void __launch_bounds__(kSpmvWarps * 32)
 // decreasing column order, so the most recently solved dependency comes last
 // and the row's work overlaps its wait (deterministic, not bit-identical).
 // ============================================================================
-constexpr int kTrsvThreads = 128;
-
-template <bool UPPER, bool REVERSE>
-__global__ void __launch_bounds__(kTrsvThreads)
-    k_trsv(TrsvArgs a) {
-    __shared__ unsigned int s_blk;
-    if (a.ctrl && a.ctrl->converged) return;
-    if (threadIdx.x == 0) s_blk = atomicAdd(a.ticket, 1u) + 1u;  // ticket starts at 0xFFFFFFFF
-    __syncthreads();
-    const unsigned int i = s_blk * kTrsvThreads + threadIdx.x;
-    if (i >= (unsigned)a.n) return;
-    const int r = a.order[i];
-    double s = UPPER ? a.in[r] : a.in[a.in_perm[r]];
-    const int k0 = a.ptr[r], k1 = a.ptr[r + 1];
-    constexpr int CH = 4;
-    if (!REVERSE) {
-        int k = k0;
-        for (; k + CH <= k1; k += CH) {
-            int c[CH];
-            double v[CH];
-            unsigned long long y[CH];
-#pragma unroll
-            for (int q = 0; q < CH; ++q) {
-                c[q] = a.col[k + q];
-                v[q] = a.val[k + q];
-            }
-#pragma unroll
-            for (int q = 0; q < CH; ++q) y[q] = ld_relaxed(a.out + c[q]);
-#pragma unroll
-            for (int q = 0; q < CH; ++q) {
-                while (y[q] == kSentinel) y[q] = ld_relaxed(a.out + c[q]);
-                s -= v[q] * __longlong_as_double(y[q]);
-            }
-        }
-        for (; k < k1; ++k) {
-            const int c = a.col[k];
-            unsigned long long y = ld_relaxed(a.out + c);
-            while (y == kSentinel) y = ld_relaxed(a.out + c);
-            s -= a.val[k] * __longlong_as_double(y);
-        }
-    } else {
-        int k = k1 - 1;
-        for (; k - CH + 1 >= k0; k -= CH) {
-            int c[CH];
-            double v[CH];
-            unsigned long long y[CH];
-#pragma unroll
-            for (int q = 0; q < CH; ++q) {
-                c[q] = a.col[k - q];
-                v[q] = a.val[k - q];
-            }
-#pragma unroll
-            for (int q = 0; q < CH; ++q) y[q] = ld_relaxed(a.out + c[q]);
-#pragma unroll
-            for (int q = 0; q < CH; ++q) {
-                while (y[q] == kSentinel) y[q] = ld_relaxed(a.out + c[q]);
-                s -= v[q] * __longlong_as_double(y[q]);
-            }
-        }
-        for (; k >= k0; --k) {
-            const int c = a.col[k];
-            unsigned long long y = ld_relaxed(a.out + c);
-            while (y == kSentinel) y = ld_relaxed(a.out + c);
-            s -= a.val[k] * __longlong_as_double(y);
-        }
-    }
-    if (UPPER) s = s / a.diag[r];
-    st_relaxed(a.out + r, s);
-    if (a.final_out) {
-        // out[col_perm[r]] = coef * x (+ add[col_perm[r]]): scatter + the
-        // caller's vector update, fused (sparse_lu.cpp:289, integrate.cpp)
-        const int q = a.out_perm[r];
-        double y = a.coef * s;
-        if (a.add) y = a.add[q] + y;
-        a.final_out[q] = y;
-    }
-}
-
 // ---------------------------------------------------------------------------
 // v2: warp tasks.  The host cuts the level order into tasks: a LONG row
 // (> kLongRow off-diagonal entries) is one warp task; consecutive short rows
@@ -252,7 +174,6 @@ __global__ void __launch_bounds__(kTrsvThreads)
 // published, so a stale copy can only be the sentinel, which falls back to
 // polling L2.
 // ---------------------------------------------------------------------------
-constexpr int kLongRow = 32;
 constexpr int kTaskLong = 1 << 30;
 __device__ void decide(Ctrl* c);
 
@@ -691,178 +612,142 @@ __global__ void __launch_bounds__(256)
 }
 
 // ---------------------------------------------------------------------------
-// Narrow levels (few rows per level: the dense separator chains at the end
-// of L and the start of U) on ONE thread-block cluster with
-// distributed-shared-memory hand-offs (FAST mode).
+// Subtree phase (FAST): the bottom of the elimination DAG as independent
+// components, one CTA each, hand-offs in SHARED memory.
 //
-// The host cuts each run of narrow levels into regions of <= cap
-// consecutive level-order positions.  Every CTA of the cluster holds a
-// replica of the region's solution values in shared memory (sentinel-
-// initialised); a row's result is pushed into all replicas with DSMEM stores
-// (one lane per CTA) and dependents poll their LOCAL shared memory, so a
-// level hand-off costs a DSMEM store + a local load instead of an L2 round
-// trip.  Dependencies outside the region (earlier regions / launches) are
-// final and read from global memory (L2, never a stale L1 line).  The host
-// re-encodes each row: far entries first (col >= 0), then near entries by
-// increasing region slot (col = -1 - slot), so every lane meets the newest
-// dependencies last.  Warp w of the cluster takes positions w, w+W, ... of the
-// region (a position only waits on smaller positions: no deadlock).
+// The host picks a set S of rows closed under the triangle's dependencies
+// (L: every dependency of a row in S is in S; U: every row that depends on a
+// row of S is in S) and cuts it into weakly connected components of at most
+// EXG_SUB_ROWS rows (union-find, plan_subtrees in api.cu).  No row of one
+// component depends on another component, so each runs on one CTA with no
+// grid-wide hand-off at all: a solved value is published into the CTA's
+// shared-memory slot (pre-filled with the all-ones sentinel) and dependents
+// poll it there (~tens of ns) instead of through L2 (~0.45 µs per level at
+// 1M).  In L the phase runs first (leaves of the elimination tree); in U it
+// runs last, its rows reading the separators solved by the earlier runs from
+// global memory (final, no poll).  Warp tasks as in k_trsv3 (rows grouped
+// within one local level, never across), warp w of the CTA takes tasks
+// w, w+8, ... of its component in level order: a task waits only on earlier
+// tasks, so the earliest unfinished task always progresses.  Each row's
+// entries are re-encoded: earlier-phase dependencies first (global row id),
+// then component slots in increasing order (~slot), so the newest
+// dependency is met last; the next task's metadata and first entries are in
+// flight while the current one waits.
 // ---------------------------------------------------------------------------
-#ifndef EXG_SPIN_NS
-#define EXG_SPIN_NS 0
-#endif
-#ifndef EXG_NARROW_THREADS
-#define EXG_NARROW_THREADS 256
-#endif
 template <bool UPPER>
-__global__ void __launch_bounds__(EXG_NARROW_THREADS, 1)
-    k_trsv_narrow(NarrowArgs a) {
-    extern __shared__ double yrep[];
-    cg::cluster_group cl = cg::this_cluster();
+__global__ void __launch_bounds__(256)
+    k_trsv_sub(SubArgs a) {
     if (a.ctrl && (a.ctrl->converged || a.ctrl->status)) return;
+    // shared memory: [slots: max_rows x 8 B][meta: max_rows x 16 B][tasks: max_tasks x 8 B]
+    //                [level task offsets: max_levels + 1]
+    extern __shared__ __align__(16) double xs[];
+    int4* smeta = reinterpret_cast<int4*>(xs + a.max_rows);
+    int2* stask = reinterpret_cast<int2*>(smeta + a.max_rows);
+    int* sltp = reinterpret_cast<int*>(stask + a.max_tasks);
     const unsigned FULL = 0xffffffffu;
-    const int rank = (int)cl.block_rank();
-    const int cs = (int)cl.num_blocks();
-    const int lane = threadIdx.x & 31;
-    const int nw = blockDim.x >> 5;
-    const int gw = rank * nw + (threadIdx.x >> 5);
-    const int wt = cs * nw;
-    unsigned long long* ybits = reinterpret_cast<unsigned long long*>(yrep);
-    volatile double* yv = yrep;
-    constexpr int NB = 4;  // near entries per lane per chunk (chunk = 128 entries)
-    for (int reg = 0; reg < a.n_regions; ++reg) {
-        const int2 R = a.regions[reg];
-        for (int i = threadIdx.x; i < R.y; i += blockDim.x) ybits[i] = kSentinel;
-        cl.sync();
-        for (int q = gw; q < R.y; q += wt) {
-            const int p = R.x + q;
-            const int r = a.rows[p];
-            unsigned long long t_start = 0, t_far = 0;
-            if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
-            const int k0 = a.nptr[p], km = a.nmid[p], k1 = a.nptr[p + 1];
-            double b = UPPER ? a.in[r] : a.in[a.in_perm[r]];
-            double dg = UPPER ? a.diag[r] : 1.0;
-            int qq = a.final_out ? a.out_perm[r] : 0;
-            double ad = (a.final_out && a.add) ? a.add[qq] : 0.0;
-            // keep these loads here: the compiler would otherwise sink them
-            // past the polling loop, onto the critical path of the hand-off
-            asm volatile("" : "+d"(b), "+d"(dg), "+r"(qq), "+d"(ad));
-            double acc = 0.0;
-            // far entries: final values, independent loads (4 in flight per lane)
-            int k = k0 + lane;
-            for (; k + 96 < km; k += 128) {
-                int c[4];
-                double v[4], y[4];
-#pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    c[t] = a.ncol[k + 32 * t];
-                    v[t] = a.nval[k + 32 * t];
-                }
-#pragma unroll
-                for (int t = 0; t < 4; ++t) y[t] = __ldca(a.out + c[t]);
-#pragma unroll
-                for (int t = 0; t < 4; ++t) acc += v[t] * y[t];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    struct Pre {
+        int2 task;
+        int4 m;
+        double b, dg, ad;
+        int qq;
+        int cc[4];
+        double v[4];
+    };
+    // a task's metadata from shared memory; its operands and first entries
+    // from global memory (independent of the solution: issued before the
+    // level barrier that precedes the task)
+    auto fetch = [&](int tl, int p0, Pre& p) {
+        p.task = stask[tl];
+        const bool lng = p.task.y & kTaskLong;
+        const int lg = lng ? 5 : ((p.task.y >> 8) & 0x7);
+        const int seg = lng ? 0 : (lane >> lg);
+        const int cnt = lng ? 1 : (p.task.y & 0xFF);
+        const int lpr = 1 << lg, sl = lane & (lpr - 1);
+        p.b = 0.0;
+        p.dg = 1.0;
+        p.ad = 0.0;
+        p.qq = 0;
+        if (seg < cnt) {
+            p.m = smeta[p.task.x - p0 + seg];
+            p.b = a.in[p.m.y];
+            if (UPPER) p.dg = a.diag[p.m.x];
+            if (a.final_out) {
+                p.qq = a.out_perm[p.m.x];
+                if (a.add) p.ad = a.add[p.qq];
             }
-            for (; k < km; k += 32) acc += a.nval[k] * __ldca(a.out + a.ncol[k]);
-            // near entries (region slots, newest last): the next chunk's
-            // (slot, value) pairs are loaded while this chunk polls shared memory
-            int cs_[NB], ns_[NB];
-            double cv_[NB], nv_[NB];
-            int base = km;
+        } else {
+            p.m = make_int4(0, 0, 0, 0);
+        }
 #pragma unroll
-            for (int t = 0; t < NB; ++t) {
-                const int kk = base + lane + 32 * t;
-                cs_[t] = kk < k1 ? -1 - a.ncol[kk] : -1;
-                cv_[t] = kk < k1 ? a.nval[kk] : 0.0;
-            }
-            while (base < k1) {
-                const int nb = base + 32 * NB;
+        for (int q = 0; q < 4; ++q) {
+            const int k = p.m.z + sl + q * lpr;
+            p.cc[q] = k < p.m.w ? a.ecol[k] : INT_MIN;
+            p.v[q] = k < p.m.w ? a.eval[k] : 0.0;
+        }
+    };
+    auto xget = [&](int c) { return c == INT_MIN ? 0.0 : c >= 0 ? __ldcg(a.out + c) : xs[~c]; };
+    for (int ci = blockIdx.x; ci < a.n_comps; ci += gridDim.x) {
+        const int4 cr = a.comps[ci];   // (first task, tasks, first position, rows)
+        const int2 cl = a.clev[ci];    // (first level offset, levels)
+        for (int i = threadIdx.x; i < cr.w; i += blockDim.x) smeta[i] = a.meta[cr.z + i];
+        for (int i = threadIdx.x; i < cr.y; i += blockDim.x) stask[i] = a.tasks[cr.x + i];
+        for (int i = threadIdx.x; i <= cl.y; i += blockDim.x) sltp[i] = a.ltp[cl.x + i] - cr.x;
+        __syncthreads();
+        Pre cur;
+        int t = sltp[0] + warp;
+        if (t < sltp[1]) fetch(t, cr.z, cur);
+        for (int lv = 0; lv < cl.y; ++lv) {
+            const int tend = sltp[lv + 1];
+            while (t < tend) {
+                const bool lng = cur.task.y & kTaskLong;
+                const int lg = lng ? 5 : ((cur.task.y >> 8) & 0x7);
+                const int lpr = 1 << lg, sl = lane & (lpr - 1);
+                const int seg = lng ? 0 : (lane >> lg);
+                const int cnt = lng ? 1 : (cur.task.y & 0xFF);
+                const bool active = seg < cnt;
+                double acc = 0.0;
 #pragma unroll
-                for (int t = 0; t < NB; ++t) {
-                    const int kk = nb + lane + 32 * t;
-                    ns_[t] = kk < k1 ? -1 - a.ncol[kk] : -1;
-                    nv_[t] = kk < k1 ? a.nval[kk] : 0.0;
+                for (int q = 0; q < 4; ++q) acc = __fma_rn(cur.v[q], xget(cur.cc[q]), acc);
+                for (int k0 = cur.m.z + sl + 4 * lpr; k0 < cur.m.w; k0 += 4 * lpr) {
+                    int cc[4];
+                    double v[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int k = k0 + q * lpr;
+                        cc[q] = k < cur.m.w ? a.ecol[k] : INT_MIN;
+                        v[q] = k < cur.m.w ? a.eval[k] : 0.0;
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) acc = __fma_rn(v[q], xget(cc[q]), acc);
                 }
-                // warp-uniform wait: every lane re-polls its not-yet-ready
-                // entries until the whole warp is ready (a lane spinning alone
-                // costs ~1 us of reconvergence per hand-off)
-                double yy[NB];
-                bool rd = true;
-#pragma unroll
-                for (int t = 0; t < NB; ++t) {
-                    yy[t] = cs_[t] >= 0 ? yv[cs_[t]] : 0.0;
-                    rd = rd && !(cs_[t] >= 0 && __double_as_longlong(yy[t]) == (long long)kSentinel);
-                }
-                while (!__all_sync(FULL, rd)) {
-                    rd = true;
-#pragma unroll
-                    for (int t = 0; t < NB; ++t) {
-                        if (cs_[t] >= 0 && __double_as_longlong(yy[t]) == (long long)kSentinel) {
-                            yy[t] = yv[cs_[t]];
-                            rd = rd && __double_as_longlong(yy[t]) != (long long)kSentinel;
-                        }
+                for (int o = lpr >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
+                if (active && sl == 0) {
+                    double sv = cur.b - acc;
+                    if (UPPER) sv = sv / cur.dg;
+                    xs[cur.task.x - cr.z + seg] = sv;
+                    a.out[cur.m.x] = sv;
+                    if (a.final_out) {
+                        double yv = a.coef * sv;
+                        if (a.add) yv = cur.ad + yv;
+                        a.final_out[cur.qq] = yv;
                     }
                 }
-#pragma unroll
-                for (int t = 0; t < NB; ++t)
-                    if (cs_[t] >= 0) acc += cv_[t] * yy[t];
-#pragma unroll
-                for (int t = 0; t < NB; ++t) {
-                    cs_[t] = ns_[t];
-                    cv_[t] = nv_[t];
-                }
-                base = nb;
+                t += nw;
+                if (t < tend) fetch(t, cr.z, cur);
             }
-            if (a.trace) {
-                __syncwarp();
-                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_far));
+            // this warp's first task of the next level: its loads are in
+            // flight across the barrier
+            if (lv + 1 < cl.y) {
+                t = tend + warp;
+                if (t < sltp[lv + 2]) fetch(t, cr.z, cur);
             }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
-            double s = b - acc;
-            if (UPPER) s = s / dg;
-            unsigned long long sb = __double_as_longlong(s);
-            if (sb == kSentinel) sb = kCanonNaN;
-            if (lane < cs) {
-                // DSMEM store into replica `lane` (explicit shared::cluster: a
-                // volatile generic store would compile to a system-scope store)
-                const unsigned laddr = (unsigned)__cvta_generic_to_shared(yrep + q);
-                unsigned raddr;
-                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(laddr), "r"(lane));
-                asm volatile("st.relaxed.cluster.shared::cluster.b64 [%0], %1;" ::"r"(raddr), "l"(sb) : "memory");
-            }
-            if (lane == 0) {
-                st_relaxed(a.out + r, s);
-                if (a.final_out) {
-                    double y = a.coef * s;
-                    if (a.add) y = ad + y;
-                    a.final_out[qq] = y;
-                }
-                if (a.trace) {
-                    unsigned long long t_end;
-                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
-                    a.trace[3 * r] = t_start;
-                    a.trace[3 * r + 1] = t_far;
-                    a.trace[3 * r + 2] = t_end;
-                }
-            }
+            __syncthreads();
         }
-        cl.sync();
     }
 }
 
-// ---------------------------------------------------------------------------
-// Block recurrence on the cluster (FAST): each region is cut into blocks of
-// kBlk consecutive level-order positions.  With s_old = b - (entries that
-// reference blocks <= k-2 or earlier regions), E_k = the coupling of block k
-// to block k-1 and D_k its diagonal block, the host precomputes
-// Dinv_k = D_k^-1 and F_k = Dinv_k E_k, so that
-//     x_k = Dinv_k s_old  -  F_k x_{k-1}.
-// Only the last term waits on the previous block: one 64x64 GEMV per 64
-// positions on the critical path instead of one hand-off per level.  Block k
-// runs on CTA k mod CS; x is pushed into every CTA's shared-memory replica
-// (DSMEM) and to global memory.
-// ---------------------------------------------------------------------------
+// Chain geometry (k_trsv_chain): 64-row blocks, kNP CTA pairs.
 constexpr int kBlk = 64;
 constexpr int kChainStages = 2;  // TMA stages per chain CTA (its pair's next block is in flight)
 constexpr int kChainMatsPerBlock = 5;  // Dinv, F1..F4 (the chain handles blocks k-1..k-4)
@@ -878,175 +763,6 @@ constexpr size_t kChainMats = kChainStages * kChainMatsPerBlock * (kBlk * kBlk /
 // shares an SM with a chain CTA (one CTA per SM)
 constexpr size_t kChainSmem = kChainMats > 120 * 1024 ? kChainMats : 120 * 1024;  // > half an SM: one CTA per SM
 static_assert(kChainSmem >= kChainMats, "chain smem");
-
-// GEMV of one warp's 8 outputs against a 64-vector held as (x0, x1) =
-// (v[lane], v[lane+32]); f0/f1 hold the warp's 8 matrix rows the same way.
-__device__ __forceinline__ void warp_gemv8(const double* f0, const double* f1, double x0, double x1,
-                                           double* part) {
-#pragma unroll
-    for (int q = 0; q < 8; ++q) part[q] = f0[q] * x0 + f1[q] * x1;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-        for (int q = 0; q < 8; ++q) part[q] += __shfl_xor_sync(0xffffffffu, part[q], o);
-}
-
-// warp-uniform wait for the 64 (or fewer) published values of a block
-__device__ __forceinline__ void wait_block(volatile double* yv, int first, int rows, double& x0,
-                                           double& x1) {
-    const int lane = threadIdx.x & 31;
-    x0 = lane < rows ? yv[first + lane] : 0.0;
-    x1 = lane + 32 < rows ? yv[first + lane + 32] : 0.0;
-    bool rd = __double_as_longlong(x0) != (long long)kSentinel &&
-              __double_as_longlong(x1) != (long long)kSentinel;
-    while (!__all_sync(0xffffffffu, rd)) {
-        if (lane < rows) x0 = yv[first + lane];
-        if (lane + 32 < rows) x1 = yv[first + lane + 32];
-        rd = __double_as_longlong(x0) != (long long)kSentinel &&
-             __double_as_longlong(x1) != (long long)kSentinel;
-    }
-}
-
-__device__ __forceinline__ void load_rows8(const double* M, int i0, int nb, int ncols, double* f0,
-                                           double* f1) {
-    const int lane = threadIdx.x & 31;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-        const int i = i0 + q;
-        f0[q] = (i < nb && lane < ncols) ? M[i * kBlk + lane] : 0.0;
-        f1[q] = (i < nb && lane + 32 < ncols) ? M[i * kBlk + lane + 32] : 0.0;
-    }
-}
-
-template <bool UPPER>
-__global__ void __launch_bounds__(256, 1)
-    k_trsv_blk(NarrowArgs a) {
-    extern __shared__ double yrep[];
-    __shared__ double sbuf[kBlk];
-    cg::cluster_group cl = cg::this_cluster();
-    if (a.ctrl && (a.ctrl->converged || a.ctrl->status)) return;
-    const unsigned FULL = 0xffffffffu;
-    const int rank = (int)cl.block_rank();
-    const int cs = (int)cl.num_blocks();
-    const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
-    unsigned long long* ybits = reinterpret_cast<unsigned long long*>(yrep);
-    volatile double* yv = yrep;
-    for (int reg = 0; reg < a.n_regions; ++reg) {
-        const int4 R = a.regions4[reg];  // np0, rows, block0, nblocks
-        for (int i = threadIdx.x; i < R.y; i += blockDim.x) ybits[i] = kSentinel;
-        cl.sync();
-        for (int kb = rank; kb < R.w; kb += cs) {
-            const int4 B = a.blocks[3 * (R.z + kb)];      // first slot, rows, -, -
-            const int4 O = a.blocks[3 * (R.z + kb) + 1];  // Dinv off, F1 off, F2 off, -
-            const int nb = B.y;
-            // ---- pass A: s_old = b - (entries older than block k-2), warp per row
-            for (int i = warp; i < nb; i += 8) {
-                const int p = R.x + B.x + i;
-                const int r = a.rows[p];
-                const double b = UPPER ? a.in[r] : a.in[a.in_perm[r]];
-                const int k0 = a.nptr[p], k1 = a.nptr[p + 1];
-                double acc = 0.0;
-                for (int base = k0; base < k1; base += 128) {
-                    int cc[4];
-                    double v[4], y[4];
-                    bool rd = true;
-#pragma unroll
-                    for (int t = 0; t < 4; ++t) {
-                        const int kk = base + lane + 32 * t;
-                        cc[t] = kk < k1 ? a.ncol[kk] : 0;
-                        v[t] = kk < k1 ? a.nval[kk] : 0.0;
-                    }
-#pragma unroll
-                    for (int t = 0; t < 4; ++t) {
-                        const int kk = base + lane + 32 * t;
-                        if (kk >= k1) y[t] = 0.0;
-                        else if (cc[t] >= 0) y[t] = __ldca(a.out + cc[t]);
-                        else {
-                            y[t] = yv[-1 - cc[t]];
-                            rd = rd && __double_as_longlong(y[t]) != (long long)kSentinel;
-                        }
-                    }
-                    while (!__all_sync(FULL, rd)) {
-                        rd = true;
-#pragma unroll
-                        for (int t = 0; t < 4; ++t) {
-                            const int kk = base + lane + 32 * t;
-                            if (kk < k1 && cc[t] < 0 && __double_as_longlong(y[t]) == (long long)kSentinel) {
-                                y[t] = yv[-1 - cc[t]];
-                                rd = rd && __double_as_longlong(y[t]) != (long long)kSentinel;
-                            }
-                        }
-                    }
-#pragma unroll
-                    for (int t = 0; t < 4; ++t) acc += v[t] * y[t];
-                }
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
-                if (lane == 0) sbuf[i] = b - acc;
-            }
-            __syncthreads();
-            // ---- c = Dinv s_old (warp w: outputs 8w..8w+7), F rows prefetched
-            const int i0 = warp * 8;
-            double c[8], part[8], f0[8], f1[8];
-            const double s0 = sbuf[lane < nb ? lane : 0], s1 = sbuf[lane + 32 < nb ? lane + 32 : 0];
-            if (O.x >= 0) {
-                load_rows8(a.pool + (long long)O.x, i0, nb, nb, f0, f1);
-                warp_gemv8(f0, f1, lane < nb ? s0 : 0.0, lane + 32 < nb ? s1 : 0.0, c);
-            } else {
-#pragma unroll
-                for (int q = 0; q < 8; ++q) c[q] = (i0 + q < nb) ? sbuf[i0 + q] : 0.0;
-            }
-            // ---- c -= F2 x_{k-2}  (one block-time of slack)
-            if (O.z >= 0) {
-                const int4 B2 = a.blocks[3 * (R.z + kb - 2)];
-                load_rows8(a.pool + (long long)O.z, i0, nb, B2.y, f0, f1);
-                double x0, x1;
-                wait_block(yv, B2.x, B2.y, x0, x1);
-                warp_gemv8(f0, f1, x0, x1, part);
-#pragma unroll
-                for (int q = 0; q < 8; ++q) c[q] = c[q] - part[q];
-            }
-            // ---- x = c - F1 x_{k-1}  (the only wait on the critical path)
-            if (O.y >= 0) {
-                const int4 B1 = a.blocks[3 * (R.z + kb - 1)];
-                load_rows8(a.pool + (long long)O.y, i0, nb, B1.y, f0, f1);
-                double x0, x1;
-                wait_block(yv, B1.x, B1.y, x0, x1);
-                warp_gemv8(f0, f1, x0, x1, part);
-#pragma unroll
-                for (int q = 0; q < 8; ++q) c[q] = c[q] - part[q];
-            }
-            // ---- publish x_k: replicas (DSMEM), global, fused epilogue
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const int i = i0 + q;
-                if (i >= nb) break;
-                unsigned long long sb = __double_as_longlong(c[q]);
-                if (sb == kSentinel) sb = kCanonNaN;
-                if (lane < cs) {
-                    const unsigned laddr = (unsigned)__cvta_generic_to_shared(yrep + B.x + i);
-                    unsigned raddr;
-                    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(laddr), "r"(lane));
-                    asm volatile("st.relaxed.cluster.shared::cluster.b64 [%0], %1;" ::"r"(raddr), "l"(sb) : "memory");
-                }
-                if (lane == 31) {
-                    const int r = a.rows[R.x + B.x + i];
-                    const double xv = __longlong_as_double(sb);
-                    st_relaxed(a.out + r, xv);
-                    if (a.final_out) {
-                        const int qq = a.out_perm[r];
-                        double yo = a.coef * xv;
-                        if (a.add) yo = a.add[qq] + yo;
-                        a.final_out[qq] = yo;
-                    }
-                }
-            }
-            __syncthreads();
-        }
-        cl.sync();
-    }
-}
 
 // ---------------------------------------------------------------------------
 // Chain + workers (FAST, narrow runs): one cooperative launch over the whole
@@ -1510,108 +1226,6 @@ __device__ __forceinline__ double warp_row_dot_exact(int k0, int k1, const int* 
     return __shfl_sync(0xffffffffu, s, 0);
 }
 
-// U apply: t[r] = diag*x[cp[r]] + sum_{c>r} U_rc x[cp[c]]  (diagonal first)
-__global__ void __launch_bounds__(256)
-    k_apply_u2(const int* __restrict__ uptr, const int* __restrict__ ucol,
-               const double* __restrict__ uval, const double* __restrict__ udiag, int n,
-               const int* __restrict__ col_perm, const double* __restrict__ x,
-               double* __restrict__ t, const Ctrl* ctrl, const double* __restrict__ vbase,
-               long long ldv) {
-    __shared__ double s_prod[8][32];
-    const double* xs = x;
-    if (ctrl) {
-        if (!ctrl->need_weight || ctrl->converged || ctrl->status) return;
-        xs = vbase + (long long)ctrl->m * ldv;
-    }
-    const int lane = threadIdx.x & 31;
-    const int r0 = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32;
-    if (r0 >= n) return;
-    const int r = r0 + lane;
-    const int len = r < n ? uptr[r + 1] - uptr[r] : 0;
-    unsigned long_mask = __ballot_sync(0xffffffffu, len > kLongRow);
-    auto xfn = [&](int c) { return xs[col_perm[c]]; };
-    double mine = 0.0;
-    while (long_mask) {
-        const int q = __ffs(long_mask) - 1;
-        long_mask &= long_mask - 1;
-        const int rq = r0 + q;
-        double s = 0.0;
-        s += udiag[rq] * xs[col_perm[rq]];
-        s = warp_row_dot_exact(uptr[rq], uptr[rq + 1], ucol, uval, xfn, s, s_prod[threadIdx.x >> 5]);
-        if (lane == q) mine = s;
-    }
-    if (r < n) {
-        if (len <= kLongRow) {
-            double s = 0.0;
-            s += udiag[r] * xs[col_perm[r]];
-            for (int k = uptr[r]; k < uptr[r + 1]; ++k) s += uval[k] * xs[col_perm[ucol[k]]];
-            mine = s;
-        }
-        t[r] = mine;
-    }
-}
-
-// L apply + ||y||^2: y[r] = sum_{c<r} L_rc t[c] + 1.0*t[r]  (diagonal last)
-__global__ void __launch_bounds__(256)
-    k_apply_l2(const int* __restrict__ lptr, const int* __restrict__ lcol,
-               const double* __restrict__ lval, int n, const double* __restrict__ t,
-               double* __restrict__ y_out, const int* __restrict__ row_perm,
-               double* __restrict__ partials, unsigned int* __restrict__ done_counter, Ctrl* ctrl,
-               double* __restrict__ weight_out) {
-    __shared__ double sh[33];
-    __shared__ bool s_last;
-    __shared__ double s_prod[8][32];
-    if (ctrl && (!ctrl->need_weight || ctrl->converged || ctrl->status)) return;
-    const int lane = threadIdx.x & 31;
-    const int r0 = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32;
-    const int r = r0 + lane;
-    double sq = 0.0;
-    if (r0 < n) {
-        const int len = r < n ? lptr[r + 1] - lptr[r] : 0;
-        unsigned long_mask = __ballot_sync(0xffffffffu, len > kLongRow);
-        auto xfn = [&](int c) { return t[c]; };
-        double mine = 0.0;
-        while (long_mask) {
-            const int q = __ffs(long_mask) - 1;
-            long_mask &= long_mask - 1;
-            const int rq = r0 + q;
-            double s = warp_row_dot_exact(lptr[rq], lptr[rq + 1], lcol, lval, xfn, 0.0, s_prod[threadIdx.x >> 5]);
-            s += 1.0 * t[rq];
-            if (lane == q) mine = s;
-        }
-        if (r < n) {
-            if (len <= kLongRow) {
-                double s = 0.0;
-                for (int k = lptr[r]; k < lptr[r + 1]; ++k) s += lval[k] * t[lcol[k]];
-                s += 1.0 * t[r];
-                mine = s;
-            }
-            if (y_out) y_out[row_perm[r]] = mine;
-            sq = mine * mine;
-        }
-    }
-    const double bs = block_sum(sq, sh);
-    if (threadIdx.x == 0) {
-        partials[blockIdx.x] = bs;
-        __threadfence();
-        const unsigned int prev = atomicAdd(done_counter, 1u);
-        s_last = (prev == gridDim.x - 1);
-    }
-    __syncthreads();
-    if (!s_last) return;
-    double acc = 0.0;
-    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) acc += ld_cg(partials + b);
-    const double tot = block_sum(acc, sh);
-    if (threadIdx.x == 0) {
-        *done_counter = 0u;
-        const double w = sqrt(tot);
-        if (weight_out) *weight_out = w;
-        if (ctrl) {
-            ctrl->weight = w;
-            decide(ctrl);
-        }
-    }
-}
 
 // ---------------------------------------------------------------------------
 // Factor apply over the EXACT warp-task lists (no dependencies: any order).
@@ -1691,76 +1305,6 @@ __global__ void __launch_bounds__(256)
     double a2 = 0.0;
     for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) a2 += ld_cg(partials + b);
     const double tot = block_sum(a2, sh);
-    if (threadIdx.x == 0) {
-        *done_counter = 0u;
-        const double w = sqrt(tot);
-        if (weight_out) *weight_out = w;
-        if (ctrl) {
-            ctrl->weight = w;
-            decide(ctrl);
-        }
-    }
-}
-
-// ============================================================================
-// Factor apply y = P^T L U Q^T x (sparse_lu.cpp:293-304), row-sequential.
-// apply_u: t[r] = diag*x[cp[r]] + sum_{c>r} U_rc x[cp[c]]  (diagonal first)
-// apply_l: y[r] = sum_{c<r} L_rc t[c] + 1.0*t[r]          (diagonal last)
-// apply_l also reduces ||y||^2 (the residual weight, krylov.cpp:238) and,
-// when ctrl is set, takes the Arnoldi convergence decision in its last block.
-// ============================================================================
-__global__ void __launch_bounds__(kSpmvWarps * 32)
-    k_apply_u_diag(const int* __restrict__ uptr, const int* __restrict__ ucol,
-                   const double* __restrict__ uval, const double* __restrict__ udiag, int n,
-                   const int* __restrict__ col_perm, const double* __restrict__ x,
-                   double* __restrict__ t, const Ctrl* ctrl, const double* __restrict__ vbase,
-                   long long ldv) {
-    const double* xs = x;
-    if (ctrl) {
-        if (!ctrl->need_weight || ctrl->converged || ctrl->status) return;
-        xs = vbase + (long long)ctrl->m * ldv;
-    }
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= n) return;
-    double s = 0.0;
-    s += udiag[r] * xs[col_perm[r]];
-    for (int k = uptr[r]; k < uptr[r + 1]; ++k) s += uval[k] * xs[col_perm[ucol[k]]];
-    t[r] = s;
-}
-
-__device__ void decide(Ctrl* c);
-
-__global__ void __launch_bounds__(256)
-    k_apply_l_norm(const int* __restrict__ lptr, const int* __restrict__ lcol,
-                   const double* __restrict__ lval, int n, const double* __restrict__ t,
-                   double* __restrict__ y_out, const int* __restrict__ row_perm,
-                   double* __restrict__ partials, unsigned int* __restrict__ done_counter,
-                   Ctrl* ctrl, double* __restrict__ weight_out) {
-    __shared__ double sh[33];
-    __shared__ bool s_last;
-    if (ctrl && (!ctrl->need_weight || ctrl->converged || ctrl->status)) return;
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    double sq = 0.0;
-    if (r < n) {
-        double s = 0.0;
-        for (int k = lptr[r]; k < lptr[r + 1]; ++k) s += lval[k] * t[lcol[k]];
-        s += 1.0 * t[r];
-        if (y_out) y_out[row_perm[r]] = s;
-        sq = s * s;
-    }
-    const double bs = block_sum(sq, sh);
-    if (threadIdx.x == 0) {
-        partials[blockIdx.x] = bs;
-        __threadfence();
-        const unsigned int prev = atomicAdd(done_counter, 1u);
-        s_last = (prev == gridDim.x - 1);
-    }
-    __syncthreads();
-    if (!s_last) return;
-    // last block: fixed-order final sum of the block partials
-    double acc = 0.0;
-    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) acc += ld_cg(partials + b);
-    const double tot = block_sum(acc, sh);
     if (threadIdx.x == 0) {
         *done_counter = 0u;
         const double w = sqrt(tot);
@@ -2546,26 +2090,26 @@ __global__ void __launch_bounds__(256)
 }
 
 // ||v||_inf (exact: max is order independent), two-stage, and elementwise ops
-// of the nonlinear error / correction (integrate.cpp:267-298)
+// of the nonlinear error / correction (integrate.cpp:267-298).  The max
+// propagates NaN (a NaN operand wins), so a non-finite vector never reads as
+// a finite norm: the caller maps it to EXG_E_NONFINITE like residual_F's
+// all_finite check (devices.cpp:205).
+__device__ __forceinline__ double nanmax(double m, double a) { return (a > m || a != a) && m == m ? a : m; }
+
 __global__ void __launch_bounds__(256)
     k_absmax(const double* __restrict__ v, int n, double* __restrict__ partials,
              unsigned int* done, double* out) {
     __shared__ double sh[32];
     __shared__ bool s_last;
     double m = 0.0;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const double a = fabs(v[i]);
-        m = m < a ? a : m;
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-        const double t = __shfl_down_sync(0xffffffffu, m, o);
-        m = m < t ? t : m;
-    }
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        m = nanmax(m, fabs(v[i]));
+    for (int o = 16; o > 0; o >>= 1) m = nanmax(m, __shfl_down_sync(0xffffffffu, m, o));
     if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = m;
     __syncthreads();
     if (threadIdx.x == 0) {
         double b = 0.0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) b = b < sh[w] ? sh[w] : b;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) b = nanmax(b, sh[w]);
         partials[blockIdx.x] = b;
         __threadfence();
         s_last = atomicAdd(done, 1u) == gridDim.x - 1;
@@ -2573,10 +2117,7 @@ __global__ void __launch_bounds__(256)
     __syncthreads();
     if (!s_last || threadIdx.x) return;
     double b = 0.0;
-    for (int k = 0; k < (int)gridDim.x; ++k) {
-        const double t = ld_cg(partials + k);
-        b = b < t ? t : b;
-    }
+    for (int k = 0; k < (int)gridDim.x; ++k) b = nanmax(b, ld_cg(partials + k));
     *out = b;
     *done = 0u;
 }
@@ -2652,43 +2193,20 @@ static int trsv2_occ() {
 }
 
 void trsv(const Launch& L, bool upper, bool reverse, const TrsvArgs& a) {
-    if (a.n <= 0) return;
-    if (a.tasks) {
-        static int occ[4] = {0, 0, 0, 0};
-        const int id = (upper ? 2 : 0) + (reverse ? 1 : 0);
-        if (!occ[id])
-            occ[id] = id == 0 ? trsv2_occ<false, false>() : id == 1 ? trsv2_occ<false, true>()
-                    : id == 2 ? trsv2_occ<true, false>() : trsv2_occ<true, true>();
-        const long long warps_needed = a.n_tasks;
-        const unsigned int grid = (unsigned int)std::max<long long>(
-            1, std::min<long long>((long long)L.num_sms * occ[id], (warps_needed + 7) / 8));
-        if (!upper && !reverse) k_trsv2<false, false><<<grid, 256, 0, L.stream>>>(a);
-        else if (!upper) k_trsv2<false, true><<<grid, 256, 0, L.stream>>>(a);
-        else if (!reverse) k_trsv2<true, false><<<grid, 256, 0, L.stream>>>(a);
-        else k_trsv2<true, true><<<grid, 256, 0, L.stream>>>(a);
-        count(L);
-        return;
-    }
-    const unsigned int grid = cdiv(a.n, kTrsvThreads);
-    if (!upper)
-        k_trsv<false, false><<<grid, kTrsvThreads, 0, L.stream>>>(a);
-    else if (!reverse)
-        k_trsv<true, false><<<grid, kTrsvThreads, 0, L.stream>>>(a);
-    else
-        k_trsv<true, true><<<grid, kTrsvThreads, 0, L.stream>>>(a);
+    if (a.n <= 0 || a.n_tasks <= 0) return;
+    static int occ[4] = {0, 0, 0, 0};
+    const int id = (upper ? 2 : 0) + (reverse ? 1 : 0);
+    if (!occ[id])
+        occ[id] = id == 0 ? trsv2_occ<false, false>() : id == 1 ? trsv2_occ<false, true>()
+                : id == 2 ? trsv2_occ<true, false>() : trsv2_occ<true, true>();
+    const long long warps_needed = a.n_tasks;
+    const unsigned int grid = (unsigned int)std::max<long long>(
+        1, std::min<long long>((long long)L.num_sms * occ[id], (warps_needed + 7) / 8));
+    if (!upper && !reverse) k_trsv2<false, false><<<grid, 256, 0, L.stream>>>(a);
+    else if (!upper) k_trsv2<false, true><<<grid, 256, 0, L.stream>>>(a);
+    else if (!reverse) k_trsv2<true, false><<<grid, 256, 0, L.stream>>>(a);
+    else k_trsv2<true, true><<<grid, 256, 0, L.stream>>>(a);
     count(L);
-}
-
-void apply_weight(const Launch& L, const int* uptr, const int* ucol, const double* uval,
-                  const double* udiag, const int* lptr, const int* lcol, const double* lval, int n,
-                  const int* col_perm, const int* row_perm, const double* x, double* t,
-                  double* y_out, double* partials, unsigned int* done, Ctrl* ctrl,
-                  const double* vbase, long long ldv, double* weight_out) {
-    k_apply_u2<<<cdiv(n, 256), 256, 0, L.stream>>>(uptr, ucol, uval, udiag, n, col_perm, x, t,
-                                                  ctrl, vbase, ldv);
-    k_apply_l2<<<cdiv(n, 256), 256, 0, L.stream>>>(lptr, lcol, lval, n, t, y_out, row_perm,
-                                                  partials, done, ctrl, weight_out);
-    count(L, 2);
 }
 
 template <bool U>
@@ -2696,33 +2214,6 @@ static int trsv3_occ() {
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_trsv3<U>, 256, 0);
     return occ > 0 ? occ : 1;
-}
-
-void trsv_blk(const Launch& L, bool upper, const NarrowArgs& a, int cluster, size_t smem) {
-    static bool attr[2] = {false, false};
-    auto fn = upper ? (void*)k_trsv_blk<true> : (void*)k_trsv_blk<false>;
-    if (!attr[upper]) {
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-        cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        attr[upper] = true;
-    }
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(cluster);
-    cfg.blockDim = dim3(256);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = L.stream;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = cluster;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    if (upper)
-        cudaLaunchKernelEx(&cfg, k_trsv_blk<true>, a);
-    else
-        cudaLaunchKernelEx(&cfg, k_trsv_blk<false>, a);
-    count(L);
 }
 
 cudaError_t trsv_chain(const Launch& L, bool upper, const ChainArgs& a) {
@@ -2742,8 +2233,9 @@ cudaError_t trsv_chain(const Launch& L, bool upper, const ChainArgs& a) {
     at[1].val.cooperative = 1;
     cfg.attrs = at;
     if (!attr[upper]) {
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kChainSmem);
-        cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaError_t ea = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kChainSmem);
+        if (ea == cudaSuccess) ea = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (ea != cudaSuccess) return ea;
         // how many kCC-CTA clusters fit at once (not every GPC holds a
         // multiple of kCC SMs)
         cfg.gridDim = dim3(kCC * (unsigned)L.num_sms);
@@ -2753,6 +2245,7 @@ cudaError_t trsv_chain(const Launch& L, bool upper, const ChainArgs& a) {
             cudaOccupancyMaxActiveClusters(&mc, k_trsv_chain<true>, &cfg);
         else
             cudaOccupancyMaxActiveClusters(&mc, k_trsv_chain<false>, &cfg);
+        if (mc < 2) return cudaErrorLaunchOutOfResources;  // chain + at least one worker cluster
         max_clusters[upper] = mc > 1 ? mc : 2;
         attr[upper] = true;
     }
@@ -2774,45 +2267,43 @@ cudaError_t trsv_chain(const Launch& L, bool upper, const ChainArgs& a) {
     return e;
 }
 
-void trsv_wide(const Launch& L, bool upper, const TrsvArgs& a) {
-    if (a.n_tasks <= 0) return;
-    static int occ[2] = {0, 0};
-    if (!occ[upper]) occ[upper] = upper ? trsv3_occ<true>() : trsv3_occ<false>();
-    const long long warps = (long long)L.num_sms * occ[upper] * 8;
-    const unsigned int grid = (unsigned int)std::max<long long>(
-        1, std::min<long long>((long long)L.num_sms * occ[upper], ((long long)a.n_tasks + 7) / 8));
-    (void)warps;
-    void* args[] = {(void*)&a};
-    cudaLaunchCooperativeKernel(upper ? (void*)k_trsv3<true> : (void*)k_trsv3<false>, dim3(grid),
-                                dim3(256), args, 0, L.stream);
+cudaError_t trsv_sub(const Launch& L, bool upper, const SubArgs& a) {
+    if (a.n_comps <= 0) return cudaSuccess;
+    static size_t attr_bytes[2] = {0, 0};
+    const size_t smem = (size_t)a.max_rows * (sizeof(double) + sizeof(int4)) + (size_t)a.max_tasks * sizeof(int2) +
+                        (size_t)(a.max_levels + 1) * sizeof(int);
+    auto fn = upper ? (const void*)k_trsv_sub<true> : (const void*)k_trsv_sub<false>;
+    if (smem > 48 * 1024 && attr_bytes[upper] < smem) {
+        const cudaError_t ea = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (ea != cudaSuccess) return ea;
+        attr_bytes[upper] = smem;
+    }
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, smem);
+    if (occ < 1) return cudaErrorLaunchOutOfResources;
+    const unsigned int grid = (unsigned int)std::min<long long>(a.n_comps, (long long)L.num_sms * occ);
+    if (upper)
+        k_trsv_sub<true><<<grid, 256, smem, L.stream>>>(a);
+    else
+        k_trsv_sub<false><<<grid, 256, smem, L.stream>>>(a);
     count(L);
+    return cudaGetLastError();
 }
 
-void trsv_narrow(const Launch& L, bool upper, const NarrowArgs& a, int cluster, size_t smem) {
-    static bool attr[2] = {false, false};
-    auto fn = upper ? (void*)k_trsv_narrow<true> : (void*)k_trsv_narrow<false>;
-    if (!attr[upper]) {
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        attr[upper] = true;
-    }
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(cluster);
-    cfg.blockDim = dim3(EXG_NARROW_THREADS);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = L.stream;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = cluster;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    if (upper)
-        cudaLaunchKernelEx(&cfg, k_trsv_narrow<true>, a);
-    else
-        cudaLaunchKernelEx(&cfg, k_trsv_narrow<false>, a);
+cudaError_t trsv_wide(const Launch& L, bool upper, const TrsvArgs& a) {
+    if (a.n_tasks <= 0) return cudaSuccess;
+    static int occ[2] = {0, 0};
+    if (!occ[upper]) occ[upper] = upper ? trsv3_occ<true>() : trsv3_occ<false>();
+    const unsigned int grid = (unsigned int)std::max<long long>(
+        1, std::min<long long>((long long)L.num_sms * occ[upper], ((long long)a.n_tasks + 7) / 8));
+    void* args[] = {(void*)&a};
+    // cooperative: every warp task's producers are resident (the sync-free
+    // hand-offs spin on them); a refused launch must not leave later kernels
+    // waiting on sentinels, so the status goes back to the caller
+    const cudaError_t e = cudaLaunchCooperativeKernel(upper ? (void*)k_trsv3<true> : (void*)k_trsv3<false>,
+                                                      dim3(grid), dim3(256), args, 0, L.stream);
     count(L);
+    return e;
 }
 
 void apply_tasks(const Launch& L, const int2* utasks, int n_utasks, const int* uorder,

@@ -77,6 +77,29 @@ def test_solve_fast_close(case, ref):
     assert np.max(np.abs(got - want)) <= 1e-13 * np.max(np.abs(want))
 
 
+@pytest.mark.parametrize("budget", [0, 16, 256, 4096])
+@pytest.mark.parametrize("cfg,kw", [(1, dict(width=64)), (1, dict(width=160)), (2, dict(width=24)),
+                                    (3, dict(n=3000))], ids=["c1-64", "c1-160", "c2-24", "c3-3000"])
+def test_solve_fast_subtree_budgets(ref, monkeypatch, cfg, kw, budget):
+    """FAST plan with the subtree phase of k_trsv_sub at several component
+    budgets (EXG_SUB_ROWS; 0 disables it): the mixed plans (components +
+    wide runs + chain) stay within the FAST bar, in both triangles."""
+    monkeypatch.setenv("EXG_SUB_ROWS", str(budget))
+    s = ex.System.generate(cfg, **kw)
+    f = ex.lu_factor(s.G)
+    fh = ref.factor_from(f)
+    try:
+        rng = np.random.default_rng(11)
+        with _ctx(s, f, F.EXG_TRSV_FAST) as c:
+            for _ in range(2):
+                b = rng.uniform(-1, 1, s.n)
+                got = c.solve(b)
+                want = ref.solve(fh, b)
+                assert np.max(np.abs(got - want)) <= 1e-13 * np.max(np.abs(want))
+    finally:
+        ref.factor_free(fh)
+
+
 def test_apply_bit_identical(case, ref):
     _, s, f, fh = case
     x = np.random.default_rng(4).uniform(-1, 1, s.n)

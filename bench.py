@@ -215,22 +215,45 @@ def setup_system(args):
                   **({"lu_from_cache": True} if cached else {})}
 
 
-def cpu_reference_steps(s, f, x0, ctl, t_stop, n_steps):
+def bench_probes(s, k=16, seed=9):
+    """The 16 seeded probe nodes (the same recipe as tools/make_golden.py)."""
+    rng = np.random.default_rng(seed)
+    return np.sort(rng.choice(s.n_nodes, size=min(k, s.n_nodes), replace=False)).astype(np.int32)
+
+
+def ref_system(ref, s):
+    """The reference's own MnaSystem: build_mna (mna.cpp:22-165) from the
+    element list wherever the config is element-defined (config 3 is
+    matrix-defined: CSR hand-over)."""
+    el, src, pt, pv, mo = s.elements()
+    if len(el):
+        return ref.system_from_elements(el, src, pt, pv, mo, s.options())
+    return ref.system_from_csr(s.n, s.G, s.C, s.B, src, pt, pv, s.options())
+
+
+def cpu_reference_steps(s, f, x0, ctl, t_stop, n_steps, rec):
     """The reference (oracle/_ref: unmodified exsim_core) restated ER loop with
-    the (bit-identical) cached factorization; returns per-step wall times."""
+    the (bit-identical) cached factorization; per-step wall times, Krylov
+    dimensions and the probed waveform."""
     sys.path.insert(0, str(ROOT / "oracle"))
-    from helpers_bench import ref_system_for  # noqa: E402
     from ref import Ref  # noqa: E402
     ref = Ref()
-    rh = ref_system_for(ref, s)
+    rh = ref_system(ref, s)
     fh = ref.factor_from(f)
     try:
-        r = ref.transient_cached(rh, fh, ctl, t_stop, np.zeros(1, np.int32), max_steps=n_steps, x0=x0)
+        r = ref.transient_cached(rh, fh, ctl, t_stop, rec, max_steps=n_steps, x0=x0)
     finally:
         ref.factor_free(fh)
         ref.system_free(rh)
-    dims = r["dims"]
-    return r["wall"], dims
+    return r["wall"], r["dims"], r["samples"]
+
+
+def shared_config(args, s, f, world):
+    """The workload description both arms print (same_config)."""
+    return {"workload": workload_name(args.config, args.width), "n": s.n, "nnz_C": s.C.nnz,
+            "nnz_G": s.G.nnz, "nnz_LU": int(f.fill_nnz), "n_inputs": s.n_inputs,
+            "steps_from": "DC point, the reference's step-size sequence", "parallelism": f"replicas{world}",
+            "l2": l2_note(12.0 * float(f.fill_nnz))}
 
 
 def dc_point(ctx, s):
@@ -302,9 +325,11 @@ def run_ours(args, rank, world, local):
     # the state is restored so the timed region runs exactly those steps again
     x_w = np.zeros(n)
     ctx._check(lib.exg_memcpy(h, x_w.ctypes.data, dx, 8 * n, 2))
+    c_prof0 = ctx.counters()
     lib.exg_profile_enable(h, 1)
     for i in range(args.warmup, min(args.warmup + args.profile_steps, nsteps)):
         dev_step(i)
+    c_prof1 = ctx.counters()
     kt = F.exg_kernel_times()
     ctx._check(lib.exg_profile_get(h, C.byref(kt)))
     lib.exg_profile_enable(h, 0)
@@ -337,18 +362,28 @@ def run_ours(args, rank, world, local):
     bytes_l = 12 * nnz_l + 4 * (n + 1) + 4 * n + 4 * n + 8 * n + 8 * n
     bytes_u = 12 * nnz_u + 8 * n + 4 * (n + 1) + 4 * n + 8 * n + 8 * n + 4 * n + 8 * n
     bytes_spmv = 12 * Cm.nnz + 4 * (n + 1) + 8 * n + 8 * n
+    G = s.G
+    mgs_passes = c_prof1.mgs_passes - c_prof0.mgs_passes
+    mgs_launches = ktimes.get("mgs", {}).get("launches", 0)
+    # algorithmic bytes per launch; MGS: 8n(J+2) with J basis
+    # vectors (+ 8n(J+1) per reorthogonalisation), counted on the device; the
+    # G-weight: one SpMV of G plus the norm of its output
     alg = {"trsv_l": bytes_l, "trsv_u": bytes_u, "spmv": bytes_spmv,
-           "mgs": None, "dense": None, "weight": None}
+           "mgs": (8.0 * n * mgs_passes / mgs_launches) if mgs_launches else None,
+           "weight": 12 * G.nnz + 4 * (n + 1) + 8 * n if args.weight == "gspmv" else None}
     dom = max(ktimes, key=lambda k: ktimes[k]["ms"]) if ktimes else "trsv_u"
     peak, peak_kind = hbm_peak()
     roof = {}
-    for k in ("trsv_l", "trsv_u", "spmv"):
-        if k in ktimes and ktimes[k]["launches"]:
+    for k in ("trsv_l", "trsv_u", "spmv", "mgs", "weight"):
+        if k in ktimes and ktimes[k]["launches"] and alg.get(k):
             per = ktimes[k]["ms"] / ktimes[k]["launches"] / 1e3
             ach = alg[k] / per / 1e9
             roof[k] = {"achieved": round(ach, 1), "frac": round(ach / peak, 4),
-                       "ms_per_launch": round(per * 1e3, 4), "bytes_per_launch": alg[k]}
-    dom_roof = dom if dom in roof else "trsv_u" if "trsv_u" in roof else next(iter(roof), None)
+                       "ms_per_launch": round(per * 1e3, 4), "bytes_per_launch": int(alg[k])}
+    if "dense" in ktimes and ktimes["dense"]["launches"]:
+        # the m x m block is latency-bound (single CTA, m <= MMAX): time only
+        roof["dense"] = {"bound": "latency", "ms_per_launch": round(ktimes["dense"]["ms"] / ktimes["dense"]["launches"], 4)}
+    dom_roof = dom if "achieved" in roof.get(dom, {}) else "trsv_u" if "trsv_u" in roof else None
     traffic = None
     tf = ROOT / "profiles" / "traffic_config1.json"
     if tf.exists():
@@ -374,6 +409,8 @@ def run_ours(args, rank, world, local):
     xh_t.numpy()[:] = x_w
     e2e_steps = args.steps
     e2e_m = []
+    rec = bench_probes(s)
+    e2e_probe = []
     ctx.synchronize()
     barrier(world)
     t0 = time.perf_counter()
@@ -386,6 +423,7 @@ def run_ours(args, rank, world, local):
                                    C.c_void_p(uk1_t.data_ptr()), hh, C.byref(cfg),
                                    C.c_void_p(xn_t.data_ptr()), C.byref(m), F.EXG_PTR_HOST))
         e2e_m.append(m.value)
+        e2e_probe.append(xn_t.numpy()[rec].copy())
         xh_t, xn_t = xn_t, xh_t
     ctx.synchronize()
     e2e_s = allmax(world, time.perf_counter() - t0)
@@ -394,34 +432,41 @@ def run_ours(args, rank, world, local):
     if e2e_m != m_seq:
         raise SystemExit(f"e2e Krylov dimensions {e2e_m} differ from the timed region's {m_seq}")
 
-    # ---- CPU baseline (rank 0, N = 1): the reference on a bounded sample
-    cpu = None
+    # ---- CPU baseline (rank 0, N = 1): the reference on a bounded sample,
+    # which doubles as the headline's own parity evidence: the same steps'
+    # Krylov dimensions and probed states against the e2e run
+    cpu, parity = None, None
     if rank == 0 and world == 1 and args.cpu_steps > 0:
-        # the same steps as the timed region's first cpu_steps (the reference
-        # runs from the DC point through the warm-up steps; only the sampled
-        # steps are timed)
-        wall, dims = cpu_reference_steps(s, f, x0, ctl, t_stop, args.warmup + args.cpu_steps)
+        k = min(args.cpu_steps, args.steps)
+        wall, dims, samples = cpu_reference_steps(s, f, x0, ctl, t_stop, args.warmup + k, rec)
         per = np.diff(np.concatenate([[0.0], wall]))[args.warmup:]
         cpu = {"value": round(len(per) / float(np.sum(per)), 5), "unit": "steps/s", "cores": 1,
                "kind": "reference",
-               "sample": f"ER steps {args.warmup}..{args.warmup + len(per) - 1} of config 1 (the first "
+               "sample": f"ER steps {args.warmup}..{args.warmup + len(per) - 1} of config {args.config} (the first "
                          f"{len(per)} timed steps), unmodified exsim_core (oracle/_ref) restated loop "
                          f"with the cached bit-identical factorization, 1 thread; per-step s "
-                         f"{[round(x, 2) for x in per]}, m {dims.tolist()[args.warmup:]}"}
+                         f"{[round(float(x), 2) for x in per]}"}
+        want = samples[args.warmup + 1: args.warmup + 1 + k]
+        got = np.array(e2e_probe[:k])
+        scale = np.maximum(np.abs(want).max(axis=0), 1e-300)
+        fs_err = float((np.abs(got - want).max(axis=0) / scale).max())
+        m_ref = [int(x) for x in dims.tolist()[args.warmup:args.warmup + k]]
+        parity = {"steps_compared": k, "krylov_dims_equal": m_ref == m_seq[:k], "m_reference": m_ref,
+                  "probe_full_scale_err": fs_err, "tol": 1e-8, "probes": int(rec.size),
+                  "ok": bool(m_ref == m_seq[:k] and fs_err <= 1e-8)}
+        if not parity["ok"]:
+            print(json.dumps({"parity_failure": parity}), file=sys.stderr, flush=True)
 
     res = {
         "metric": METRIC, "value": round(value, 4), "unit": "steps/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic (seeded config-{args.config} generator, DESIGN.md §8)",
-        "config": {"workload": workload_name(args.config, args.width), "n": n,
-                   "nnz_C": s.C.nnz, "nnz_G": s.G.nnz, "nnz_LU": int(f.fill_nnz),
-                   "n_inputs": ni, "trsv_mode": args.trsv, "weight_mode": args.weight, "loop": args.loop,
-                   "parallelism": f"replicas{world}",
-                   "l2": l2_note(12.0 * float(f.fill_nnz))},
+        "config": shared_config(args, s, f, world),
+        "modes": {"trsv": args.trsv, "weight": args.weight, "loop": args.loop},
         "arnoldi_iters_per_s": round(allsum(world, float(iters)) / (ms_max / 1e3), 3),
         "m_per_step": m_seq, "gpu_launches": int(launches),
-        "roofline": roofline, "cpu_baseline": cpu,
+        "roofline": roofline, "cpu_baseline": cpu, "parity": parity,
         "e2e": {"value": round(e2e_val, 4), "unit": "steps/s",
                 "h2d_bytes_per_step": 8 * n + 16 * ni, "d2h_bytes_per_step": 8 * n,
                 "steps": e2e_steps, "api": "exg_er_step(pinned host buffers), same steps as the timed region"},
@@ -432,11 +477,18 @@ def run_ours(args, rank, world, local):
 
 
 def run_reference(args, rank, world):
-    """The reference arm: the unmodified reference (oracle/_ref) CPU path."""
+    """The reference arm: the unmodified reference (oracle/_ref: exsim_core
+    compiled from /root/reference) on the host cores, same workload and metric.
+
+    No product library is mapped in this process: the inputs come from the
+    host-side generator and setup LU compiled without CUDA into
+    oracle/_build/libsetup.so (EXG_LIB, set in main() before any import), the
+    system is assembled by the reference's own build_mna, and everything timed
+    is the reference's code (the restated transient() loop over its public API
+    with the cached factorization, which tests/golden/lu_hash_c1.json pins to
+    its own lu_factor at 1M)."""
     if rank != 0:
         return
-    import paper_1511_04515_b200 as ex
-    from paper_1511_04515_b200 import _ffi as F
     sys.path.insert(0, str(ROOT / "oracle"))
     from ref import Ref
     s, f, setup = setup_system(args)
@@ -446,11 +498,12 @@ def run_reference(args, rank, world):
         ctl.h_init = 1e-12
     t_stop = s.options().tran_stop
     ref = Ref()
-    from helpers_bench import ref_system_for
-    rh = ref_system_for(ref, s)
+    t0 = time.perf_counter()
+    rh = ref_system(ref, s)
+    setup["ref_build_mna_s"] = round(time.perf_counter() - t0, 2)
     fh = ref.factor_from(f)
     # DC point: dc_solve's linear branch = lu_factor(G) + solve(B u0)
-    # (integrate.cpp:70-75); the factor is the bit-identical one
+    # (integrate.cpp:70-75) with the cached factorization
     u0 = s.eval_sources(0.0)
     x0 = ref.solve(fh, ref.spmv(s.B, u0))
     n_total = args.warmup + args.steps
@@ -466,14 +519,16 @@ def run_reference(args, rank, world):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(timed / args.steps * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic (seeded config-{args.config} generator, DESIGN.md §8)", "impl": "reference",
-        "config": {"workload": workload_name(args.config, args.width), "n": s.n},
+        "config": shared_config(args, s, f, world),
         "cpu_baseline": {"value": round(value, 6), "unit": "steps/s", "cores": 1, "kind": "reference",
-                         "sample": f"steps {args.warmup}..{n_total - 1} of the config-1 transient, "
-                                   "unmodified exsim_core restated ER loop (cached factorization "
-                                   "from the bit-identical host LU), 1 thread"},
+                         "sample": f"steps {args.warmup}..{n_total - 1} of the config-{args.config} transient, "
+                                   "unmodified exsim_core restated ER loop (cached factorization), "
+                                   "1 thread (the reference is single-threaded)"},
         "e2e": {"value": round(value, 6), "unit": "steps/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
-        "setup": setup, "m_per_step": r["dims"].tolist(),
+        "setup": setup,
+        "m_per_step": [int(x) for x in r["dims"][r["dims_off"][args.warmup]:r["dims_off"][n_total]].tolist()],
+        "libraries": "oracle/_ref/libexsim_ref.so (timed), oracle/_build/libsetup.so (inputs, untimed)",
     }
     print(json.dumps(res), flush=True)
 
@@ -495,6 +550,11 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=4)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        # the reference arm maps no product library: the package's host API
+        # binds the CUDA-free setup library built by oracle/Makefile
+        os.environ["EXG_LIB"] = str(ROOT / "oracle" / "_build" / "libsetup.so")
+        os.environ["EXG_HOST_ONLY"] = "1"
     rank, world, local = dist_setup()
     if args.impl == "reference":
         run_reference(args, rank, world)

@@ -106,6 +106,9 @@ typedef struct exg_counters {
     int64_t graph_builds;    /* graph captures + instantiations */
     int32_t l_schedule;      /* level schedule of L: 0 ASAP, 1 ALAP */
     int32_t u_schedule;      /* of U */
+    int64_t mgs_passes;      /* algorithmic n-vector passes of orthogonalize: J + 2 per call
+                                with J basis vectors, + J + 1 per reorthogonalisation */
+    int64_t reorths;         /* reorthogonalisation passes (krylov.cpp:59) */
 } exg_counters;
 
 exg_status exg_create(int device, exg_ctx** out);

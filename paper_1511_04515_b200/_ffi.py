@@ -96,7 +96,8 @@ class exg_counters(C.Structure):
                 ("mevp_calls", C.c_int64), ("trsv_calls", C.c_int64), ("l_levels", C.c_int32),
                 ("u_levels", C.c_int32), ("nnz_l", C.c_int64), ("nnz_u", C.c_int64),
                 ("graph_launches", C.c_int64), ("graph_builds", C.c_int64),
-                ("l_schedule", C.c_int32), ("u_schedule", C.c_int32)]
+                ("l_schedule", C.c_int32), ("u_schedule", C.c_int32), ("mgs_passes", C.c_int64),
+                ("reorths", C.c_int64)]
 
 
 class exg_kernel_times(C.Structure):

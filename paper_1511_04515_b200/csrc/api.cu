@@ -388,7 +388,7 @@ void mevp_dev(exg_ctx* c, const double* v, double h, const exg_mevp_cfg& cfg, in
         c->prof_end(EXG_K_SPMV, p0);
         solve_dev(c, c->t, c->w, -1.0, nullptr, c->ctrl);
         cudaEvent_t p1 = c->prof_begin();
-        exg::dev::mgs(L, ma, blocks, K);
+        ck(exg::dev::mgs(L, ma, blocks, K), "mgs launch");
         c->prof_end(EXG_K_MGS, p1);
         cudaEvent_t p2 = c->prof_begin();
         exg::dev::dense(L, da, dense_m);
@@ -466,6 +466,8 @@ void mevp_dev(exg_ctx* c, const double* v, double h, const exg_mevp_cfg& cfg, in
             sync_ctrl(c);
             c->cnt.arnoldi_iters += hc.arnoldi_iters;
             c->launches += g->body_kernels * hc.arnoldi_iters;
+            c->cnt.mgs_passes += hc.mgs_passes;
+            c->cnt.reorths += hc.reorths;
         } else {
             for (int jj = 0; jj < cfg.m_max; ++jj) {
                 iteration(jj + 1, 0);
@@ -473,6 +475,8 @@ void mevp_dev(exg_ctx* c, const double* v, double h, const exg_mevp_cfg& cfg, in
                 sync_ctrl(c);
                 if (hc.status || hc.converged) break;
             }
+            c->cnt.mgs_passes += hc.mgs_passes;
+            c->cnt.reorths += hc.reorths;
         }
     }
     ctrl_status(c);
@@ -1008,7 +1012,8 @@ void exg_destroy(exg_ctx* c) {
         if (p) cudaFree(p);
     double* dp[] = {c->l_val, c->u_val, c->u_diag, c->vin, c->vout, c->t, c->w, c->xk, c->xnext,
                     c->gb, c->startv, c->v1, c->t1, c->t2, c->t3, c->tmp, c->u_k, c->u_k1, c->V,
-                    c->hbar, c->hinv, c->coef, c->dscratch, c->partials, c->weight, c->probe_out};
+                    c->hbar, c->hinv, c->coef, c->dscratch, c->partials, c->weight, c->probe_out,
+};
     for (double* p : dp)
         if (p) cudaFree(p);
     if (c->trsv_buf) cudaFree(c->trsv_buf);
@@ -1024,7 +1029,8 @@ void exg_destroy(exg_ctx* c) {
     if (c->h_ctrl) cudaFreeHost(c->h_ctrl);
     {
         double* dq[] = {c->mos_par, c->mos_op, c->mos_r, c->Fk, c->dF, c->nw, c->nu, c->nv,
-                        c->aux.V, c->aux.hbar, c->aux.hinv, c->aux.coef, c->aux.dscratch};
+                        c->aux.V, c->aux.hbar, c->aux.hinv, c->aux.coef, c->aux.dscratch,
+};
         for (double* p : dq)
             if (p) cudaFree(p);
         if (c->mos_nodes) cudaFree(c->mos_nodes);
@@ -1793,6 +1799,7 @@ exg_status exg_counters_reset(exg_ctx* c) {
     c->launches = 0;
     c->cnt.arnoldi_iters = c->cnt.mevp_calls = c->cnt.trsv_calls = 0;
     c->cnt.graph_launches = c->cnt.graph_builds = 0;
+    c->cnt.mgs_passes = c->cnt.reorths = 0;
     return EXG_OK;
 }
 

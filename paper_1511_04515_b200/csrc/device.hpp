@@ -144,7 +144,7 @@ void spmv_norm(const Launch& L, const int* rowptr, const int* col, const double*
 void start(const Launch& L, const double* v, const double* xk, int n, double* partials,
            double* v0, Ctrl* ctrl, int er_mode);
 int mgs_max_blocks(int K);
-void mgs(const Launch& L, const MgsArgs& a, int n_blocks, int K);
+cudaError_t mgs(const Launch& L, const MgsArgs& a, int n_blocks, int K);
 void dense(const Launch& L, const DenseArgs& a, int m);
 void iter_end(const Launch& L, Ctrl* ctrl, unsigned long long cond = 0);
 void fill_ones(const Launch& L, void* p, size_t bytes);

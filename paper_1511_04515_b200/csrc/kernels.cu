@@ -1557,6 +1557,8 @@ __global__ void __launch_bounds__(1024)
                 c->happy = happy;
                 c->h_next = happy ? 0.0 : post;
                 c->m = j + 1;
+                c->mgs_passes += pass == 0 ? (unsigned)(j + 3) : (unsigned)(2 * j + 5);
+                c->reorths += pass;
             }
             return;
         }
@@ -2359,7 +2361,7 @@ int mgs_max_blocks(int K) {
     }
 }
 
-void mgs(const Launch& L, const MgsArgs& a, int n_blocks, int K) {
+cudaError_t mgs(const Launch& L, const MgsArgs& a, int n_blocks, int K) {
     void* args[] = {(void*)&a};
     void* fn;
     switch (K) {
@@ -2369,12 +2371,15 @@ void mgs(const Launch& L, const MgsArgs& a, int n_blocks, int K) {
         case 8: fn = (void*)k_mgs<8>; break;
         default: fn = (void*)k_mgs<16>; break;
     }
+    cudaError_t e;
     if (n_blocks == 1)
-        cudaLaunchKernel(fn, dim3(1), dim3(1024), args, 0, L.stream);
+        e = cudaLaunchKernel(fn, dim3(1), dim3(1024), args, 0, L.stream);
     else
-        cudaLaunchCooperativeKernel(fn, dim3(n_blocks), dim3(1024), args, 0, L.stream);
+        e = cudaLaunchCooperativeKernel(fn, dim3(n_blocks), dim3(1024), args, 0, L.stream);
     count(L);
+    return e;
 }
+
 
 void dense(const Launch& L, const DenseArgs& a0, int m) {
     static bool attr = false;

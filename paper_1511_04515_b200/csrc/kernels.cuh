@@ -43,6 +43,8 @@ struct Ctrl {
     double h_sub;
     double xinf;      // ||x_k||_inf for the er_eval early-out
     unsigned int arnoldi_iters;
+    unsigned int mgs_passes;  // algorithmic n-vector passes of the MGS kernels (J + 2, + J + 1 per reorth)
+    unsigned int reorths;     // reorthogonalisation passes taken
 };
 
 __device__ __forceinline__ unsigned long long ld_relaxed(const double* p) {

@@ -154,6 +154,20 @@ exg_status exg_factor_get(const exg_factor* f, int* n, const int** Lp, const int
 /* seconds spent in ordering / numeric phases of the last exg_lu_factor */
 exg_status exg_factor_timing(const exg_factor* f, double* order_s, double* numeric_s);
 
+/* ---- FAST-solve plan (diagnostics / tests) ------------------------------- *
+ * Builds the blocked augmented system the FAST triangular solve runs
+ * (paper_1511_04515_b200/csrc/trsv_plan.hpp; replaces the row-by-row sweep of
+ * Factorization::solve, sparse_lu.cpp:255-291, for one triangle) and
+ * evaluates it on the CPU in plan order.  ptr/col/val: the STRICTLY
+ * triangular part in pivot coordinates; diag: U's diagonal (upper only);
+ * in_index: where row r reads its right-hand side.  params (may be null):
+ * {min_block, max_block, chunk_over, recent, chunk}.  x: n results.
+ * stats (may be null): {orig_levels, levels, n_blocks, block_rows,
+ * max_block, n_partials, n_aug, n_tasks}. */
+exg_status exg_aug_plan_solve(int upper, int n, const int* ptr, const int* col, const double* val,
+                              const double* diag, const int* in_index, const int* params,
+                              const double* b, double* x, long long* stats);
+
 /* ---- transient (the reference's time-stepping loop, ER / ERC) ------------ */
 
 enum { EXG_METHOD_ER = 1, EXG_METHOD_ERC = 2 };

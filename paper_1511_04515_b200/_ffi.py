@@ -135,6 +135,7 @@ _HOST_PROTOS = {
     "exg_residual_F_host": (I, [P, PD, PD, PD]),
     "exg_lu_factor": (I, [I, PI, PI, PD, D, C.POINTER(P)]),
     "exg_factor_free": (None, [P]),
+    "exg_aug_plan_solve": (I, [I, I, PI, PI, PD, PD, PI, PI, PD, PD, C.POINTER(C.c_longlong)]),
     "exg_factor_get": (I, [P, PI, C.POINTER(PI), C.POINTER(PI), C.POINTER(PD), C.POINTER(PI),
                            C.POINTER(PI), C.POINTER(PD), C.POINTER(PI), C.POINTER(PI)]),
     "exg_factor_timing": (I, [P, PD, PD]),

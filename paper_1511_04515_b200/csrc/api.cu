@@ -15,6 +15,7 @@
 #include "exg.h"
 #include "kernels.cuh"
 #include "ctx.hpp"
+#include "trsv_plan.hpp"
 
 using exg::dev::Ctrl;
 
@@ -161,11 +162,14 @@ void solve_dev(exg_ctx* c, const double* b, double* final_out, double coef, cons
     const bool fast = c->opt.trsv_mode == EXG_TRSV_FAST;
     const size_t chain_doubles = fast ? (size_t)(c->plan[0].chain_rows + c->plan[1].chain_rows +
                                                  c->plan[0].chain_slots + c->plan[1].chain_slots) : 0;
-    exg::dev::fill_ones(c->L(), c->trsv_buf, kTrsvHdr + sizeof(double) * (2 * (size_t)n + chain_doubles));
+    // output of each sweep: n unknowns, or the augmented system's n_aug
+    const size_t ny = fast && c->plan[0].n_atasks ? (size_t)c->plan[0].n_aug : (size_t)n;
+    const size_t nx = fast && c->plan[1].n_atasks ? (size_t)c->plan[1].n_aug : (size_t)n;
+    exg::dev::fill_ones(c->L(), c->trsv_buf, kTrsvHdr + sizeof(double) * (ny + nx + chain_doubles));
     unsigned int* tickets = reinterpret_cast<unsigned int*>(c->trsv_buf);
     double* y = reinterpret_cast<double*>(c->trsv_buf + kTrsvHdr);
-    double* x = y + n;
-    double* sbuf_dev = x + n;  // chain runs' s vectors, run after run
+    double* x = y + ny;
+    double* sbuf_dev = x + nx;  // chain runs' s values, run after run
     double* pbuf_dev = sbuf_dev + c->plan[0].chain_rows + c->plan[1].chain_rows;  // partial slots
     const int fq = fast ? 2 : 0;
     int next_ticket = 0;
@@ -198,6 +202,18 @@ void solve_dev(exg_ctx* c, const double* b, double* final_out, double coef, cons
             exg::dev::trsv(c->L(), upper, fast, a);
         } else {
             const TriPlan& P = c->plan[tri];
+            if (P.n_atasks) {
+                // blocked augmented system: one sync-free warp-task launch
+                a.tasks = P.atasks;
+                a.n_tasks = P.n_atasks;
+                a.meta = P.ameta;
+                a.col = P.acol;
+                a.val = P.aval;
+                a.diag = P.adiag;
+                ck(exg::dev::trsv_wide(c->L(), upper, a), "augmented solve launch");
+                c->prof_end(upper ? EXG_K_TRSV_U : EXG_K_TRSV_L, e0);
+                continue;
+            }
             const bool run_timing = getenv("EXG_RUN_TIMING") != nullptr && !c->capturing;
             std::vector<cudaEvent_t> rev;
             for (const TriPlan::Run& run : P.runs) {
@@ -733,22 +749,22 @@ void plan_triangle(exg_ctx* c, TriPlan& P, bool upper_tri, const std::vector<int
         P.cncol = dalloc<int>(std::max<size_t>(cncol.size(), 1));
         P.cnval = dalloc<double>(std::max<size_t>(cnval.size(), 1));
         P.cblocks = dalloc<int4>(cblocks.size());
-        ck(cudaMemcpy(P.crows, crows.data(), crows.size() * sizeof(int), cudaMemcpyHostToDevice), "chain");
-        ck(cudaMemcpy(P.cnptr, cnptr.data(), cnptr.size() * sizeof(int), cudaMemcpyHostToDevice), "chain");
+        ck(cudaMemcpyAsync(P.crows, crows.data(), crows.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream), "chain");
+        ck(cudaMemcpyAsync(P.cnptr, cnptr.data(), cnptr.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream), "chain");
         if (!cncol.empty()) {
-            ck(cudaMemcpy(P.cncol, cncol.data(), cncol.size() * sizeof(int), cudaMemcpyHostToDevice), "chain");
-            ck(cudaMemcpy(P.cnval, cnval.data(), cnval.size() * sizeof(double), cudaMemcpyHostToDevice), "chain");
+            ck(cudaMemcpyAsync(P.cncol, cncol.data(), cncol.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream), "chain");
+            ck(cudaMemcpyAsync(P.cnval, cnval.data(), cnval.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream), "chain");
         }
-        ck(cudaMemcpy(P.cblocks, cblocks.data(), cblocks.size() * sizeof(int4), cudaMemcpyHostToDevice), "chain");
+        ck(cudaMemcpyAsync(P.cblocks, cblocks.data(), cblocks.size() * sizeof(int4), cudaMemcpyHostToDevice, c->stream), "chain");
         P.ctasks = dalloc<int4>(std::max<size_t>(ctasks.size(), 1));
-        ck(cudaMemcpy(P.ctasks, ctasks.data(), ctasks.size() * sizeof(int4), cudaMemcpyHostToDevice), "chain");
+        ck(cudaMemcpyAsync(P.ctasks, ctasks.data(), ctasks.size() * sizeof(int4), cudaMemcpyHostToDevice, c->stream), "chain");
         P.crq = dalloc<int2>(std::max<size_t>(crq.size(), 1));
-        ck(cudaMemcpy(P.crq, crq.data(), crq.size() * sizeof(int2), cudaMemcpyHostToDevice), "chain");
+        ck(cudaMemcpyAsync(P.crq, crq.data(), crq.size() * sizeof(int2), cudaMemcpyHostToDevice, c->stream), "chain");
         P.cpslot = dalloc<int>(std::max<size_t>(cpslot.size(), 1));
-        ck(cudaMemcpy(P.cpslot, cpslot.data(), cpslot.size() * sizeof(int), cudaMemcpyHostToDevice), "chain");
+        ck(cudaMemcpyAsync(P.cpslot, cpslot.data(), cpslot.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream), "chain");
         P.pool = dalloc<double>(std::max<size_t>(pool.size(), 1));
         if (!pool.empty())
-            ck(cudaMemcpy(P.pool, pool.data(), pool.size() * sizeof(double), cudaMemcpyHostToDevice), "chain");
+            ck(cudaMemcpyAsync(P.pool, pool.data(), pool.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream), "chain");
         // run-local views: the nptr index of position j of run q is pos0 + q + j
         for (size_t q = 0; q < cruns.size(); ++q) {
             TriPlan::Chain ch;
@@ -841,7 +857,7 @@ void transpose_pattern(int n, const std::vector<int>& ptr, const std::vector<int
 // (L: ascending row, U: descending), warp tasks within one local level, and
 // each row's entries re-encoded (earlier-phase rows first as global ids, then
 // component slots ascending as ~slot).  Components are issued largest first.
-void build_sub(SubPlan& P, bool upper, const std::vector<int>& comp, int ncomp,
+void build_sub(exg_ctx* c, SubPlan& P, bool upper, const std::vector<int>& comp, int ncomp,
                const std::vector<int>& ptr, const std::vector<int>& col,
                const std::vector<double>& val, const int* row_perm) {
     P.free_dev();
@@ -938,18 +954,18 @@ void build_sub(SubPlan& P, bool upper, const std::vector<int>& comp, int ncomp,
     P.comps = dalloc<int4>(comps.size());
     P.clev = dalloc<int2>(clev.size());
     P.ltp = dalloc<int>(ltp.size());
-    ck(cudaMemcpy(P.clev, clev.data(), clev.size() * sizeof(int2), cudaMemcpyHostToDevice), "sub plan");
-    ck(cudaMemcpy(P.ltp, ltp.data(), ltp.size() * sizeof(int), cudaMemcpyHostToDevice), "sub plan");
+    ck(cudaMemcpyAsync(P.clev, clev.data(), clev.size() * sizeof(int2), cudaMemcpyHostToDevice, c->stream), "sub plan");
+    ck(cudaMemcpyAsync(P.ltp, ltp.data(), ltp.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream), "sub plan");
     P.tasks = dalloc<int2>(tasks.size());
     P.meta = dalloc<int4>(meta.size());
     P.ecol = dalloc<int>(std::max<size_t>(ecol.size(), 1));
     P.eval = dalloc<double>(std::max<size_t>(eval.size(), 1));
-    ck(cudaMemcpy(P.comps, comps.data(), comps.size() * sizeof(int4), cudaMemcpyHostToDevice), "sub plan");
-    ck(cudaMemcpy(P.tasks, tasks.data(), tasks.size() * sizeof(int2), cudaMemcpyHostToDevice), "sub plan");
-    ck(cudaMemcpy(P.meta, meta.data(), meta.size() * sizeof(int4), cudaMemcpyHostToDevice), "sub plan");
+    ck(cudaMemcpyAsync(P.comps, comps.data(), comps.size() * sizeof(int4), cudaMemcpyHostToDevice, c->stream), "sub plan");
+    ck(cudaMemcpyAsync(P.tasks, tasks.data(), tasks.size() * sizeof(int2), cudaMemcpyHostToDevice, c->stream), "sub plan");
+    ck(cudaMemcpyAsync(P.meta, meta.data(), meta.size() * sizeof(int4), cudaMemcpyHostToDevice, c->stream), "sub plan");
     if (!ecol.empty()) {
-        ck(cudaMemcpy(P.ecol, ecol.data(), ecol.size() * sizeof(int), cudaMemcpyHostToDevice), "sub plan");
-        ck(cudaMemcpy(P.eval, eval.data(), eval.size() * sizeof(double), cudaMemcpyHostToDevice), "sub plan");
+        ck(cudaMemcpyAsync(P.ecol, ecol.data(), ecol.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream), "sub plan");
+        ck(cudaMemcpyAsync(P.eval, eval.data(), eval.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream), "sub plan");
     }
 }
 
@@ -974,8 +990,9 @@ exg_status exg_create(int device, exg_ctx** out) {
     }
     c->bar = dalloc<unsigned int>(4);
     c->done = dalloc<unsigned int>(4);
-    ck(cudaMemset(c->bar, 0, 4 * sizeof(unsigned int)), "memset");
-    ck(cudaMemset(c->done, 0, 4 * sizeof(unsigned int)), "memset");
+    ck(cudaMemsetAsync(c->bar, 0, 4 * sizeof(unsigned int), c->stream), "memset");
+    ck(cudaMemsetAsync(c->done, 0, 4 * sizeof(unsigned int), c->stream), "memset");
+    ck(cudaStreamSynchronize(c->stream), "memset sync");
     c->weight = dalloc<double>(4);
     c->ctrl = static_cast<Ctrl*>(static_cast<void*>(dalloc<char>(exg::dev::ctrl_size())));
     void* hp = nullptr;
@@ -1077,7 +1094,8 @@ exg_status exg_set_csr(exg_ctx* c, int which, int n_rows, int n_cols, int nnz, c
 exg_status exg_update_values(exg_ctx* c, int which, const double* val) {
     API_BEGIN
     const DCsr& m = mat(c, which);
-    ck(cudaMemcpy(m.val, val, sizeof(double) * m.nnz, cudaMemcpyHostToDevice), "update values");
+    ck(cudaMemcpyAsync(m.val, val, sizeof(double) * m.nnz, cudaMemcpyHostToDevice, c->stream), "update values");
+    ck(cudaStreamSynchronize(c->stream), "upload sync");  // host buffers may be released on return
     API_END(c)
 }
 
@@ -1295,11 +1313,11 @@ exg_status exg_set_factors(exg_ctx* c, int n, const int* Lp, const int* Li, cons
     c->n = n;
     auto up_i = [&](int*& d, const int* h, size_t cnt) {
         d = dalloc<int>(cnt);
-        if (cnt) ck(cudaMemcpy(d, h, cnt * sizeof(int), cudaMemcpyHostToDevice), "factor upload");
+        if (cnt) ck(cudaMemcpyAsync(d, h, cnt * sizeof(int), cudaMemcpyHostToDevice, c->stream), "factor upload");
     };
     auto up_d = [&](double*& d, const double* h, size_t cnt) {
         d = dalloc<double>(cnt);
-        if (cnt) ck(cudaMemcpy(d, h, cnt * sizeof(double), cudaMemcpyHostToDevice), "factor upload");
+        if (cnt) ck(cudaMemcpyAsync(d, h, cnt * sizeof(double), cudaMemcpyHostToDevice, c->stream), "factor upload");
     };
     up_i(c->l_ptr, lp.data(), n + 1);
     up_i(c->l_col, lc.data(), lc.size());
@@ -1314,10 +1332,56 @@ exg_status exg_set_factors(exg_ctx* c, int n, const int* Lp, const int* Li, cons
     up_i(c->u_order, uord.data(), n);
     // FAST-mode plan: runs of wide levels (warp tasks, all SMs) and of narrow
     // levels (one thread-block cluster, DSMEM hand-offs)
-    plan_triangle(c, c->plan[0], false, lford, lflev, lnl_f, lp, lc, lv, ltasks_f, nullptr, nullptr, l_sub);
-    plan_triangle(c, c->plan[1], true, uford, uflev, unl_f, up, uc, uv, utasks_f, &ud, col_perm, u_sub);
-    build_sub(c->plan[0].sub, false, lcomp, lncomp, lp, lc, lv, row_perm);
-    build_sub(c->plan[1].sub, true, ucomp, uncomp, up, uc, uv, row_perm);
+    // FAST plan: the blocked augmented system (default, trsv_plan.hpp), or
+    // the level-run plan (wide runs + cluster chain, EXG_FAST_PLAN=chain)
+    const char* fp_env = getenv("EXG_FAST_PLAN");
+    const bool use_aug = !(fp_env && std::string(fp_env) == "chain");
+    if (!use_aug) {
+        plan_triangle(c, c->plan[0], false, lford, lflev, lnl_f, lp, lc, lv, ltasks_f, nullptr, nullptr, l_sub);
+        plan_triangle(c, c->plan[1], true, uford, uflev, unl_f, up, uc, uv, utasks_f, &ud, col_perm, u_sub);
+        build_sub(c, c->plan[0].sub, false, lcomp, lncomp, lp, lc, lv, row_perm);
+        build_sub(c, c->plan[1].sub, true, ucomp, uncomp, up, uc, uv, row_perm);
+    } else {
+        exg::AugParams prm;
+        if (const char* e = getenv("EXG_AUG")) {  // min_block,max_block,chunk_over,recent,chunk
+            int v[5] = {prm.min_block, prm.max_block, prm.chunk_over, prm.recent, prm.chunk};
+            sscanf(e, "%d,%d,%d,%d,%d", &v[0], &v[1], &v[2], &v[3], &v[4]);
+            prm = exg::AugParams{v[0], v[1], v[2], v[3], v[4]};
+        }
+        std::vector<int> ident(n);
+        for (int i = 0; i < n; ++i) ident[i] = i;
+        for (int tri = 0; tri < 2; ++tri) {
+            TriPlan& P = c->plan[tri];
+            P.free_dev();
+            P.runs.clear();
+            exg::AugPlan A;
+            if (tri == 0)
+                exg::build_aug_plan(false, n, lp.data(), lc.data(), lv.data(), nullptr, row_perm, prm, A);
+            else
+                exg::build_aug_plan(true, n, up.data(), uc.data(), uv.data(), ud.data(), ident.data(), prm, A);
+            P.ameta = reinterpret_cast<int4*>(dalloc<int>(A.meta.size()));
+            P.atasks = reinterpret_cast<int2*>(dalloc<int>(std::max<size_t>(A.tasks.size(), 2)));
+            P.acol = dalloc<int>(std::max<size_t>(A.col.size(), 1));
+            P.aval = dalloc<double>(std::max<size_t>(A.val.size(), 1));
+            P.adiag = dalloc<double>(A.diag.size());
+            ck(cudaMemcpyAsync(P.ameta, A.meta.data(), A.meta.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream), "aug plan");
+            ck(cudaMemcpyAsync(P.atasks, A.tasks.data(), A.tasks.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream), "aug plan");
+            if (!A.col.empty()) {
+                ck(cudaMemcpyAsync(P.acol, A.col.data(), A.col.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream), "aug plan");
+                ck(cudaMemcpyAsync(P.aval, A.val.data(), A.val.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream), "aug plan");
+            }
+            ck(cudaMemcpyAsync(P.adiag, A.diag.data(), A.diag.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream), "aug plan");
+            ck(cudaStreamSynchronize(c->stream), "aug plan sync");  // A is released below
+            P.n_atasks = (int)(A.tasks.size() / 2);
+            P.n_aug = A.n_aug;
+            P.aug_levels = A.levels;
+            c->cnt_aug[tri][0] = A.levels;
+            c->cnt_aug[tri][1] = A.n_blocks;
+            c->cnt_aug[tri][2] = A.block_rows;
+            c->cnt_aug[tri][3] = A.n_partials;
+            c->cnt_aug[tri][4] = (long long)A.col.size();
+        }
+    }
     {
         std::vector<int4> lm(n), um(n);
         for (int p = 0; p < n; ++p) {
@@ -1330,17 +1394,19 @@ exg_status exg_set_factors(exg_ctx* c, int n, const int* Lp, const int* Li, cons
         if (c->meta[1]) cudaFree(c->meta[1]);
         c->meta[0] = dalloc<int4>(n);
         c->meta[1] = dalloc<int4>(n);
-        ck(cudaMemcpy(c->meta[0], lm.data(), n * sizeof(int4), cudaMemcpyHostToDevice), "meta");
-        ck(cudaMemcpy(c->meta[1], um.data(), n * sizeof(int4), cudaMemcpyHostToDevice), "meta");
+        ck(cudaMemcpyAsync(c->meta[0], lm.data(), n * sizeof(int4), cudaMemcpyHostToDevice, c->stream), "meta");
+        ck(cudaMemcpyAsync(c->meta[1], um.data(), n * sizeof(int4), cudaMemcpyHostToDevice, c->stream), "meta");
     }
     const std::vector<int2>* tl[4] = {&ltasks, &utasks, &ltasks_f, &utasks_f};
     for (int q = 0; q < 4; ++q) {
         if (c->tasks[q]) cudaFree(c->tasks[q]);
         c->tasks[q] = dalloc<int2>(tl[q]->size());
-        ck(cudaMemcpy(c->tasks[q], tl[q]->data(), tl[q]->size() * sizeof(int2), cudaMemcpyHostToDevice), "tasks");
+        ck(cudaMemcpyAsync(c->tasks[q], tl[q]->data(), tl[q]->size() * sizeof(int2), cudaMemcpyHostToDevice, c->stream), "tasks");
         c->n_tasks[q] = (int)tl[q]->size();
     }
-    c->trsv_buf = dalloc<char>(kTrsvHdr + sizeof(double) * (2 * (size_t)n + c->plan[0].chain_rows +
+    c->trsv_buf = dalloc<char>(kTrsvHdr + sizeof(double) * ((size_t)std::max<long long>(n, c->plan[0].n_aug) +
+                                                       (size_t)std::max<long long>(n, c->plan[1].n_aug) +
+                                                       c->plan[0].chain_rows +
                                                        c->plan[1].chain_rows + c->plan[0].chain_slots +
                                                        c->plan[1].chain_slots));
     ensure_vectors(c, n);
@@ -1353,6 +1419,7 @@ exg_status exg_set_factors(exg_ctx* c, int n, const int* Lp, const int* Li, cons
     c->mmax_alloc = 0;  // Krylov workspace re-sized on next use
     dfree(c->V);
     c->basis_valid = false;
+    ck(cudaStreamSynchronize(c->stream), "upload sync");  // host buffers may be released on return
     API_END(c)
 }
 
@@ -1594,12 +1661,12 @@ exg_status exg_set_devices(exg_ctx* c, int n_mos, const int* nodes4, const doubl
     c->node_ptr = dalloc<int>(n + 1);
     c->node_list = dalloc<int>(std::max(cnt[n], 1));
     if (n_mos) {
-        ck(cudaMemcpy(c->mos_nodes, nodes4, 4 * sizeof(int) * n_mos, cudaMemcpyHostToDevice), "mos");
-        ck(cudaMemcpy(c->mos_par, par6, 6 * sizeof(double) * n_mos, cudaMemcpyHostToDevice), "mos");
-        ck(cudaMemset(c->mos_op, 0, 5 * sizeof(double) * n_mos), "mos");
+        ck(cudaMemcpyAsync(c->mos_nodes, nodes4, 4 * sizeof(int) * n_mos, cudaMemcpyHostToDevice, c->stream), "mos");
+        ck(cudaMemcpyAsync(c->mos_par, par6, 6 * sizeof(double) * n_mos, cudaMemcpyHostToDevice, c->stream), "mos");
+        ck(cudaMemsetAsync(c->mos_op, 0, 5 * sizeof(double) * n_mos, c->stream), "mos");
     }
-    ck(cudaMemcpy(c->node_ptr, cnt.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice), "mos");
-    if (cnt[n]) ck(cudaMemcpy(c->node_list, list.data(), sizeof(int) * cnt[n], cudaMemcpyHostToDevice), "mos");
+    ck(cudaMemcpyAsync(c->node_ptr, cnt.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice, c->stream), "mos");
+    if (cnt[n]) ck(cudaMemcpyAsync(c->node_list, list.data(), sizeof(int) * cnt[n], cudaMemcpyHostToDevice, c->stream), "mos");
     double** vs[] = {&c->Fk, &c->dF, &c->nw, &c->nu, &c->nv};
     for (double** p : vs) {
         dfree(*p);
@@ -1612,12 +1679,14 @@ exg_status exg_set_devices(exg_ctx* c, int n_mos, const int* nodes4, const doubl
         c->aux.h_ctrl = static_cast<Ctrl*>(hp);
         std::memset(c->aux.h_ctrl, 0, exg::dev::ctrl_size());
     }
+    ck(cudaStreamSynchronize(c->stream), "upload sync");  // host buffers may be released on return
     API_END(c)
 }
 
 exg_status exg_set_oppoints(exg_ctx* c, const double* op5) {
     API_BEGIN
-    if (c->n_mos) ck(cudaMemcpy(c->mos_op, op5, 5 * sizeof(double) * c->n_mos, cudaMemcpyHostToDevice), "op");
+    if (c->n_mos) ck(cudaMemcpyAsync(c->mos_op, op5, 5 * sizeof(double) * c->n_mos, cudaMemcpyHostToDevice, c->stream), "op");
+    ck(cudaStreamSynchronize(c->stream), "upload sync");  // host buffers may be released on return
     API_END(c)
 }
 

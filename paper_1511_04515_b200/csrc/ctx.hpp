@@ -73,7 +73,30 @@ struct TriPlan {
     int2* crq = nullptr;
     long long chain_rows = 0, chain_slots = 0;  // scratch of the chain runs (s values, partial slots)
     SubPlan sub;
+    // blocked augmented system (trsv_plan.hpp): one k_trsv3 launch over
+    // n_aug unknowns; used when aug_tasks > 0
+    int4* ameta = nullptr;
+    int2* atasks = nullptr;
+    int* acol = nullptr;
+    double* aval = nullptr;
+    double* adiag = nullptr;
+    int n_atasks = 0;
+    long long n_aug = 0;
+    int aug_levels = 0;
+    void free_aug() {
+        void* ps[] = {ameta, atasks, acol, aval, adiag};
+        for (void* p : ps)
+            if (p) cudaFree(p);
+        ameta = nullptr;
+        atasks = nullptr;
+        acol = nullptr;
+        aval = adiag = nullptr;
+        n_atasks = 0;
+        n_aug = 0;
+        aug_levels = 0;
+    }
     void free_dev() {
+        free_aug();
         sub.free_dev();
         void* ps[] = {pool, crows, cnptr, cncol, cnval, cblocks, ctasks, cpslot, crq};
         for (void* p : ps)
@@ -137,6 +160,7 @@ struct exg_ctx {
     unsigned long long *ntrace_l = nullptr, *ntrace_u = nullptr;
     // solve scratch: [2 tickets + pad (16 B)][y n][x n], memset to 0xFF per solve
     char* trsv_buf = nullptr;
+    long long cnt_aug[2][5] = {};  // per triangle: levels, blocks, block rows, partials, entries
     // n-vectors
     int vec_n = 0;
     double *vin = nullptr, *vout = nullptr, *t = nullptr, *w = nullptr, *xk = nullptr,

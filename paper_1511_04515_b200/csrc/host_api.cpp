@@ -4,6 +4,7 @@
 #include <limits>
 
 #include "host.hpp"
+#include "trsv_plan.hpp"
 
 
 namespace {
@@ -235,6 +236,37 @@ exg_status exg_step_control_from(const exg_system* s, exg_step_control* c) {
     c->method = EXG_METHOD_ER;
     c->gamma = 0.1;
     return EXG_OK;
+}
+
+
+exg_status exg_aug_plan_solve(int upper, int n, const int* ptr, const int* col, const double* val,
+                              const double* diag, const int* in_index, const int* params,
+                              const double* b, double* x, long long* stats) {
+    HOST_GUARD_BEGIN
+    if (n < 0 || !ptr || (upper && !diag) || !in_index) throw exg::Error{EXG_E_CONTRACT, "exg_aug_plan_solve: bad arguments"};
+    exg::AugParams prm;
+    if (params) {
+        prm.min_block = params[0];
+        prm.max_block = params[1];
+        prm.chunk_over = params[2];
+        prm.recent = params[3];
+        prm.chunk = params[4];
+    }
+    if (prm.max_block < 1 || prm.recent < 0 || prm.chunk < 1 || prm.chunk_over < prm.recent)
+        throw exg::Error{EXG_E_CONTRACT, "exg_aug_plan_solve: bad plan parameters"};
+    exg::AugPlan P;
+    exg::build_aug_plan(upper != 0, n, ptr, col, val, diag, in_index, prm, P);
+    if (b && x) {
+        std::vector<double> out(P.n_aug, 0.0);
+        exg::eval_aug_plan(P, upper != 0, b, out.data());
+        std::memcpy(x, out.data(), sizeof(double) * n);
+    }
+    if (stats) {
+        const long long st[8] = {P.orig_levels, P.levels,     P.n_blocks, P.block_rows,
+                                 P.max_block,   P.n_partials, P.n_aug,    (long long)P.tasks.size() / 2};
+        std::memcpy(stats, st, sizeof st);
+    }
+    HOST_GUARD_END
 }
 
 }  // extern "C"

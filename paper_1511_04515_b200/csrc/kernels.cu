@@ -450,9 +450,11 @@ __global__ void __launch_bounds__(256)
         pr = Pre{0.0, 1.0, 0.0, 0};
         if (seg < cnt) {
             m = a.meta[task.x + seg];
-            pr.b = a.in[m.y];
+            // augmented rows (trsv_plan.hpp) may have no right-hand side (-1)
+            // and outputs beyond n (block y's, partial sums): no epilogue
+            pr.b = m.y >= 0 ? a.in[m.y] : 0.0;
             if (UPPER) pr.dg = a.diag[m.x];
-            if (a.final_out) {
+            if (a.final_out && m.x < a.n) {
                 pr.qq = a.out_perm[m.x];
                 if (a.add) pr.ad = a.add[pr.qq];
             }
@@ -549,7 +551,7 @@ __global__ void __launch_bounds__(256)
                 double s = pr.b - acc;
                 if (UPPER) s = s / pr.dg;
                 st_relaxed(a.out + r, s);
-                if (a.final_out) {
+                if (a.final_out && r < a.n) {
                     double yv = a.coef * s;
                     if (a.add) yv = pr.ad + yv;
                     a.final_out[pr.qq] = yv;
@@ -588,7 +590,7 @@ __global__ void __launch_bounds__(256)
                 double s = pr.b - acc;
                 if (UPPER) s = s / pr.dg;
                 st_relaxed(a.out + r, s);
-                if (a.final_out) {
+                if (a.final_out && r < a.n) {
                     double yv = a.coef * s;
                     if (a.add) yv = pr.ad + yv;
                     a.final_out[pr.qq] = yv;

@@ -60,6 +60,17 @@ struct PinnedDoubles {
     }
 };
 
+struct EventPair {  // created recorded-complete: the first wait returns at once
+    cudaEvent_t e[2] = {nullptr, nullptr};
+    EventPair() {
+        for (auto& x : e) cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
+    }
+    ~EventPair() {
+        for (auto& x : e)
+            if (x) cudaEventDestroy(x);
+    }
+};
+
 struct DeviceDoubles {
     double* p = nullptr;
     ~DeviceDoubles() {
@@ -245,6 +256,9 @@ exg_status exg_transient(exg_ctx* ctx, const exg_system* sp, const exg_step_cont
     try {
         const exg::System& sys = sp->sys;
         if (t_stop <= 0.0) throw Fail{EXG_E_CONTRACT, "transient: t_stop must be positive"};
+        // ER and ER-C only: BENR (integrate.cpp:400-416) stays reference host code
+        if (!ctl || (ctl->method != EXG_METHOD_ER && ctl->method != EXG_METHOD_ERC))
+            throw Fail{EXG_E_CONTRACT, "transient: method must be EXG_METHOD_ER or EXG_METHOD_ERC"};
         if (!sys.mos.empty()) {
             *out = nullptr;
             return transient_nonlinear(ctx, sys, ctl, t_stop, rec_idx, n_rec, out);
@@ -322,8 +336,13 @@ exg_status exg_transient(exg_ctx* ctx, const exg_system* sp, const exg_step_cont
         const int n = sys.n;
         const int ni = sys.n_inputs();
         chk(ctx, exg_memcpy(ctx, ctx->xnext, x.data(), sizeof(double) * n, cudaMemcpyHostToDevice));
+        // two pinned staging slots for (u_k, u_k1), used alternately; an event
+        // per slot marks its H2D copies done before the slot is rewritten, so
+        // correctness does not depend on a host sync elsewhere in the step
         PinnedDoubles u_pin;
-        if (ni) cuda_chk(cudaMallocHost(&u_pin.p, sizeof(double) * 2 * ni), "cudaMallocHost");
+        if (ni) cuda_chk(cudaMallocHost(&u_pin.p, sizeof(double) * 4 * ni), "cudaMallocHost");
+        EventPair u_done;
+        int u_slot = 0;
         // recorded samples: a device ring of up to 256 steps (<= 64 MB) and a
         // pinned host mirror; one read-back per ring instead of a sync per step
         const int k_rec = static_cast<int>(rec.size());
@@ -354,14 +373,18 @@ exg_status exg_transient(exg_ctx* ctx, const exg_system* sp, const exg_step_cont
             const std::vector<double> u_k = exg::eval_sources(sys, t);
             const std::vector<double> u_k1 = exg::eval_sources(sys, t + h_try);
             if (ni) {
-                // pinned staging, stream-ordered before er_begin; the previous
-                // step's gather synchronised, so its copies have completed
-                std::memcpy(u_pin.p, u_k.data(), sizeof(double) * ni);
-                std::memcpy(u_pin.p + ni, u_k1.data(), sizeof(double) * ni);
-                cuda_chk(cudaMemcpyAsync(ctx->u_k, u_pin.p, sizeof(double) * ni, cudaMemcpyHostToDevice,
+                // pinned staging, stream-ordered before er_begin; wait until
+                // the copies that last read this slot (two steps ago) are done
+                double* slot = u_pin.p + (size_t)2 * ni * u_slot;
+                cuda_chk(cudaEventSynchronize(u_done.e[u_slot]), "u slot wait");
+                std::memcpy(slot, u_k.data(), sizeof(double) * ni);
+                std::memcpy(slot + ni, u_k1.data(), sizeof(double) * ni);
+                cuda_chk(cudaMemcpyAsync(ctx->u_k, slot, sizeof(double) * ni, cudaMemcpyHostToDevice,
                                          ctx->stream), "u_k upload");
-                cuda_chk(cudaMemcpyAsync(ctx->u_k1, u_pin.p + ni, sizeof(double) * ni,
+                cuda_chk(cudaMemcpyAsync(ctx->u_k1, slot + ni, sizeof(double) * ni,
                                          cudaMemcpyHostToDevice, ctx->stream), "u_k1 upload");
+                cuda_chk(cudaEventRecord(u_done.e[u_slot], ctx->stream), "u slot event");
+                u_slot ^= 1;
             }
             // x_k <- previous x_next (device to device)
             chk(ctx, exg_er_begin(ctx, ctx->xnext, ctx->u_k, ctx->u_k1, h_try, EXG_PTR_DEVICE));

@@ -1,0 +1,361 @@
+// Blocked augmented triangular system for the FAST solve (see trsv_plan.hpp).
+#include "trsv_plan.hpp"
+
+#include <algorithm>
+#include <atomic>
+#include <numeric>
+#include <stdexcept>
+#include <thread>
+
+namespace exg {
+namespace {
+
+struct Block {
+    int a, b;  // rows [a, b)
+};
+
+// Maximal runs of rows whose diagonal block is dense.  L: row i joins [a, i)
+// when its last i-a entries are exactly a..i-1.  U (scanned upwards): row i
+// joins [i+1, b) when its first b-1-i entries are exactly i+1..b-1.
+std::vector<Block> dense_blocks(bool upper, int n, const int* ptr, const int* col, int min_block,
+                                int max_block) {
+    std::vector<Block> out;
+    auto keep = [&](int a, int b) {
+        if (b - a < min_block) return;
+        for (int s = a; s < b; s += max_block) out.push_back({s, std::min(b, s + max_block)});
+    };
+    if (!upper) {
+        int a = 0;
+        for (int i = 1; i <= n; ++i) {
+            bool ext = false;
+            if (i < n) {
+                const int need = i - a, len = ptr[i + 1] - ptr[i];
+                ext = len >= need && col[ptr[i + 1] - need] == a;
+            }
+            if (!ext) {
+                keep(a, i);
+                a = i;
+            }
+        }
+    } else {
+        int b = n;
+        for (int i = n - 2; i >= -1; --i) {
+            bool ext = false;
+            if (i >= 0) {
+                const int need = b - 1 - i, len = ptr[i + 1] - ptr[i];
+                ext = len >= need && col[ptr[i] + need - 1] == b - 1;
+            }
+            if (!ext) {
+                keep(i + 1, b);
+                b = i + 1;
+            }
+        }
+    }
+    // scan order: L ascending, U descending
+    std::sort(out.begin(), out.end(), [upper](const Block& x, const Block& y) { return upper ? x.a > y.a : x.a < y.a; });
+    return out;
+}
+
+// Explicit inverse of a dense block, row-major s x s.  L: unit lower (entries
+// strictly below the diagonal in m); U: upper with diagonal d.
+void invert_block(bool upper, int s, const std::vector<double>& m, const double* d, std::vector<double>& inv) {
+    inv.assign((size_t)s * s, 0.0);
+    if (!upper) {
+        for (int i = 0; i < s; ++i) {
+            double* ri = &inv[(size_t)i * s];
+            ri[i] = 1.0;
+            for (int k = 0; k < i; ++k) {
+                const double f = m[(size_t)i * s + k];
+                if (f == 0.0) continue;
+                const double* rk = &inv[(size_t)k * s];
+                for (int j = 0; j <= k; ++j) ri[j] -= f * rk[j];
+            }
+        }
+    } else {
+        std::vector<double> acc(s);
+        for (int i = s - 1; i >= 0; --i) {
+            std::fill(acc.begin() + i, acc.end(), 0.0);
+            for (int k = i + 1; k < s; ++k) {
+                const double f = m[(size_t)i * s + k];
+                if (f == 0.0) continue;
+                const double* rk = &inv[(size_t)k * s];
+                for (int j = k; j < s; ++j) acc[j] += f * rk[j];
+            }
+            double* ri = &inv[(size_t)i * s];
+            ri[i] = 1.0 / d[i];
+            for (int j = i + 1; j < s; ++j) ri[j] = -acc[j] / d[i];
+        }
+    }
+}
+
+struct Row {
+    int out, in;
+    double dg;
+    long long e0, e1;  // entries in the staging arrays
+};
+
+}  // namespace
+
+void build_aug_plan(bool upper, int n, const int* ptr, const int* col, const double* val,
+                    const double* diag, const int* in_index, const AugParams& prm, AugPlan& P) {
+    P = AugPlan{};
+    P.n = n;
+    // levels of the plain triangle (statistics)
+    {
+        std::vector<int> lv(n, 0);
+        int nl = 0;
+        for (int q = 0; q < n; ++q) {
+            const int r = upper ? n - 1 - q : q;
+            int v = 0;
+            for (int k = ptr[r]; k < ptr[r + 1]; ++k) v = std::max(v, lv[col[k]] + 1);
+            lv[r] = v;
+            nl = std::max(nl, v + 1);
+        }
+        P.orig_levels = n ? nl : 0;
+    }
+    const std::vector<Block> blocks =
+        prm.min_block > 0 ? dense_blocks(upper, n, ptr, col, prm.min_block, prm.max_block) : std::vector<Block>{};
+    // block inverses (independent; largest first over a few host threads)
+    std::vector<std::vector<double>> invs(blocks.size());
+    {
+        std::vector<int> ord(blocks.size());
+        std::iota(ord.begin(), ord.end(), 0);
+        std::sort(ord.begin(), ord.end(), [&](int x, int y) {
+            return blocks[x].b - blocks[x].a > blocks[y].b - blocks[y].a;
+        });
+        const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+        std::vector<std::thread> th;
+        std::atomic<int> cursor{0};
+        auto work = [&]() {
+            std::vector<double> m;
+            while (true) {
+                const int q = cursor.fetch_add(1);
+                if (q >= (int)ord.size()) return;
+                const Block& B = blocks[ord[q]];
+                const int s = B.b - B.a;
+                m.assign((size_t)s * s, 0.0);
+                for (int i = 0; i < s; ++i) {
+                    const int r = B.a + i;
+                    if (!upper) {
+                        // last i entries of row r are columns a..r-1
+                        for (int k = 0; k < i; ++k) m[(size_t)i * s + k] = val[ptr[r + 1] - i + k];
+                    } else {
+                        // first s-1-i entries of row r are columns r+1..b-1
+                        for (int k = 0; k < s - 1 - i; ++k) m[(size_t)i * s + i + 1 + k] = val[ptr[r] + k];
+                    }
+                }
+                invert_block(upper, s, m, upper ? diag + B.a : nullptr, invs[ord[q]]);
+            }
+        };
+        for (unsigned t = 0; t < hw; ++t) th.emplace_back(work);
+        for (auto& t : th) t.join();
+    }
+    // ---- augmented rows in a topological order, with levels and partials
+    std::vector<Row> rows;
+    rows.reserve((size_t)n + n / 4);
+    std::vector<int> ecol;
+    std::vector<double> eval;
+    ecol.reserve((size_t)ptr[n] + n);
+    eval.reserve((size_t)ptr[n] + n);
+    std::vector<int> level;  // per unknown id
+    level.assign(n, -1);
+    long long next_id = n;
+    auto new_id = [&]() {
+        level.push_back(-1);
+        return (int)next_id++;
+    };
+    std::vector<int> rlev;  // per row (parallel to rows)
+    std::vector<std::pair<int, int>> tmp;  // (dep level, entry index) for chunking
+    std::vector<int> tcol;
+    std::vector<double> tval;
+    // finalize one row whose entries are tcol/tval: partial sums for a long
+    // history, then the row itself
+    auto emit = [&](int out, int in, double dg) {
+        const int cnt = (int)tcol.size();
+        int lmax = -1;
+        if (cnt > prm.chunk_over) {
+            tmp.resize(cnt);
+            for (int k = 0; k < cnt; ++k) tmp[k] = {level[tcol[k]], k};
+            std::stable_sort(tmp.begin(), tmp.end(),
+                             [](const std::pair<int, int>& x, const std::pair<int, int>& y) { return x.first < y.first; });
+            const int n_old = cnt - prm.recent;
+            std::vector<int> keep_c;
+            std::vector<double> keep_v;
+            for (int c0 = 0; c0 < n_old; c0 += prm.chunk) {
+                const int c1 = std::min(n_old, c0 + prm.chunk);
+                const int pid = new_id();
+                Row pr{pid, -1, 1.0, (long long)ecol.size(), 0};
+                int pl = 0;
+                for (int z = c0; z < c1; ++z) {
+                    ecol.push_back(tcol[tmp[z].second]);
+                    eval.push_back(tval[tmp[z].second]);
+                    pl = std::max(pl, tmp[z].first + 1);
+                }
+                pr.e1 = (long long)ecol.size();
+                level[pid] = pl;
+                rows.push_back(pr);
+                rlev.push_back(pl);
+                ++P.n_partials;
+                keep_c.push_back(pid);
+                keep_v.push_back(-1.0);
+            }
+            for (int z = n_old; z < cnt; ++z) {
+                keep_c.push_back(tcol[tmp[z].second]);
+                keep_v.push_back(tval[tmp[z].second]);
+            }
+            tcol.swap(keep_c);
+            tval.swap(keep_v);
+        }
+        Row r{out, in, dg, (long long)ecol.size(), 0};
+        // entries oldest first (L) / newest first (U: the kernel walks U rows
+        // backwards), so a warp meets its newest dependency last
+        const int m = (int)tcol.size();
+        tmp.resize(m);
+        for (int k = 0; k < m; ++k) {
+            tmp[k] = {level[tcol[k]], k};
+            lmax = std::max(lmax, tmp[k].first);
+        }
+        std::stable_sort(tmp.begin(), tmp.end(), [&](const std::pair<int, int>& x, const std::pair<int, int>& y) {
+            return upper ? x.first > y.first : x.first < y.first;
+        });
+        for (int k = 0; k < m; ++k) {
+            ecol.push_back(tcol[tmp[k].second]);
+            eval.push_back(tval[tmp[k].second]);
+        }
+        r.e1 = (long long)ecol.size();
+        level[out] = lmax + 1;
+        rows.push_back(r);
+        rlev.push_back(lmax + 1);
+        tcol.clear();
+        tval.clear();
+    };
+    size_t bi = 0;  // next block in scan order
+    std::vector<int> yid;
+    for (int q = 0; q < n; ++q) {
+        const int r = upper ? n - 1 - q : q;
+        const bool at_block = bi < blocks.size() && (upper ? blocks[bi].b - 1 == r : blocks[bi].a == r);
+        if (!at_block) {
+            for (int k = ptr[r]; k < ptr[r + 1]; ++k) {
+                tcol.push_back(col[k]);
+                tval.push_back(val[k]);
+            }
+            emit(r, in_index[r], upper ? diag[r] : 1.0);
+            continue;
+        }
+        const Block B = blocks[bi];
+        const std::vector<double>& inv = invs[bi];
+        ++bi;
+        const int s = B.b - B.a;
+        ++P.n_blocks;
+        P.block_rows += s;
+        P.max_block = std::max(P.max_block, s);
+        yid.assign(s, -1);
+        // y rows: the external part of every block row
+        for (int z = 0; z < s; ++z) {
+            const int i = upper ? s - 1 - z : z;
+            const int rr = B.a + i;
+            for (int k = ptr[rr]; k < ptr[rr + 1]; ++k) {
+                const int c = col[k];
+                if (c >= B.a && c < B.b) continue;
+                tcol.push_back(c);
+                tval.push_back(val[k]);
+            }
+            yid[i] = new_id();
+            emit(yid[i], in_index[rr], 1.0);
+        }
+        // x rows: x_i = sum_k inv_ik y_k  (stored as out = 0 - sum (-inv) y)
+        for (int z = 0; z < s; ++z) {
+            const int i = upper ? s - 1 - z : z;
+            const int k0 = upper ? i : 0, k1 = upper ? s : i + 1;
+            for (int k = k0; k < k1; ++k) {
+                const double v = inv[(size_t)i * s + k];
+                if (v == 0.0) continue;
+                tcol.push_back(yid[k]);
+                tval.push_back(-v);
+            }
+            emit(B.a + i, -1, 1.0);
+        }
+        q += s - 1;
+    }
+    P.n_aug = next_id;
+    // ---- positions by level (stable: creation order within a level)
+    int nl = 0;
+    for (int v : rlev) nl = std::max(nl, v + 1);
+    P.levels = nl;
+    std::vector<long long> lstart(nl + 1, 0);
+    for (int v : rlev) lstart[v + 1]++;
+    for (int l = 0; l < nl; ++l) lstart[l + 1] += lstart[l];
+    std::vector<int> pos_row(rows.size());
+    {
+        std::vector<long long> fillp(lstart.begin(), lstart.end() - 1);
+        for (size_t i = 0; i < rows.size(); ++i) pos_row[fillp[rlev[i]]++] = (int)i;
+    }
+    P.meta.resize(4 * rows.size());
+    P.col.reserve(ecol.size());
+    P.val.reserve(eval.size());
+    P.diag.assign(P.n_aug, 1.0);
+    for (size_t p = 0; p < rows.size(); ++p) {
+        const Row& r = rows[pos_row[p]];
+        P.meta[4 * p] = r.out;
+        P.meta[4 * p + 1] = r.in;
+        P.meta[4 * p + 2] = (int)P.col.size();
+        for (long long k = r.e0; k < r.e1; ++k) {
+            P.col.push_back(ecol[k]);
+            P.val.push_back(eval[k]);
+        }
+        if (P.col.size() > (size_t)INT32_MAX) throw std::runtime_error("augmented plan: too many entries");
+        P.meta[4 * p + 3] = (int)P.col.size();
+        P.diag[r.out] = r.dg;
+    }
+    // ---- warp tasks (as make_tasks, FAST): long rows alone; short rows
+    // grouped within one level and one length class, 1..8 lanes per row
+    P.level_first_task.assign(nl + 1, 0);
+    int g0 = -1, gc = 0, glev = -1, glg = -1;
+    auto flush = [&]() {
+        if (gc) {
+            P.tasks.push_back(g0);
+            P.tasks.push_back(gc | (glg << 8));
+        }
+        gc = 0;
+    };
+    int cur_level = -1;
+    for (size_t p = 0; p < rows.size(); ++p) {
+        const int lv = rlev[pos_row[p]];
+        if (lv != cur_level) {
+            flush();
+            for (int l = cur_level + 1; l <= lv; ++l) P.level_first_task[l] = (int)P.tasks.size() / 2;
+            cur_level = lv;
+        }
+        const int len = P.meta[4 * p + 3] - P.meta[4 * p + 2];
+        if (len > 32) {
+            flush();
+            P.tasks.push_back((int)p);
+            P.tasks.push_back(1 | (1 << 30));
+            continue;
+        }
+        const int lg = len <= 4 ? 0 : len <= 8 ? 1 : len <= 16 ? 2 : 3;
+        if (gc && (lg != glg || (gc + 1) << lg > 32)) flush();
+        if (!gc) {
+            g0 = (int)p;
+            glev = lv;
+            glg = lg;
+        }
+        ++gc;
+    }
+    flush();
+    for (int l = cur_level + 1; l <= nl; ++l) P.level_first_task[l] = (int)P.tasks.size() / 2;
+    (void)glev;
+}
+
+void eval_aug_plan(const AugPlan& P, bool upper, const double* in, double* out) {
+    const size_t np = P.meta.size() / 4;
+    for (size_t p = 0; p < np; ++p) {
+        const int o = P.meta[4 * p], i = P.meta[4 * p + 1];
+        double s = i >= 0 ? in[i] : 0.0;
+        for (int k = P.meta[4 * p + 2]; k < P.meta[4 * p + 3]; ++k) s -= P.val[k] * out[P.col[k]];
+        if (upper) s = s / P.diag[o];
+        out[o] = s;
+    }
+}
+
+}  // namespace exg

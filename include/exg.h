@@ -197,6 +197,11 @@ exg_status exg_profile_enable(exg_ctx* ctx, int on);
  * (start, end) of the warp-task sweeps for L then U (4n), then (start,
  * far-done, end) of the cluster sweeps for L then U (6n); zero = not run there */
 exg_status exg_debug_trace_solve(exg_ctx* ctx, const double* b, unsigned long long* times);
+/* debug: one FAST solve pair over the stream plan (k_trsv4) with 5 values per
+ * warp task {level, begin, dependencies ready, published (ns, %globaltimer),
+ * warp}, L's tasks then U's.  counts (6): tasks of L, U; warps of L, U; stream
+ * bytes of L, U.  Call with times == NULL to size the buffer. */
+exg_status exg_debug_trace_stream(exg_ctx* ctx, const double* b, unsigned long long* times, long long* counts);
 exg_status exg_profile_get(exg_ctx* ctx, exg_kernel_times* out); /* synchronises; resets */
 
 exg_status exg_counters_get(exg_ctx* ctx, exg_counters* out);

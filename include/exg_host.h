@@ -168,6 +168,18 @@ exg_status exg_aug_plan_solve(int upper, int n, const int* ptr, const int* col, 
                               const double* diag, const int* in_index, const int* params,
                               const double* b, double* x, long long* stats);
 
+/* The same augmented system cut into the per-warp record streams k_trsv4
+ * consumes (trsv_plan.hpp), evaluated on the CPU in global task order with the
+ * kernel's arithmetic.  out_index (may be null): epilogue index per row
+ * (U: col_perm); final_out/add (may be null), coef: the fused epilogue
+ * final_out[q] = add[q] + coef * x.  params (may be null): {min_block,
+ * max_block}.  stats (may be null): {orig_levels, levels, n_aug, n_tasks,
+ * n_rows, n_entries, n_slots, stream bytes, max record bytes, n_partials}. */
+exg_status exg_stream_plan_solve(int upper, int n, const int* ptr, const int* col, const double* val,
+                                 const double* diag, const int* in_index, const int* out_index,
+                                 const int* params, int n_warps, const double* b, double* x,
+                                 double* final_out, double coef, const double* add, long long* stats);
+
 /* ---- transient (the reference's time-stepping loop, ER / ERC) ------------ */
 
 enum { EXG_METHOD_ER = 1, EXG_METHOD_ERC = 2 };

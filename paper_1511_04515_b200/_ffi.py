@@ -136,6 +136,8 @@ _HOST_PROTOS = {
     "exg_lu_factor": (I, [I, PI, PI, PD, D, C.POINTER(P)]),
     "exg_factor_free": (None, [P]),
     "exg_aug_plan_solve": (I, [I, I, PI, PI, PD, PD, PI, PI, PD, PD, C.POINTER(C.c_longlong)]),
+    "exg_stream_plan_solve": (I, [I, I, PI, PI, PD, PD, PI, PI, PI, I, PD, PD, PD, D, PD,
+                                  C.POINTER(C.c_longlong)]),
     "exg_factor_get": (I, [P, PI, C.POINTER(PI), C.POINTER(PI), C.POINTER(PD), C.POINTER(PI),
                            C.POINTER(PI), C.POINTER(PD), C.POINTER(PI), C.POINTER(PI)]),
     "exg_factor_timing": (I, [P, PD, PD]),
@@ -168,6 +170,7 @@ _DEV_PROTOS = {
     "exg_counters_reset": (I, [P]),
     "exg_profile_enable": (I, [P, I]),
     "exg_debug_trace_solve": (I, [P, PD, C.POINTER(C.c_uint64)]),
+    "exg_debug_trace_stream": (I, [P, PD, C.POINTER(C.c_uint64), C.POINTER(C.c_longlong)]),
     "exg_profile_get": (I, [P, C.POINTER(exg_kernel_times)]),
     "exg_synchronize": (I, [P]),
     "exg_device_alloc": (I, [P, C.c_size_t, C.POINTER(P)]),

@@ -123,6 +123,19 @@ void ensure_inputs(exg_ctx* c, int ni) {
     c->n_inputs = ni;
 }
 
+// exchange slots of k_mgs2 for bases of up to mmax columns
+void ensure_mgs_slots(exg_ctx* c, int mmax) {
+    const int need = 2 * (mmax + 1) + 3;
+    if (c->mgs_slots && c->mgs_inst_cap >= need) return;
+    c->clear_graphs();
+    dfree(c->mgs_slots);
+    const size_t doubles = 8 + (size_t)2 * need * c->num_sms * exg::dev::kMgs2BMax;
+    c->mgs_slots = dalloc<double>(doubles);
+    ck(cudaMemsetAsync(c->mgs_slots, 0xFF, doubles * sizeof(double), c->stream), "mgs slots");
+    ck(cudaMemsetAsync(c->mgs_slots, 0, 64, c->stream), "mgs slots");
+    c->mgs_inst_cap = need;
+}
+
 void ensure_krylov(exg_ctx* c, int mmax) {
     if (c->mmax_alloc >= mmax && c->V) return;
     c->clear_graphs();
@@ -134,6 +147,8 @@ void ensure_krylov(exg_ctx* c, int mmax) {
     dfree(c->dscratch);
     c->ldv = ((long long)n + 31) / 32 * 32;
     c->V = dalloc<double>((size_t)(mmax + 1) * c->ldv);
+    // the ldv padding of every column stays zero (k_mgs2 streams whole tiles)
+    ck(cudaMemsetAsync(c->V, 0, (size_t)(mmax + 1) * c->ldv * sizeof(double), c->stream), "basis clear");
     c->hld = mmax + 2;
     c->hbar = dalloc<double>((size_t)(mmax + 1) * c->hld);
     c->hinv = dalloc<double>((size_t)mmax * mmax);
@@ -163,8 +178,8 @@ void solve_dev(exg_ctx* c, const double* b, double* final_out, double coef, cons
     const size_t chain_doubles = fast ? (size_t)(c->plan[0].chain_rows + c->plan[1].chain_rows +
                                                  c->plan[0].chain_slots + c->plan[1].chain_slots) : 0;
     // output of each sweep: n unknowns, or the augmented system's n_aug
-    const size_t ny = fast && c->plan[0].n_atasks ? (size_t)c->plan[0].n_aug : (size_t)n;
-    const size_t nx = fast && c->plan[1].n_atasks ? (size_t)c->plan[1].n_aug : (size_t)n;
+    const size_t ny = fast && c->plan[0].n_aug ? (size_t)c->plan[0].n_aug : (size_t)n;
+    const size_t nx = fast && c->plan[1].n_aug ? (size_t)c->plan[1].n_aug : (size_t)n;
     exg::dev::fill_ones(c->L(), c->trsv_buf, kTrsvHdr + sizeof(double) * (ny + nx + chain_doubles));
     unsigned int* tickets = reinterpret_cast<unsigned int*>(c->trsv_buf);
     double* y = reinterpret_cast<double*>(c->trsv_buf + kTrsvHdr);
@@ -202,6 +217,23 @@ void solve_dev(exg_ctx* c, const double* b, double* final_out, double coef, cons
             exg::dev::trsv(c->L(), upper, fast, a);
         } else {
             const TriPlan& P = c->plan[tri];
+            if (P.s_warps) {
+                // per-warp record streams of the blocked augmented system
+                exg::dev::StreamArgs sa{};
+                sa.data = P.sdata;
+                sa.warp_off = P.swarp_off;
+                sa.n_warps = P.s_warps;
+                sa.in = a.in;
+                sa.out = a.out;
+                sa.final_out = a.final_out;
+                sa.add = a.add;
+                sa.coef = a.coef;
+                sa.ctrl = ctrl;
+                sa.trace = a.trace;
+                ck(exg::dev::trsv_stream(c->L(), upper, sa), "stream solve launch");
+                c->prof_end(upper ? EXG_K_TRSV_U : EXG_K_TRSV_L, e0);
+                continue;
+            }
             if (P.n_atasks) {
                 // blocked augmented system: one sync-free warp-task launch
                 a.tasks = P.atasks;
@@ -387,9 +419,19 @@ void mevp_dev(exg_ctx* c, const double* v, double h, const exg_mevp_cfg& cfg, in
         blocks = std::min(blocks, 4096);
     }
     exg::dev::MgsArgs ma{n, c->ldv, c->V, c->w, c->hbar, c->hld, c->partials + c->mgs_partials_off, c->bar, c->ctrl};
+    // FAST mode: grouped Gram-Schmidt with streamed basis tiles (k_mgs2);
+    // EXG_MGS=1 keeps the column-by-column kernel, EXG_MGS_B sets the group size
+    exg::dev::Mgs2Shape ms{};
+    static const bool mgs_v1 = getenv("EXG_MGS") && atoi(getenv("EXG_MGS")) == 1;
+    static const int mgs_b = getenv("EXG_MGS_B") ? atoi(getenv("EXG_MGS_B")) : 0;
+    const bool use_mgs2 = c->opt.trsv_mode == EXG_TRSV_FAST && !mgs_v1 && exg::dev::mgs2_shape(n, c->num_sms, mgs_b, &ms);
+    if (use_mgs2) ensure_mgs_slots(c, cfg.m_max);
+    exg::dev::Mgs2Args ma2{n, c->ldv, c->V, c->w, c->hbar, c->hld, c->mgs_slots ? c->mgs_slots + 8 : nullptr,
+                           reinterpret_cast<unsigned int*>(c->mgs_slots), c->ctrl, c->mgs_inst_cap, 0, 0, 0};
     exg::dev::DenseArgs da{c->ctrl, c->hbar, c->hld, c->hinv, c->coef, c->dscratch, 0, 0, h};
     const bool gspmv = c->opt.weight_mode == EXG_WEIGHT_GSPMV;
     if (gspmv) mat(c, EXG_MAT_G);
+    static const bool side_ok = !(getenv("EXG_NO_FORK") && atoi(getenv("EXG_NO_FORK")));
     // one Arnoldi iteration (krylov.cpp:118-168); every kernel takes j, m and
     // the stop decision from the control block, so the same launches serve
     // the eager loop and the graph body.  dense_m bounds the dimension the
@@ -404,16 +446,35 @@ void mevp_dev(exg_ctx* c, const double* v, double h, const exg_mevp_cfg& cfg, in
         c->prof_end(EXG_K_SPMV, p0);
         solve_dev(c, c->t, c->w, -1.0, nullptr, c->ctrl);
         cudaEvent_t p1 = c->prof_begin();
-        ck(exg::dev::mgs(L, ma, blocks, K), "mgs launch");
+        if (use_mgs2)
+            ck(exg::dev::mgs2(L, ma2, ms), "mgs2 launch");
+        else
+            ck(exg::dev::mgs(L, ma, blocks, K), "mgs launch");
         c->prof_end(EXG_K_MGS, p1);
+        // the dense block (one CTA, latency-bound) and the residual weight (a
+        // streaming pass over G or the factors) only share the iteration's
+        // control block fields they each own: they run side by side, the
+        // weight on the side stream (forked and joined through events, which
+        // the graph capture records as parallel branches)
+        const bool fork = !c->profiling && gspmv && side_ok;
+        if (fork) {
+            ck(cudaEventRecord(c->ev_fork, c->stream), "fork");
+            ck(cudaStreamWaitEvent(c->side_stream, c->ev_fork, 0), "fork");
+        }
         cudaEvent_t p2 = c->prof_begin();
         exg::dev::dense(L, da, dense_m);
         c->prof_end(EXG_K_DENSE, p2);
         cudaEvent_t p3 = c->prof_begin();
         if (gspmv) {
             const DCsr& G = c->mats[EXG_MAT_G];
-            exg::dev::spmv_norm(L, G.rowptr, G.col, G.val, n, c->V, c->ldv, c->partials, c->done,
-                                c->ctrl, 1, nullptr);
+            exg::dev::Launch Ls = L;
+            if (fork) Ls.stream = c->side_stream;
+            exg::dev::spmv_norm(Ls, G.rowptr, G.col, G.val, n, c->V, c->ldv, c->partials, c->done,
+                                c->ctrl, fork ? 2 : 1, nullptr);
+            if (fork) {
+                ck(cudaEventRecord(c->ev_join, c->side_stream), "join");
+                ck(cudaStreamWaitEvent(c->stream, c->ev_join, 0), "join");
+            }
         } else {
             apply_dev(c, nullptr, nullptr, c->ctrl, nullptr);
         }
@@ -430,11 +491,11 @@ void mevp_dev(exg_ctx* c, const double* v, double h, const exg_mevp_cfg& cfg, in
             const void* ps[] = {C.rowptr, C.col, C.val, G.rowptr, G.col, G.val, c->V, c->w, c->t,
                                 c->hbar, c->hinv, c->coef, c->dscratch, c->partials, c->bar,
                                 c->done, c->ctrl, c->trsv_buf, c->l_ptr, c->u_ptr, c->tmp, c->t3,
-                                c->v1, c->weight};
+                                c->v1, c->mgs_slots};
             static_assert(sizeof(ps) / sizeof(ps[0]) <= 24, "graph key");
             for (size_t i = 0; i < sizeof(ps) / sizeof(ps[0]); ++i) key.p[i] = ps[i];
-            const long long vs[] = {n, c->ldv, blocks, K, cfg.m_max, c->opt.trsv_mode, c->opt.weight_mode,
-                                    C.n_rows};
+            const long long vs[] = {n, c->ldv, use_mgs2 ? -ms.B : blocks, K, cfg.m_max, c->opt.trsv_mode,
+                                    c->opt.weight_mode, C.n_rows};
             for (size_t i = 0; i < 8; ++i) key.v[i] = vs[i];
             exg_ctx::ArnoldiGraph* g = nullptr;
             for (auto& e : c->graphs)
@@ -980,6 +1041,9 @@ exg_status exg_create(int device, exg_ctx** out) {
     c->device = device;
     ck(cudaSetDevice(device), "cudaSetDevice");
     ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+    ck(cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking), "side stream");
+    ck(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming), "event");
+    ck(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming), "event");
     cudaDeviceProp prop;
     ck(cudaGetDeviceProperties(&prop, device), "props");
     if (prop.major < 10) throw ApiError{EXG_E_CUDA, "exsim-B200 requires an sm_100a (Blackwell) GPU"};
@@ -1030,7 +1094,7 @@ void exg_destroy(exg_ctx* c) {
     double* dp[] = {c->l_val, c->u_val, c->u_diag, c->vin, c->vout, c->t, c->w, c->xk, c->xnext,
                     c->gb, c->startv, c->v1, c->t1, c->t2, c->t3, c->tmp, c->u_k, c->u_k1, c->V,
                     c->hbar, c->hinv, c->coef, c->dscratch, c->partials, c->weight, c->probe_out,
-};
+                    c->mgs_slots};
     for (double* p : dp)
         if (p) cudaFree(p);
     if (c->trsv_buf) cudaFree(c->trsv_buf);
@@ -1061,6 +1125,9 @@ void exg_destroy(exg_ctx* c) {
         cudaEventDestroy(pe.second.second);
     }
     for (cudaEvent_t e : c->event_pool) cudaEventDestroy(e);
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
+    if (c->side_stream) cudaStreamDestroy(c->side_stream);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -1334,9 +1401,53 @@ exg_status exg_set_factors(exg_ctx* c, int n, const int* Lp, const int* Li, cons
     // levels (one thread-block cluster, DSMEM hand-offs)
     // FAST plan: the blocked augmented system (default, trsv_plan.hpp), or
     // the level-run plan (wide runs + cluster chain, EXG_FAST_PLAN=chain)
-    const char* fp_env = getenv("EXG_FAST_PLAN");
-    const bool use_aug = !(fp_env && std::string(fp_env) == "chain");
-    if (!use_aug) {
+    const char* fp_env = getenv("EXG_FAST_PLAN");  // stream (default) | aug | chain
+    const std::string fplan = fp_env ? fp_env : "stream";
+    const bool use_aug = fplan != "chain";
+    if (fplan == "stream") {
+        // per-warp record streams (k_trsv4) over the augmented system with
+        // every row cut to <= 128 entries
+        exg::AugParams prm = exg::stream_aug_params();
+        if (const char* e = getenv("EXG_AUG_BLOCK")) sscanf(e, "%d,%d", &prm.min_block, &prm.max_block);
+        std::vector<int> ident(n);
+        for (int i = 0; i < n; ++i) ident[i] = i;
+        for (int tri = 0; tri < 2; ++tri) {
+            TriPlan& P = c->plan[tri];
+            P.free_dev();
+            P.runs.clear();
+            exg::StreamParams sp;
+            sp.n_warps = exg::dev::trsv_stream_warps(tri == 1, c->num_sms);
+            if (sp.n_warps <= 0) throw ApiError{EXG_E_CUDA, "k_trsv4 cannot be launched on this device"};
+            exg::StreamPlan S;
+            {
+                exg::AugPlan A;
+                if (tri == 0)
+                    exg::build_aug_plan(false, n, lp.data(), lc.data(), lv.data(), nullptr, row_perm, prm, A);
+                else
+                    exg::build_aug_plan(true, n, up.data(), uc.data(), uv.data(), ud.data(), ident.data(), prm, A);
+                // small systems: no more warps than tasks would keep busy
+                exg::build_stream_plan(A, tri == 1, tri == 1 ? col_perm : nullptr, sp, S);
+                c->cnt_aug[tri][1] = A.n_blocks;
+                c->cnt_aug[tri][2] = A.block_rows;
+                c->cnt_aug[tri][3] = A.n_partials;
+            }
+            P.sdata = dalloc<unsigned char>(std::max<size_t>(S.data.size(), 16));
+            P.swarp_off = dalloc<long long>(S.warp_off.size());
+            ck(cudaMemcpyAsync(P.sdata, S.data.data(), S.data.size(), cudaMemcpyHostToDevice, c->stream), "stream plan");
+            ck(cudaMemcpyAsync(P.swarp_off, S.warp_off.data(), S.warp_off.size() * sizeof(long long),
+                               cudaMemcpyHostToDevice, c->stream), "stream plan");
+            ck(cudaStreamSynchronize(c->stream), "stream plan sync");  // S is released below
+            P.s_warps = S.n_warps;
+            P.s_bytes = (long long)S.data.size();
+            P.n_aug = S.n_aug;
+            P.aug_levels = S.levels;
+            c->cnt_aug[tri][0] = S.levels;
+            c->cnt_aug[tri][4] = S.n_entries;
+            c->cnt_aug[tri][5] = S.n_tasks;
+            c->cnt_aug[tri][6] = (long long)S.data.size();
+            c->cnt_aug[tri][7] = S.n_warps;
+        }
+    } else if (!use_aug) {
         plan_triangle(c, c->plan[0], false, lford, lflev, lnl_f, lp, lc, lv, ltasks_f, nullptr, nullptr, l_sub);
         plan_triangle(c, c->plan[1], true, uford, uflev, unl_f, up, uc, uv, utasks_f, &ud, col_perm, u_sub);
         build_sub(c, c->plan[0].sub, false, lcomp, lncomp, lp, lc, lv, row_perm);
@@ -1826,6 +1937,40 @@ exg_status exg_debug_trace_solve(exg_ctx* c, const double* b, unsigned long long
     ck(cudaStreamSynchronize(c->stream), "sync");
     cudaFree(tr);
     cudaFree(ntr);
+    API_END(c)
+}
+
+// debug: one stream-plan solve pair with per-task timestamps (k_trsv4):
+// 5 values per task {level, begin, dependencies ready, published, warp}, L's
+// tasks then U's.  counts[0..1]: tasks of L and U (call with times == null
+// first to size the buffer); counts[2..3]: warps; counts[4..5]: stream bytes.
+exg_status exg_debug_trace_stream(exg_ctx* c, const double* b, unsigned long long* times, long long* counts) {
+    API_BEGIN
+    require_factors(c);
+    if (!c->plan[0].s_warps || !c->plan[1].s_warps || c->opt.trsv_mode != EXG_TRSV_FAST)
+        throw ApiError{EXG_E_CONTRACT, "exg_debug_trace_stream: FAST mode with the stream plan only"};
+    const long long nl = c->cnt_aug[0][5], nu = c->cnt_aug[1][5];
+    if (counts) {
+        counts[0] = nl;
+        counts[1] = nu;
+        counts[2] = c->plan[0].s_warps;
+        counts[3] = c->plan[1].s_warps;
+        counts[4] = c->plan[0].s_bytes;
+        counts[5] = c->plan[1].s_bytes;
+    }
+    if (times) {
+        const int n = c->n;
+        unsigned long long* tr = dalloc<unsigned long long>((size_t)5 * (nl + nu));
+        ck(cudaMemsetAsync(tr, 0, sizeof(unsigned long long) * 5 * (size_t)(nl + nu), c->stream), "memset");
+        c->trace_l = tr;
+        c->trace_u = tr + 5 * (size_t)nl;
+        const double* bd = resolve_in(c, b, n, EXG_PTR_HOST, c->vin);
+        solve_dev(c, bd, c->vout, 1.0, nullptr, nullptr);
+        c->trace_l = c->trace_u = nullptr;
+        ck(cudaMemcpyAsync(times, tr, sizeof(unsigned long long) * 5 * (size_t)(nl + nu), cudaMemcpyDeviceToHost, c->stream), "d2h");
+        ck(cudaStreamSynchronize(c->stream), "sync");
+        cudaFree(tr);
+    }
     API_END(c)
 }
 

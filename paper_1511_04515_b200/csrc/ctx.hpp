@@ -83,7 +83,18 @@ struct TriPlan {
     int n_atasks = 0;
     long long n_aug = 0;
     int aug_levels = 0;
+    // per-warp record streams of the augmented system (k_trsv4); used when s_warps > 0
+    unsigned char* sdata = nullptr;
+    long long* swarp_off = nullptr;
+    int s_warps = 0;
+    long long s_bytes = 0;
     void free_aug() {
+        if (sdata) cudaFree(sdata);
+        if (swarp_off) cudaFree(swarp_off);
+        sdata = nullptr;
+        swarp_off = nullptr;
+        s_warps = 0;
+        s_bytes = 0;
         void* ps[] = {ameta, atasks, acol, aval, adiag};
         for (void* p : ps)
             if (p) cudaFree(p);
@@ -114,6 +125,8 @@ struct TriPlan {
 struct exg_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t side_stream = nullptr;  // residual weight beside the dense block (mevp_dev)
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int num_sms = 148;
     long long launches = 0;
     exg_counters cnt{};
@@ -160,7 +173,7 @@ struct exg_ctx {
     unsigned long long *ntrace_l = nullptr, *ntrace_u = nullptr;
     // solve scratch: [2 tickets + pad (16 B)][y n][x n], memset to 0xFF per solve
     char* trsv_buf = nullptr;
-    long long cnt_aug[2][5] = {};  // per triangle: levels, blocks, block rows, partials, entries
+    long long cnt_aug[2][8] = {};  // per triangle: levels, blocks, block rows, partials, entries, tasks, stream bytes, warps
     // n-vectors
     int vec_n = 0;
     double *vin = nullptr, *vout = nullptr, *t = nullptr, *w = nullptr, *xk = nullptr,
@@ -177,6 +190,9 @@ struct exg_ctx {
     size_t mgs_partials_off = 0;
     unsigned int *bar = nullptr, *done = nullptr;
     double* weight = nullptr;
+    // k_mgs2 exchange slots: [seq counter, 64 B][2 sets x mgs_inst_cap x num_sms x kMgs2BMax]
+    double* mgs_slots = nullptr;
+    int mgs_inst_cap = 0;
     exg::dev::Ctrl* ctrl = nullptr;
     exg::dev::Ctrl* h_ctrl = nullptr;  // pinned mirror
     bool basis_valid = false;

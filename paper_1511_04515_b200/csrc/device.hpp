@@ -32,6 +32,20 @@ struct TrsvArgs {
     const int4* meta;   // v3: per level-order position {row, b index, k0, k1}
 };
 
+// k_trsv4 (trsv_stream.cu): per-warp record streams of one triangle
+struct StreamArgs {
+    const unsigned char* data;   // all streams (trsv_plan.hpp record format)
+    const long long* warp_off;   // n_warps + 1 byte offsets (page multiples)
+    int n_warps;
+    const double* in;            // right-hand side (L: b, gathered through the baked row_perm; U: L's output)
+    double* out;                 // n_aug results, sentinel-initialised
+    double* final_out;           // U: fused epilogue final_out[q] = (add ? add[q] : 0) + coef * x
+    const double* add;
+    double coef;
+    const Ctrl* ctrl;
+    unsigned long long* trace;   // debug: 5 values per task, or null
+};
+
 struct SubArgs {
     int n_comps;
     int max_rows;         // shared-memory slots (largest component)
@@ -93,6 +107,26 @@ struct MgsArgs {
     Ctrl* ctrl;
 };
 
+// k_mgs2 (mgs.cu): grouped Gram-Schmidt with TMA-streamed basis tiles (FAST mode)
+constexpr int kMgs2BMax = 4;
+struct Mgs2Args {
+    int n;
+    long long ldv;
+    double* V;
+    const double* w;
+    double* hbar;
+    int hld;
+    double* slots;       // 2 sets x inst_cap x grid x kMgs2BMax partial-sum slots (sentinel-initialised)
+    unsigned int* seq;   // launch counter (selects the slot set)
+    Ctrl* ctrl;
+    int inst_cap;        // exchanges one launch may need: 2 (m_max + 1) + 3
+    int tile, S, B;      // filled by mgs2 from the shape
+};
+struct Mgs2Shape {
+    int grid, tile, S, B;
+    size_t smem;
+};
+
 struct DenseArgs {
     Ctrl* ctrl;
     const double* hbar;
@@ -130,6 +164,8 @@ void erc_update(const Launch& L, const double* w, const double* value, const dou
 void trsv(const Launch& L, bool upper, bool reverse, const TrsvArgs& a);
 cudaError_t trsv_wide(const Launch& L, bool upper, const TrsvArgs& a);
 cudaError_t trsv_chain(const Launch& L, bool upper, const ChainArgs& a);
+int trsv_stream_warps(bool upper, int num_sms);  // co-resident warps of k_trsv4 (0 = cannot launch)
+cudaError_t trsv_stream(const Launch& L, bool upper, const StreamArgs& a);
 cudaError_t trsv_sub(const Launch& L, bool upper, const SubArgs& a);
 void apply_tasks(const Launch& L, const int2* utasks, int n_utasks, const int* uorder,
                  const int2* ltasks, int n_ltasks, const int* lorder, const int* uptr,
@@ -145,6 +181,8 @@ void start(const Launch& L, const double* v, const double* xk, int n, double* pa
            double* v0, Ctrl* ctrl, int er_mode);
 int mgs_max_blocks(int K);
 cudaError_t mgs(const Launch& L, const MgsArgs& a, int n_blocks, int K);
+bool mgs2_shape(int n, int num_sms, int b_override, Mgs2Shape* s);
+cudaError_t mgs2(const Launch& L, Mgs2Args a, const Mgs2Shape& s);
 void dense(const Launch& L, const DenseArgs& a, int m);
 void iter_end(const Launch& L, Ctrl* ctrl, unsigned long long cond = 0);
 void fill_ones(const Launch& L, void* p, size_t bytes);

@@ -269,4 +269,37 @@ exg_status exg_aug_plan_solve(int upper, int n, const int* ptr, const int* col, 
     HOST_GUARD_END
 }
 
+exg_status exg_stream_plan_solve(int upper, int n, const int* ptr, const int* col, const double* val,
+                                 const double* diag, const int* in_index, const int* out_index,
+                                 const int* params, int n_warps, const double* b, double* x,
+                                 double* final_out, double coef, const double* add, long long* stats) {
+    HOST_GUARD_BEGIN
+    if (n < 0 || !ptr || (upper && !diag) || !in_index || n_warps < 1)
+        throw exg::Error{EXG_E_CONTRACT, "exg_stream_plan_solve: bad arguments"};
+    exg::AugParams prm = exg::stream_aug_params();
+    if (params) {
+        prm.min_block = params[0];
+        prm.max_block = params[1];
+    }
+    if (prm.max_block < 1) throw exg::Error{EXG_E_CONTRACT, "exg_stream_plan_solve: bad plan parameters"};
+    exg::AugPlan P;
+    exg::build_aug_plan(upper != 0, n, ptr, col, val, diag, in_index, prm, P);
+    exg::StreamParams sp;
+    sp.n_warps = n_warps;
+    sp.min_tasks_per_warp = 0;  // exactly the caller's warp count
+    exg::StreamPlan S;
+    exg::build_stream_plan(P, upper != 0, out_index, sp, S);
+    if (b && x) {
+        std::vector<double> out(S.n_aug, 0.0);
+        exg::eval_stream_plan(S, upper != 0, b, out.data(), final_out, coef, add);
+        std::memcpy(x, out.data(), sizeof(double) * n);
+    }
+    if (stats) {
+        const long long st[10] = {P.orig_levels, S.levels,    S.n_aug,   S.n_tasks,           S.n_rows,
+                                  S.n_entries,   S.n_slots,   (long long)S.data.size(), S.max_record, P.n_partials};
+        std::memcpy(stats, st, sizeof st);
+    }
+    HOST_GUARD_END
+}
+
 }  // extern "C"

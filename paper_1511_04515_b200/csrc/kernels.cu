@@ -1366,8 +1366,13 @@ __global__ void __launch_bounds__(256)
     __shared__ double sh[33];
     __shared__ bool s_last;
     const double* x = vbase;
+    // from_ctrl_m 1: after the dense block (skips when no residual test is
+    // pending, decides here); 2: beside the dense block (need_weight is being
+    // written concurrently: always computes, k_iter_end decides)
     if (ctrl && from_ctrl_m) {
-        if (!ctrl->need_weight || ctrl->converged || ctrl->status) return;
+        if (ctrl->converged || ctrl->status) return;
+        if (from_ctrl_m == 1 && !ctrl->need_weight) return;
+        if (ctrl->happy) return;  // no v_{m+1} was written (set by the MGS kernel)
         x = vbase + (long long)ctrl->m * ldv;
     }
     // grid-stride rows (a few partials per SM, not one per 256 rows: the
@@ -1395,7 +1400,7 @@ __global__ void __launch_bounds__(256)
         if (weight_out) *weight_out = w;
         if (ctrl && from_ctrl_m) {
             ctrl->weight = w;
-            decide(ctrl);
+            if (from_ctrl_m == 1) decide(ctrl);
         }
     }
 }

@@ -2,6 +2,8 @@
 #include "trsv_plan.hpp"
 
 #include <algorithm>
+#include <cmath>
+#include <cstring>
 #include <atomic>
 #include <numeric>
 #include <stdexcept>
@@ -171,14 +173,23 @@ void build_aug_plan(bool upper, int n, const int* ptr, const int* col, const dou
     // finalize one row whose entries are tcol/tval: partial sums for a long
     // history, then the row itself
     auto emit = [&](int out, int in, double dg) {
-        const int cnt = (int)tcol.size();
         int lmax = -1;
-        if (cnt > prm.chunk_over) {
+        // partial sums for a long history; with a cap the pass repeats (partials
+        // of partials) until the row fits
+        while ((int)tcol.size() > prm.chunk_over) {
+            const int cnt = (int)tcol.size();
             tmp.resize(cnt);
             for (int k = 0; k < cnt; ++k) tmp[k] = {level[tcol[k]], k};
             std::stable_sort(tmp.begin(), tmp.end(),
                              [](const std::pair<int, int>& x, const std::pair<int, int>& y) { return x.first < y.first; });
-            const int n_old = cnt - prm.recent;
+            int n_old = cnt - prm.recent;
+            if (prm.cap > 0) {
+                // full chunks from the oldest entries; the remainder and the
+                // partial references share the row: rem + chunks <= cap
+                int c = cnt / prm.chunk;
+                if (cnt - c * prm.chunk + c > prm.cap) ++c;
+                n_old = std::min(cnt, c * prm.chunk);
+            }
             std::vector<int> keep_c;
             std::vector<double> keep_v;
             for (int c0 = 0; c0 < n_old; c0 += prm.chunk) {
@@ -205,6 +216,7 @@ void build_aug_plan(bool upper, int n, const int* ptr, const int* col, const dou
             }
             tcol.swap(keep_c);
             tval.swap(keep_v);
+            if (prm.cap <= 0) break;
         }
         Row r{out, in, dg, (long long)ecol.size(), 0};
         // entries oldest first (L) / newest first (U: the kernel walks U rows
@@ -290,6 +302,7 @@ void build_aug_plan(bool upper, int n, const int* ptr, const int* col, const dou
         std::vector<long long> fillp(lstart.begin(), lstart.end() - 1);
         for (size_t i = 0; i < rows.size(); ++i) pos_row[fillp[rlev[i]]++] = (int)i;
     }
+    P.level_first_pos.assign(lstart.begin(), lstart.end());
     P.meta.resize(4 * rows.size());
     P.col.reserve(ecol.size());
     P.val.reserve(eval.size());
@@ -355,6 +368,178 @@ void eval_aug_plan(const AugPlan& P, bool upper, const double* in, double* out) 
         for (int k = P.meta[4 * p + 2]; k < P.meta[4 * p + 3]; ++k) s -= P.val[k] * out[P.col[k]];
         if (upper) s = s / P.diag[o];
         out[o] = s;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// per-warp record streams (trsv_plan.hpp)
+// ---------------------------------------------------------------------------
+namespace {
+
+inline int lanes_log2_for(int len) {  // smallest lg with len <= 4 * 2^lg
+    int lg = 0;
+    while (len > (4 << lg)) ++lg;
+    return lg;
+}
+
+template <typename T>
+inline void put(std::vector<unsigned char>& v, size_t at, T x) {
+    std::memcpy(v.data() + at, &x, sizeof(T));
+}
+template <typename T>
+inline T get(const unsigned char* p) {
+    T x;
+    std::memcpy(&x, p, sizeof(T));
+    return x;
+}
+
+}  // namespace
+
+void build_stream_plan(const AugPlan& P, bool upper, const int* out_index, const StreamParams& prm,
+                       StreamPlan& S) {
+    S = StreamPlan{};
+    if (prm.n_warps < 1 || prm.page < 16 || prm.page % 16 || prm.ring % prm.page)
+        throw std::runtime_error("stream plan: bad parameters");
+    const int MS = upper ? kStreamMetaU : kStreamMetaL;
+    S.n = P.n;
+    S.page = prm.page;
+    S.levels = P.levels;
+    S.n_aug = P.n_aug;
+    const size_t np = P.meta.size() / 4;
+    S.n_rows = (long long)np;
+    // ---- tasks: within a level rows are independent, so they are taken
+    // longest first and grouped by lane class
+    struct Task {
+        long long first;  // index into `ord`
+        int cnt, lg, nq, level;
+    };
+    std::vector<int> ord(np);
+    std::iota(ord.begin(), ord.end(), 0);
+    auto len_of = [&](int p) { return P.meta[4 * (size_t)p + 3] - P.meta[4 * (size_t)p + 2]; };
+    std::vector<Task> tasks;
+    for (int l = 0; l < P.levels; ++l) {
+        const long long a = P.level_first_pos[l], b = P.level_first_pos[l + 1];
+        std::stable_sort(ord.begin() + a, ord.begin() + b, [&](int x, int y) { return len_of(x) > len_of(y); });
+        long long i = a;
+        while (i < b) {
+            const int len = len_of(ord[i]);
+            if (len > 128) throw std::runtime_error("stream plan: a row exceeds 128 entries (AugParams.cap)");
+            const int lg = lanes_log2_for(len), per = 32 >> lg;
+            Task t{i, 0, lg, (len + (1 << lg) - 1) >> lg, l};
+            while (i < b && t.cnt < per && lanes_log2_for(len_of(ord[i])) == lg) {
+                ++t.cnt;
+                ++i;
+            }
+            tasks.push_back(t);
+        }
+    }
+    S.n_tasks = (long long)tasks.size();
+    int W = prm.n_warps;
+    if (prm.min_tasks_per_warp > 0) {
+        const long long want = ((long long)tasks.size() / prm.min_tasks_per_warp + 7) / 8 * 8;
+        W = (int)std::max<long long>(8, std::min<long long>(W, want));
+        W = std::min(W, prm.n_warps);
+    }
+    S.n_warps = W;
+    // ---- stream sizes
+    auto rec_bytes = [&](const Task& t) { return 16 + t.cnt * MS + t.nq * 32 * 12; };
+    std::vector<long long> bytes(W, 0);
+    for (size_t t = 0; t < tasks.size(); ++t) {
+        const int rb = rec_bytes(tasks[t]);
+        bytes[t % W] += rb;
+        S.max_record = std::max(S.max_record, rb);
+    }
+    if (2 * S.max_record + prm.page > prm.ring) throw std::runtime_error("stream plan: ring too small for two records");
+    S.warp_off.assign(W + 1, 0);
+    for (int w = 0; w < W; ++w) {
+        const long long padded = (bytes[w] + 16 + prm.page - 1) / prm.page * prm.page;  // + end marker
+        S.warp_off[w + 1] = S.warp_off[w] + padded;
+    }
+    S.data.assign((size_t)S.warp_off[W], 0);
+    std::vector<long long> cur(S.warp_off.begin(), S.warp_off.end() - 1);
+    for (size_t t = 0; t < tasks.size(); ++t) {
+        const Task& T = tasks[t];
+        const int rb = rec_bytes(T);
+        size_t at = (size_t)cur[t % W];
+        cur[t % W] += rb;
+        put<int>(S.data, at, T.cnt | (T.lg << 8) | (T.nq << 16));
+        put<int>(S.data, at + 4, rb);
+        put<int>(S.data, at + 8, T.level);
+        put<int>(S.data, at + 12, (int)t);
+        const size_t meta_at = at + 16, col_at = meta_at + (size_t)T.cnt * MS, val_at = col_at + (size_t)T.nq * 128;
+        for (int q = 0; q < T.nq * 32; ++q) put<int>(S.data, col_at + 4 * (size_t)q, -1);
+        const int lpr = 1 << T.lg;
+        for (int seg = 0; seg < T.cnt; ++seg) {
+            const int p = ord[T.first + seg];
+            const int out = P.meta[4 * (size_t)p], in = P.meta[4 * (size_t)p + 1];
+            const int k0 = P.meta[4 * (size_t)p + 2], k1 = P.meta[4 * (size_t)p + 3];
+            const size_t m = meta_at + (size_t)seg * MS;
+            put<int>(S.data, m, out);
+            put<int>(S.data, m + 4, in);
+            if (upper) {
+                put<int>(S.data, m + 8, (out_index && out < P.n) ? out_index[out] : -1);
+                put<int>(S.data, m + 12, 0);
+                put<double>(S.data, m + 16, P.diag[out]);
+            }
+            for (int e = 0; e < k1 - k0; ++e) {
+                const int sl = e & (lpr - 1), q = e >> T.lg;
+                const int slot = q * 32 + seg * lpr + sl;
+                put<int>(S.data, col_at + 4 * (size_t)slot, P.col[k0 + e]);
+                put<double>(S.data, val_at + 8 * (size_t)slot, P.val[k0 + e]);
+            }
+            S.n_entries += k1 - k0;
+        }
+        S.n_slots += T.nq * 32;
+    }
+}
+
+void eval_stream_plan(const StreamPlan& S, bool upper, const double* in, double* out, double* final_out,
+                      double coef, const double* add) {
+    const int W = S.n_warps, MS = upper ? kStreamMetaU : kStreamMetaL;
+    std::vector<long long> cur(S.warp_off.begin(), S.warp_off.end() - 1);
+    long long done = 0;
+    for (long long t = 0; done < W; ++t) {
+        const int w = (int)(t % W);
+        if (w == 0) done = 0;
+        const unsigned char* r = S.data.data() + cur[w];
+        const int w0 = get<int>(r);
+        if (w0 == 0) {  // this warp has finished (all later rounds too)
+            ++done;
+            continue;
+        }
+        const int cnt = w0 & 0xFF, lg = (w0 >> 8) & 0xFF, nq = (w0 >> 16) & 0xFF, lpr = 1 << lg;
+        cur[w] += get<int>(r + 4);
+        const unsigned char* meta = r + 16;
+        const unsigned char* cols = meta + (size_t)cnt * MS;
+        const unsigned char* vals = cols + (size_t)nq * 128;
+        double acc[32];
+        for (int lane = 0; lane < 32; ++lane) {
+            double a = 0.0;
+            for (int q = 0; q < nq; ++q) {
+                const int c = get<int>(cols + 4 * (size_t)(q * 32 + lane));
+                if (c >= 0) a = std::fma(get<double>(vals + 8 * (size_t)(q * 32 + lane)), out[c], a);
+            }
+            acc[lane] = a;
+        }
+        for (int o = lpr >> 1; o > 0; o >>= 1) {
+            double nx[32];
+            for (int lane = 0; lane < 32; ++lane) nx[lane] = acc[lane] + acc[lane ^ o];
+            std::memcpy(acc, nx, sizeof nx);
+        }
+        for (int seg = 0; seg < cnt; ++seg) {
+            const unsigned char* m = meta + (size_t)seg * MS;
+            const int o = get<int>(m), i = get<int>(m + 4);
+            double s = (i >= 0 ? in[i] : 0.0) - acc[seg * lpr];
+            if (upper) s = s / get<double>(m + 16);
+            out[o] = s;
+            if (upper && final_out) {
+                const int qq = get<int>(m + 8);
+                if (qq >= 0) {
+                    const double y = coef * s;
+                    final_out[qq] = add ? add[qq] + y : y;
+                }
+            }
+        }
     }
 }
 

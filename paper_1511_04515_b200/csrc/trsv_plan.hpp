@@ -46,6 +46,7 @@ struct AugPlan {
     // warp tasks over the positions: {first position, cnt | log2(lanes) << 8 | LONG << 30}
     std::vector<int> tasks;  // 2 ints per task
     std::vector<int> level_first_task;  // levels + 1 entries
+    std::vector<long long> level_first_pos;  // levels + 1 entries (positions are in level order)
 };
 
 struct AugParams {
@@ -54,6 +55,8 @@ struct AugParams {
     int chunk_over = 384;   // rows with more entries get partial sums
     int recent = 128;       // newest entries kept inline
     int chunk = 256;        // entries per partial sum
+    int cap = 0;            // > 0: no row keeps more than cap entries (partials of partials if
+                            // needed); the stream plan needs cap <= 128 (one 4-entry batch per lane)
 };
 
 // upper: U (rows depend on larger indices, divided by diag); else strictly
@@ -66,5 +69,70 @@ void build_aug_plan(bool upper, int n, const int* ptr, const int* col, const dou
 // CPU evaluation of a plan in position order (test helper: the same
 // arithmetic the kernel performs, sequentially).  out has n_aug entries.
 void eval_aug_plan(const AugPlan& P, bool upper, const double* in, double* out);
+
+// ---------------------------------------------------------------------------
+// Per-warp record streams for k_trsv4 (kernels.cu).
+//
+// The augmented rows (every one <= 128 entries: AugParams.cap) are cut, level
+// by level, into warp tasks of at most 32 lanes x 4 entries; task t belongs to
+// warp t mod W (W = co-resident warps of the launch), and each warp's tasks
+// are serialised, in order, into ONE contiguous byte stream that the warp
+// pulls through a shared-memory ring with bulk async copies (TMA), several
+// KB ahead.  Nothing on a task's path is a dependent global load any more:
+// its descriptor, row metadata, column ids and values arrive together.
+//
+// Record (8-byte aligned):
+//   header 16 B  {cnt | lg << 8 | nq << 16, record bytes, level, task id}
+//                cnt rows (1..32), 2^lg lanes per row, nq (0..4) entry batches;
+//                word 0 == 0 ends the stream
+//   cnt metas    L: {out id, rhs index or -1}                      (8 B)
+//                U: {out id, rhs index or -1, epilogue index or -1, 0, diag}  (24 B)
+//   nq x 32 column ids (int32, -1 = empty slot), nq x 32 values (fp64)
+// Lane l = seg * 2^lg + sl owns entries sl, sl + 2^lg, ... of row seg, stored
+// at slot q * 32 + l (conflict-free shared-memory reads, coalesced in HBM).
+// Streams are padded to whole pages; warp_off[w] is the byte offset of warp
+// w's stream in `data`.
+struct StreamParams {
+    int n_warps = 0;              // co-resident warps of the launch (upper bound)
+    int page = 1024;
+    int ring = 8192;
+    int min_tasks_per_warp = 4;   // small systems use fewer warps (a multiple of 8)
+};
+
+struct StreamPlan {
+    int n = 0;
+    int n_warps = 0;
+    int page = 0;
+    int levels = 0;
+    long long n_aug = 0;
+    long long n_tasks = 0, n_rows = 0, n_entries = 0, n_slots = 0;
+    int max_record = 0;
+    std::vector<long long> warp_off;  // n_warps + 1
+    std::vector<unsigned char> data;
+};
+
+constexpr int kStreamMetaL = 8, kStreamMetaU = 24;
+
+// augmented-system parameters of the stream plan: every row <= 128 entries
+inline AugParams stream_aug_params() {
+    AugParams p;
+    p.chunk_over = 128;
+    p.recent = 0;
+    p.chunk = 128;
+    p.cap = 128;
+    return p;
+}
+
+// out_index (may be null): epilogue index of x row r (U: col_perm), written
+// into the metas of rows with out < n.
+void build_stream_plan(const AugPlan& P, bool upper, const int* out_index, const StreamParams& prm,
+                       StreamPlan& S);
+
+// CPU evaluation of the streams in global task order with the kernel's
+// arithmetic (per-lane fused multiply-adds, xor-butterfly over the row's
+// lanes, b - acc, U: / diag).  out: n_aug entries.  final_out (may be null):
+// final_out[q] = (add ? add[q] : 0) + coef * x for rows carrying an epilogue index.
+void eval_stream_plan(const StreamPlan& S, bool upper, const double* in, double* out, double* final_out,
+                      double coef, const double* add);
 
 }  // namespace exg

@@ -107,3 +107,73 @@ def test_aug_plan_rejects_bad_parameters():
                                   F.as_ptr(d, C.c_double), F.as_ptr(z, C.c_int), (C.c_int * 5)(8, 0, 1, 1, 1),
                                   None, None, None)
     assert rc == F.EXG_E_CONTRACT
+
+
+# ---- per-warp record streams (k_trsv4's input format, trsv_plan.hpp) ---------------------------
+def stream_solve(upper, n, part, in_index, b, n_warps, out_index=None, coef=1.0, add=None, params=None):
+    ptr, col, val, diag = part
+    x = np.zeros(n)
+    fin = np.full(n, np.nan) if out_index is not None else None
+    st = (C.c_longlong * 10)()
+    prm = (C.c_int * 2)(*params) if params else None
+    rc = F.lib.exg_stream_plan_solve(
+        int(upper), n, F.as_ptr(ptr, C.c_int), F.as_ptr(col, C.c_int), F.as_ptr(val, C.c_double),
+        F.as_ptr(diag, C.c_double), F.as_ptr(in_index, C.c_int),
+        F.as_ptr(out_index, C.c_int) if out_index is not None else None, prm, n_warps,
+        F.as_ptr(b, C.c_double), F.as_ptr(x, C.c_double),
+        F.as_ptr(fin, C.c_double) if fin is not None else None, coef,
+        F.as_ptr(add, C.c_double) if add is not None else None, st)
+    assert rc == F.EXG_OK, F.lib.exg_host_error_message().decode()
+    return x, fin, dict(zip(["orig_levels", "levels", "n_aug", "tasks", "rows", "entries", "slots", "bytes",
+                             "max_record", "partials"], list(st)))
+
+
+@pytest.mark.parametrize("cfg,kw", CASES, ids=[f"c{c}" for c, _ in CASES])
+@pytest.mark.parametrize("n_warps", [8, 1000, 3552])
+def test_stream_plan_solves_the_factor(orc, cfg, kw, n_warps):
+    """The streams, evaluated warp-round-robin as the kernel's static schedule runs them, solve
+    the factor to FAST mode's 1e-13, including the fused epilogue of the U sweep."""
+    s = ex.System.generate(cfg, **kw)
+    f = ex.lu_factor(s.G)
+    n = f.n
+    lpart, upart = strict_parts(f)
+    rng = np.random.default_rng(cfg)
+    b = rng.uniform(-1, 1, n)
+    add = rng.uniform(-1, 1, n)
+    y, _, sl = stream_solve(False, n, lpart, np.asarray(f.row_perm, np.int32), b, n_warps)
+    z, fin, su = stream_solve(True, n, upart, np.arange(n, dtype=np.int32), y, n_warps,
+                              out_index=np.asarray(f.col_perm, np.int32), coef=-2.0, add=add)
+    x = np.empty(n)
+    x[np.asarray(f.col_perm)] = z
+    want = orc.solve(f, b)
+    scale = np.max(np.abs(want))
+    assert np.max(np.abs(x - want)) / scale <= 1e-13
+    assert np.max(np.abs(fin - (add - 2.0 * want))) / max(scale, 1.0) <= 1e-12
+    for st in (sl, su):
+        assert st["levels"] <= st["orig_levels"] + 2
+        assert st["rows"] == st["n_aug"] and st["entries"] <= st["slots"]
+        assert 2 * st["max_record"] + 1024 <= 8192  # two records fit the kernel's ring
+        assert st["bytes"] % 1024 == 0
+
+
+def test_stream_plan_long_rows_become_partials():
+    """A dense triangle of 700 rows: rows of up to 699 entries are cut into 128-entry partial sums
+    (and the block inverse keeps the level count at a handful)."""
+    n = 700
+    rng = np.random.default_rng(5)
+    ptr, col, val = [0], [], []
+    for r in range(n):
+        col += list(range(r))
+        val += list(rng.uniform(-0.01, 0.01, r))
+        ptr.append(len(col))
+    part = (np.array(ptr, np.int32), np.array(col, np.int32), np.array(val), np.ones(n))
+    b = rng.uniform(-1, 1, n)
+    Ld = np.eye(n)
+    for r in range(n):
+        Ld[r, :r] = val[ptr[r]:ptr[r + 1]]
+    want = np.linalg.solve(Ld, b)
+    for params in (None, (100000, 4096)):  # with the block inverse / plain rows with partial sums only
+        x, _, st = stream_solve(False, n, part, np.arange(n, dtype=np.int32), b, 64, params=params)
+        assert st["partials"] > 0
+        assert np.allclose(x, want, rtol=0, atol=1e-12)
+    assert st["levels"] >= n  # no block rewrite: the dense triangle stays sequential

@@ -197,6 +197,9 @@ exg_status exg_profile_enable(exg_ctx* ctx, int on);
  * (start, end) of the warp-task sweeps for L then U (4n), then (start,
  * far-done, end) of the cluster sweeps for L then U (6n); zero = not run there */
 exg_status exg_debug_trace_solve(exg_ctx* ctx, const double* b, unsigned long long* times);
+/* debug / test: dense_expm (dense_matrix.cpp:185-225) of a host m x m row-major
+ * matrix through the dense-block kernel, bit-identical to the reference. */
+exg_status exg_debug_dense_expm(exg_ctx* ctx, int m, const double* A, double* E);
 /* debug: one FAST solve pair over the stream plan (k_trsv4) with 5 values per
  * warp task {level, begin, dependencies ready, published (ns, %globaltimer),
  * warp}, L's tasks then U's.  counts (6): tasks of L, U; warps of L, U; stream

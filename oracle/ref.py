@@ -272,6 +272,15 @@ class Ref:
                                                   C.c_long(max_steps), xp, C.byref(rh)))
         return self._tran(rh)
 
+    def transient_policy(self, sh, ctl, t_stop, rec_idx, method=1, threshold=0.1, max_steps=0):
+        """Restated loop with the refactor policy of exg_step_control.refactor_threshold:
+        the Linearization and lu_factor(G_k) are renewed only when a device conductance
+        moved by more than `threshold` (0: every step, bit-identical to transient())."""
+        import copy
+        c2 = copy.copy(ctl)
+        c2.refactor_threshold = threshold
+        return self.transient_cached(sh, None, c2, t_stop, rec_idx, method=method, max_steps=max_steps)
+
 
 class Orc:
     """The plain-C restatement (oracle/exsim_oracle.c)."""

@@ -561,6 +561,21 @@ int ref_transient(void* s, int method, const exg_step_control* c, double t_stop,
     GUARD_END
 }
 
+// largest relative move of a device conductance between two linearizations
+// (the product's jacobian_change, csrc/transient.cu, same arithmetic)
+static double jacobian_change(const Linearization& a, const Linearization& b) {
+    double worst = 0.0;
+    auto rel = [&](double x, double y) {
+        const double d = std::fabs(x - y), m = std::max(std::fabs(x), std::fabs(y));
+        if (d > 0.0) worst = std::max(worst, d / m);
+    };
+    for (size_t i = 0; i < a.op.size(); ++i) {
+        rel(a.op[i].gm, b.op[i].gm);
+        rel(a.op[i].gds, b.op[i].gds);
+    }
+    return worst;
+}
+
 // Restated ER/ERC loop (integrate.cpp:368-480).  fact != null: linear
 // circuit, reuse that factorization for every step (G_k == G_lin,
 // devices.cpp:190-192); fact == null: lu_factor(G_k) every step, as the
@@ -599,6 +614,9 @@ int ref_transient_cached(void* s, void* fact, int method, const exg_step_control
 
     double t = 0.0;
     long k = 0;
+    Linearization lin;
+    std::unique_ptr<Factorization> own;
+    bool have_lin = false;
     const auto wall0 = std::chrono::steady_clock::now();
     std::vector<double> wall;
     while (t < t_stop - t_tiny) {
@@ -609,9 +627,22 @@ int ref_transient_cached(void* s, void* fact, int method, const exg_step_control
         h_try = std::max(h_try, std::min(hmin_eff, seg_end - t));
 
         const std::uint64_t lu0 = lu_factor_count();
-        Linearization lin = evaluate(sys, x);
-        std::unique_ptr<Factorization> own;
-        if (!cached) own = std::make_unique<Factorization>(lu_factor(lin.G_k));
+        // refactor policy (exg_step_control.refactor_threshold, BASELINE.json
+        // config 4): the whole Linearization and its factorization stay frozen
+        // until a device conductance moved by more than the threshold; 0 =
+        // evaluate + lu_factor every step, as the reference
+        {
+            Linearization lin_new = evaluate(sys, x);
+            bool refresh = true;
+            if (have_lin && !cached && c->refactor_threshold > 0.0 &&
+                jacobian_change(lin, lin_new) <= c->refactor_threshold)
+                refresh = false;
+            if (refresh) {
+                lin = std::move(lin_new);
+                if (!cached) own = std::make_unique<Factorization>(lu_factor(lin.G_k));
+                have_lin = true;
+            }
+        }
         const Factorization& G_fact = cached ? *cached : *own;
 
         StepRecord rec_;

@@ -74,7 +74,8 @@ class exg_step_control(C.Structure):
                 ("grow_threshold", C.c_int32), ("grow_only_on_clean", C.c_int32),
                 ("eps", C.c_double), ("m_max", C.c_int32), ("max_rejects", C.c_int32),
                 ("h_init", C.c_double), ("hmin", C.c_double), ("hmax", C.c_double),
-                ("fixed_step", C.c_int32), ("method", C.c_int32), ("gamma", C.c_double)]
+                ("fixed_step", C.c_int32), ("method", C.c_int32), ("gamma", C.c_double),
+                ("refactor_threshold", C.c_double)]
 
 
 class exg_mevp_cfg(C.Structure):
@@ -170,6 +171,7 @@ _DEV_PROTOS = {
     "exg_counters_reset": (I, [P]),
     "exg_profile_enable": (I, [P, I]),
     "exg_debug_trace_solve": (I, [P, PD, C.POINTER(C.c_uint64)]),
+    "exg_debug_dense_expm": (I, [P, I, PD, PD]),
     "exg_debug_trace_stream": (I, [P, PD, C.POINTER(C.c_uint64), C.POINTER(C.c_longlong)]),
     "exg_profile_get": (I, [P, C.POINTER(exg_kernel_times)]),
     "exg_synchronize": (I, [P]),

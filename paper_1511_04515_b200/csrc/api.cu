@@ -178,8 +178,9 @@ void solve_dev(exg_ctx* c, const double* b, double* final_out, double coef, cons
     const size_t chain_doubles = fast ? (size_t)(c->plan[0].chain_rows + c->plan[1].chain_rows +
                                                  c->plan[0].chain_slots + c->plan[1].chain_slots) : 0;
     // output of each sweep: n unknowns, or the augmented system's n_aug
-    const size_t ny = fast && c->plan[0].n_aug ? (size_t)c->plan[0].n_aug : (size_t)n;
-    const size_t nx = fast && c->plan[1].n_aug ? (size_t)c->plan[1].n_aug : (size_t)n;
+    // (+ 1: the stream plan's dummy entry)
+    const size_t ny = fast && c->plan[0].n_aug ? (size_t)c->plan[0].n_aug + 1 : (size_t)n;
+    const size_t nx = fast && c->plan[1].n_aug ? (size_t)c->plan[1].n_aug + 1 : (size_t)n;
     exg::dev::fill_ones(c->L(), c->trsv_buf, kTrsvHdr + sizeof(double) * (ny + nx + chain_doubles));
     unsigned int* tickets = reinterpret_cast<unsigned int*>(c->trsv_buf);
     double* y = reinterpret_cast<double*>(c->trsv_buf + kTrsvHdr);
@@ -221,8 +222,9 @@ void solve_dev(exg_ctx* c, const double* b, double* final_out, double coef, cons
                 // per-warp record streams of the blocked augmented system
                 exg::dev::StreamArgs sa{};
                 sa.data = P.sdata;
-                sa.warp_off = P.swarp_off;
+                sa.desc = P.sdesc;
                 sa.n_warps = P.s_warps;
+                sa.n_aug = P.n_aug;
                 sa.in = a.in;
                 sa.out = a.out;
                 sa.final_out = a.final_out;
@@ -230,6 +232,8 @@ void solve_dev(exg_ctx* c, const double* b, double* final_out, double coef, cons
                 sa.coef = a.coef;
                 sa.ctrl = ctrl;
                 sa.trace = a.trace;
+                static const int nodeps = getenv("EXG_STREAM_NODEPS") ? atoi(getenv("EXG_STREAM_NODEPS")) : 0;
+                sa.nodeps = nodeps;
                 ck(exg::dev::trsv_stream(c->L(), upper, sa), "stream solve launch");
                 c->prof_end(upper ? EXG_K_TRSV_U : EXG_K_TRSV_L, e0);
                 continue;
@@ -428,7 +432,7 @@ void mevp_dev(exg_ctx* c, const double* v, double h, const exg_mevp_cfg& cfg, in
     if (use_mgs2) ensure_mgs_slots(c, cfg.m_max);
     exg::dev::Mgs2Args ma2{n, c->ldv, c->V, c->w, c->hbar, c->hld, c->mgs_slots ? c->mgs_slots + 8 : nullptr,
                            reinterpret_cast<unsigned int*>(c->mgs_slots), c->ctrl, c->mgs_inst_cap, 0, 0, 0};
-    exg::dev::DenseArgs da{c->ctrl, c->hbar, c->hld, c->hinv, c->coef, c->dscratch, 0, 0, h};
+    exg::dev::DenseArgs da{c->ctrl, c->hbar, c->hld, c->hinv, c->coef, c->dscratch, 0, 0, h, nullptr};
     const bool gspmv = c->opt.weight_mode == EXG_WEIGHT_GSPMV;
     if (gspmv) mat(c, EXG_MAT_G);
     static const bool side_ok = !(getenv("EXG_NO_FORK") && atoi(getenv("EXG_NO_FORK")));
@@ -1432,10 +1436,10 @@ exg_status exg_set_factors(exg_ctx* c, int n, const int* Lp, const int* Li, cons
                 c->cnt_aug[tri][3] = A.n_partials;
             }
             P.sdata = dalloc<unsigned char>(std::max<size_t>(S.data.size(), 16));
-            P.swarp_off = dalloc<long long>(S.warp_off.size());
+            P.sdesc = dalloc<int>(S.desc.size());
             ck(cudaMemcpyAsync(P.sdata, S.data.data(), S.data.size(), cudaMemcpyHostToDevice, c->stream), "stream plan");
-            ck(cudaMemcpyAsync(P.swarp_off, S.warp_off.data(), S.warp_off.size() * sizeof(long long),
-                               cudaMemcpyHostToDevice, c->stream), "stream plan");
+            ck(cudaMemcpyAsync(P.sdesc, S.desc.data(), S.desc.size() * sizeof(int), cudaMemcpyHostToDevice,
+                               c->stream), "stream plan");
             ck(cudaStreamSynchronize(c->stream), "stream plan sync");  // S is released below
             P.s_warps = S.n_warps;
             P.s_bytes = (long long)S.data.size();
@@ -1515,8 +1519,8 @@ exg_status exg_set_factors(exg_ctx* c, int n, const int* Lp, const int* Li, cons
         ck(cudaMemcpyAsync(c->tasks[q], tl[q]->data(), tl[q]->size() * sizeof(int2), cudaMemcpyHostToDevice, c->stream), "tasks");
         c->n_tasks[q] = (int)tl[q]->size();
     }
-    c->trsv_buf = dalloc<char>(kTrsvHdr + sizeof(double) * ((size_t)std::max<long long>(n, c->plan[0].n_aug) +
-                                                       (size_t)std::max<long long>(n, c->plan[1].n_aug) +
+    c->trsv_buf = dalloc<char>(kTrsvHdr + sizeof(double) * ((size_t)std::max<long long>(n, c->plan[0].n_aug + 1) +
+                                                       (size_t)std::max<long long>(n, c->plan[1].n_aug + 1) +
                                                        c->plan[0].chain_rows +
                                                        c->plan[1].chain_rows + c->plan[0].chain_slots +
                                                        c->plan[1].chain_slots));
@@ -1971,6 +1975,36 @@ exg_status exg_debug_trace_stream(exg_ctx* c, const double* b, unsigned long lon
         ck(cudaStreamSynchronize(c->stream), "sync");
         cudaFree(tr);
     }
+    API_END(c)
+}
+
+// debug / test: dense_expm (dense_matrix.cpp:185-225) of a host m x m
+// row-major matrix through k_dense (shared-memory scratch for small m, the
+// global scratch above), bit-identical to the reference
+exg_status exg_debug_dense_expm(exg_ctx* c, int m, const double* A, double* E) {
+    API_BEGIN
+    if (m < 1 || m > 512 || !A || !E) throw ApiError{EXG_E_CONTRACT, "exg_debug_dense_expm: bad arguments"};
+    const size_t mm = (size_t)m * m;
+    double* dA = dalloc<double>(mm);
+    double* dE = dalloc<double>(mm);
+    double* dS = dalloc<double>(20 * mm);
+    Ctrl* dc = reinterpret_cast<Ctrl*>(dalloc<char>(sizeof(Ctrl)));
+    Ctrl hc;
+    std::memset(&hc, 0, sizeof hc);
+    hc.m = m;
+    ck(cudaMemcpyAsync(dc, &hc, sizeof hc, cudaMemcpyHostToDevice, c->stream), "h2d");
+    ck(cudaMemcpyAsync(dA, A, mm * sizeof(double), cudaMemcpyHostToDevice, c->stream), "h2d");
+    exg::dev::DenseArgs da{dc, nullptr, 0, dA, nullptr, dS, 0, 3, 1.0, dE};
+    exg::dev::dense(c->L(), da, m);
+    ck(cudaMemcpyAsync(E, dE, mm * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
+    ck(cudaMemcpyAsync(&hc, dc, sizeof hc, cudaMemcpyDeviceToHost, c->stream), "d2h");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    cudaFree(dA);
+    cudaFree(dE);
+    cudaFree(dS);
+    cudaFree(dc);
+    if (hc.status == 2) throw ApiError{EXG_E_NONFINITE, "dense_expm: non-finite entry"};
+    if (hc.status) throw ApiError{EXG_E_SINGULAR, "dense_solve: singular matrix"};
     API_END(c)
 }
 

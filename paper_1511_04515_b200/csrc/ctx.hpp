@@ -85,14 +85,14 @@ struct TriPlan {
     int aug_levels = 0;
     // per-warp record streams of the augmented system (k_trsv4); used when s_warps > 0
     unsigned char* sdata = nullptr;
-    long long* swarp_off = nullptr;
+    int* sdesc = nullptr;
     int s_warps = 0;
     long long s_bytes = 0;
     void free_aug() {
         if (sdata) cudaFree(sdata);
-        if (swarp_off) cudaFree(swarp_off);
+        if (sdesc) cudaFree(sdesc);
         sdata = nullptr;
-        swarp_off = nullptr;
+        sdesc = nullptr;
         s_warps = 0;
         s_bytes = 0;
         void* ps[] = {ameta, atasks, acol, aval, adiag};

@@ -35,15 +35,17 @@ struct TrsvArgs {
 // k_trsv4 (trsv_stream.cu): per-warp record streams of one triangle
 struct StreamArgs {
     const unsigned char* data;   // all streams (trsv_plan.hpp record format)
-    const long long* warp_off;   // n_warps + 1 byte offsets (page multiples)
+    const int* desc;             // 8 ints per warp: stream offset, tasks, first record sizes
     int n_warps;
+    long long n_aug;             // unknowns; out[n_aug] is the dummy entry (0.0)
     const double* in;            // right-hand side (L: b, gathered through the baked row_perm; U: L's output)
-    double* out;                 // n_aug results, sentinel-initialised
+    double* out;                 // n_aug + 1 results, sentinel-initialised
     double* final_out;           // U: fused epilogue final_out[q] = (add ? add[q] : 0) + coef * x
     const double* add;
     double coef;
     const Ctrl* ctrl;
     unsigned long long* trace;   // debug: 5 values per task, or null
+    int nodeps;                  // debug (EXG_STREAM_NODEPS): ignore readiness, wrong results: throughput bound only
 };
 
 struct SubArgs {
@@ -137,6 +139,7 @@ struct DenseArgs {
     int smem_cap;     // dynamic shared memory of the launch (bytes)
     int mode;
     double h_eval;
+    double* full_out;  // mode 3 (debug): the whole m x m exponential
 };
 
 // ---- launch wrappers (kernels.cu) ------------------------------------------

@@ -235,6 +235,7 @@ exg_status exg_step_control_from(const exg_system* s, exg_step_control* c) {
     c->fixed_step = 0;
     c->method = EXG_METHOD_ER;
     c->gamma = 0.1;
+    c->refactor_threshold = 0.0;
     return EXG_OK;
 }
 
@@ -290,7 +291,7 @@ exg_status exg_stream_plan_solve(int upper, int n, const int* ptr, const int* co
     exg::StreamPlan S;
     exg::build_stream_plan(P, upper != 0, out_index, sp, S);
     if (b && x) {
-        std::vector<double> out(S.n_aug, 0.0);
+        std::vector<double> out(S.n_aug + 1, 0.0);
         exg::eval_stream_plan(S, upper != 0, b, out.data(), final_out, coef, add);
         std::memcpy(x, out.data(), sizeof(double) * n);
     }

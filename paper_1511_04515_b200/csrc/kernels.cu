@@ -1892,6 +1892,7 @@ __device__ int d_expm(int m, const double* M, double* out, double* w, double* co
 //   mode 0: Arnoldi iteration check at ctrl->h
 //   mode 1: final coefficients coef[i] = beta * e^{h H^-1}(i,0) at h_eval
 //   mode 2: residual scalar s at h_eval for the cached basis (mevp_residual)
+//   mode 3: debug, the whole exponential e^{h_eval * hinv} (exg_debug_dense_expm)
 __global__ void __launch_bounds__(256)
     k_dense(DenseArgs a) {
     extern __shared__ double dyn_smem[];
@@ -1963,7 +1964,9 @@ __global__ void __launch_bounds__(256)
         if (threadIdx.x == 0) c->status = st == 2 ? 2 : 3;
         return;
     }
-    if (a.mode == 1) {
+    if (a.mode == 3) {
+        for (int idx = threadIdx.x; idx < mm; idx += blockDim.x) a.full_out[idx] = e[idx];
+    } else if (a.mode == 1) {
         for (int i = threadIdx.x; i < m; i += blockDim.x) a.coef[i] = c->beta * e[i * m];
     } else if (threadIdx.x == 0) {
         double s = 0.0;

@@ -54,7 +54,9 @@ __device__ __forceinline__ unsigned long long ld_relaxed(const double* p) {
 }
 __device__ __forceinline__ void st_relaxed(double* p, double x) {
     unsigned long long v = __double_as_longlong(x);
-    if (v == kSentinel) v = kCanonNaN;  // never publish the sentinel
+    // never publish the sentinel, nor any NaN sharing its high word (readers
+    // may test the high word alone)
+    if ((v >> 32) == 0xFFFFFFFFull) v = kCanonNaN;
     asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }

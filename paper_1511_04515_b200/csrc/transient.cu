@@ -120,6 +120,23 @@ void upload_linearization(exg_ctx* ctx, const exg::Linearization& lin, const exg
     chk(ctx, exg_set_oppoints(ctx, op.data()));
 }
 
+// largest relative move of a device conductance (gm, gds) between two
+// linearizations of the same circuit: the "Jacobian change" of the refactor
+// policy (exg_step_control.refactor_threshold; restated identically in
+// oracle/ref_shim.cpp)
+double jacobian_change(const exg::Linearization& a, const exg::Linearization& b) {
+    double worst = 0.0;
+    auto rel = [&](double x, double y) {
+        const double d = std::fabs(x - y), m = std::max(std::fabs(x), std::fabs(y));
+        if (d > 0.0) worst = std::max(worst, d / m);
+    };
+    for (size_t i = 0; i < a.op.size(); ++i) {
+        rel(a.op[i].gm, b.op[i].gm);
+        rel(a.op[i].gds, b.op[i].gds);
+    }
+    return worst;
+}
+
 // integrate.cpp:368-480 with nonlinear devices
 exg_status transient_nonlinear(exg_ctx* ctx, const exg::System& sys, const exg_step_control* ctl,
                                double t_stop, const int* rec_idx, int n_rec, exg_tran_result** out) {
@@ -159,6 +176,9 @@ exg_status transient_nonlinear(exg_ctx* ctx, const exg::System& sys, const exg_s
     chk(ctx, exg_set_csr(ctx, EXG_MAT_B, sys.B.n_rows, sys.B.n_cols, sys.B.nnz(), sys.B.rowptr.data(),
                          sys.B.col.data(), sys.B.val.data()));
     bool devices_set = false;
+    bool have_lin = false;
+    exg::Linearization lin;
+    exg::Factor f;
     double lu_s = 0.0;
     double t = 0.0;
     while (t < t_stop - t_tiny) {
@@ -167,17 +187,27 @@ exg_status transient_nonlinear(exg_ctx* ctx, const exg::System& sys, const exg_s
         if (seg_end - t - h_try < t_tiny) h_try = seg_end - t;
         h_try = std::max(h_try, std::min(hmin_eff, seg_end - t));
 
+        // linearization at x_k (integrate.cpp:419-421).  With a refactor
+        // threshold the frozen Linearization and its factors are kept while no
+        // device conductance moved by more than that relative amount
         auto ta = clock::now();
-        exg::Linearization lin;
-        exg::Factor f;
+        bool refresh = true;
         try {
-            exg::evaluate(sys, x, lin);
-            exg::lu_factor(lin.G, 0.1, f);
+            exg::Linearization lin_new;
+            exg::evaluate(sys, x, lin_new);
+            if (have_lin && ctl->refactor_threshold > 0.0 &&
+                jacobian_change(lin, lin_new) <= ctl->refactor_threshold)
+                refresh = false;
+            if (refresh) {
+                lin = std::move(lin_new);
+                exg::lu_factor(lin.G, 0.1, f);
+                have_lin = true;
+            }
         } catch (const exg::Error& e) {
             throw Fail{e.status, e.what};
         }
         lu_s += std::chrono::duration<double>(clock::now() - ta).count();
-        upload_linearization(ctx, lin, f, devices_set);
+        if (refresh) upload_linearization(ctx, lin, f, devices_set);
         if (!devices_set) {  // device tables (after the first set_factors fixes n)
             std::vector<int> nodes(4 * sys.mos.size());
             std::vector<double> par(6 * sys.mos.size());
@@ -225,7 +255,7 @@ exg_status transient_nonlinear(exg_ctx* ctx, const exg::System& sys, const exg_s
         }
         res->t.push_back(t + h_try);
         res->h.push_back(h_try);
-        res->lu.push_back(1);
+        res->lu.push_back(refresh ? 1 : 0);
         res->rej.push_back(rejects);
         res->err.push_back(err_norm);
         res->dims_off.push_back(static_cast<int>(res->dims.size()));

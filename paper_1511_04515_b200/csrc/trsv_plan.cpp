@@ -4,6 +4,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <cstdio>
+#include <cstdlib>
 #include <atomic>
 #include <numeric>
 #include <stdexcept>
@@ -260,6 +262,28 @@ void build_aug_plan(bool upper, int n, const int* ptr, const int* col, const dou
         const int s = B.b - B.a;
         ++P.n_blocks;
         P.block_rows += s;
+        if (getenv("EXG_FOLD_STATS")) {  // development: pattern growth of inv(T_BB) * T_B,ext
+            static std::vector<int> mark;
+            if ((int)mark.size() < n) mark.assign(n, -1);
+            long long uni = 0, run = 0, ext = 0;
+            for (int z = 0; z < s; ++z) {
+                const int i = upper ? s - 1 - z : z;
+                const int rr = B.a + i;
+                for (int k = ptr[rr]; k < ptr[rr + 1]; ++k) {
+                    const int c = col[k];
+                    if (c >= B.a && c < B.b) continue;
+                    ++ext;
+                    if (mark[c] != B.a) {
+                        mark[c] = B.a;
+                        ++run;
+                    }
+                }
+                uni += run;
+            }
+            P.fold_ext += ext;
+            P.fold_union += uni;
+            if (s >= 256) fprintf(stderr, "block rows %d ext %lld union %lld inv %lld\n", s, ext, uni, (long long)s * s / 2);
+        }
         P.max_block = std::max(P.max_block, s);
         yid.assign(s, -1);
         // y rows: the external part of every block row
@@ -398,13 +422,13 @@ inline T get(const unsigned char* p) {
 void build_stream_plan(const AugPlan& P, bool upper, const int* out_index, const StreamParams& prm,
                        StreamPlan& S) {
     S = StreamPlan{};
-    if (prm.n_warps < 1 || prm.page < 16 || prm.page % 16 || prm.ring % prm.page)
-        throw std::runtime_error("stream plan: bad parameters");
+    if (prm.n_warps < 1) throw std::runtime_error("stream plan: bad parameters");
     const int MS = upper ? kStreamMetaU : kStreamMetaL;
     S.n = P.n;
-    S.page = prm.page;
     S.levels = P.levels;
     S.n_aug = P.n_aug;
+    if (P.n_aug >= INT32_MAX) throw std::runtime_error("stream plan: too many unknowns");
+    const int dummy = (int)P.n_aug;
     const size_t np = P.meta.size() / 4;
     S.n_rows = (long long)np;
     // ---- tasks: within a level rows are independent, so they are taken
@@ -424,8 +448,10 @@ void build_stream_plan(const AugPlan& P, bool upper, const int* out_index, const
         while (i < b) {
             const int len = len_of(ord[i]);
             if (len > 128) throw std::runtime_error("stream plan: a row exceeds 128 entries (AugParams.cap)");
-            const int lg = lanes_log2_for(len), per = 32 >> lg;
+            const int lg = lanes_log2_for(len);
             Task t{i, 0, lg, (len + (1 << lg) - 1) >> lg, l};
+            // rows per task: the lane count, and the record must fit its slot
+            const int per = std::max(1, std::min(32 >> lg, (kStreamSlot - 16 - t.nq * 384) / MS));
             while (i < b && t.cnt < per && lanes_log2_for(len_of(ord[i])) == lg) {
                 ++t.cnt;
                 ++i;
@@ -437,37 +463,61 @@ void build_stream_plan(const AugPlan& P, bool upper, const int* out_index, const
     int W = prm.n_warps;
     if (prm.min_tasks_per_warp > 0) {
         const long long want = ((long long)tasks.size() / prm.min_tasks_per_warp + 7) / 8 * 8;
-        W = (int)std::max<long long>(8, std::min<long long>(W, want));
+        W = (int)std::max<long long>(8, std::min<long long>(W, want));  // a multiple of 8 (and of any CTA's warps)
         W = std::min(W, prm.n_warps);
     }
     S.n_warps = W;
     // ---- stream sizes
-    auto rec_bytes = [&](const Task& t) { return 16 + t.cnt * MS + t.nq * 32 * 12; };
+    auto rec_bytes = [&](const Task& t) { return (16 + t.nq * 384 + t.cnt * MS + 15) / 16 * 16; };
     std::vector<long long> bytes(W, 0);
     for (size_t t = 0; t < tasks.size(); ++t) {
         const int rb = rec_bytes(tasks[t]);
         bytes[t % W] += rb;
         S.max_record = std::max(S.max_record, rb);
     }
-    if (2 * S.max_record + prm.page > prm.ring) throw std::runtime_error("stream plan: ring too small for two records");
-    S.warp_off.assign(W + 1, 0);
+    if (S.max_record > kStreamSlot) throw std::runtime_error("stream plan: record larger than its slot");
+    if (P.levels > 0xFFFF) throw std::runtime_error("stream plan: too many levels");
+    std::vector<long long> off(W + 1, 0);
+    for (int w = 0; w < W; ++w) off[w + 1] = off[w] + bytes[w];
+    S.data.assign((size_t)off[W] + 16, 0);
+    S.desc.assign((size_t)8 * W, 0);
     for (int w = 0; w < W; ++w) {
-        const long long padded = (bytes[w] + 16 + prm.page - 1) / prm.page * prm.page;  // + end marker
-        S.warp_off[w + 1] = S.warp_off[w] + padded;
+        S.desc[8 * (size_t)w] = (int)(off[w] & 0xFFFFFFFFll);
+        S.desc[8 * (size_t)w + 1] = (int)(off[w] >> 32);
+        const long long nt = ((long long)tasks.size() - w + W - 1) / W;
+        S.desc[8 * (size_t)w + 2] = (int)std::max<long long>(0, nt);
+        for (int k = 0; k < kStreamRing - 1; ++k) {
+            const size_t t = (size_t)w + (size_t)k * W;
+            S.desc[8 * (size_t)w + 3 + k] = t < tasks.size() ? rec_bytes(tasks[t]) : 0;
+        }
     }
-    S.data.assign((size_t)S.warp_off[W], 0);
-    std::vector<long long> cur(S.warp_off.begin(), S.warp_off.end() - 1);
+    // the task that produces each unknown: a task's flag is its dependency
+    // with the latest producer
+    std::vector<int> prod((size_t)P.n_aug, -1);
+    for (size_t t = 0; t < tasks.size(); ++t)
+        for (int seg = 0; seg < tasks[t].cnt; ++seg) prod[P.meta[4 * (size_t)ord[tasks[t].first + seg]]] = (int)t;
+    std::vector<long long> cur(off.begin(), off.end() - 1);
     for (size_t t = 0; t < tasks.size(); ++t) {
         const Task& T = tasks[t];
         const int rb = rec_bytes(T);
         size_t at = (size_t)cur[t % W];
         cur[t % W] += rb;
-        put<int>(S.data, at, T.cnt | (T.lg << 8) | (T.nq << 16));
-        put<int>(S.data, at + 4, rb);
-        put<int>(S.data, at + 8, T.level);
+        int flag = dummy, flag_task = -1;
+        for (int seg = 0; seg < T.cnt; ++seg) {
+            const int p = ord[T.first + seg];
+            for (int k = P.meta[4 * (size_t)p + 2]; k < P.meta[4 * (size_t)p + 3]; ++k)
+                if (prod[P.col[k]] > flag_task) {
+                    flag_task = prod[P.col[k]];
+                    flag = P.col[k];
+                }
+        }
+        const size_t ahead = t + (size_t)(kStreamRing - 1) * W;
+        put<int>(S.data, at, T.cnt | (T.lg << 8) | (T.nq << 12) | (T.level << 16));
+        put<int>(S.data, at + 4, ahead < tasks.size() ? rec_bytes(tasks[ahead]) : 0);
+        put<int>(S.data, at + 8, flag);
         put<int>(S.data, at + 12, (int)t);
-        const size_t meta_at = at + 16, col_at = meta_at + (size_t)T.cnt * MS, val_at = col_at + (size_t)T.nq * 128;
-        for (int q = 0; q < T.nq * 32; ++q) put<int>(S.data, col_at + 4 * (size_t)q, -1);
+        const size_t col_at = at + 16, val_at = col_at + (size_t)T.nq * 128, meta_at = val_at + (size_t)T.nq * 256;
+        for (int q = 0; q < T.nq * 32; ++q) put<int>(S.data, col_at + 4 * (size_t)q, dummy);
         const int lpr = 1 << T.lg;
         for (int seg = 0; seg < T.cnt; ++seg) {
             const int p = ord[T.first + seg];
@@ -496,28 +546,29 @@ void build_stream_plan(const AugPlan& P, bool upper, const int* out_index, const
 void eval_stream_plan(const StreamPlan& S, bool upper, const double* in, double* out, double* final_out,
                       double coef, const double* add) {
     const int W = S.n_warps, MS = upper ? kStreamMetaU : kStreamMetaL;
-    std::vector<long long> cur(S.warp_off.begin(), S.warp_off.end() - 1);
-    long long done = 0;
-    for (long long t = 0; done < W; ++t) {
+    std::vector<long long> cur(W), left(W);
+    for (int w = 0; w < W; ++w) {
+        cur[w] = ((long long)(unsigned)S.desc[8 * (size_t)w]) | ((long long)S.desc[8 * (size_t)w + 1] << 32);
+        left[w] = S.desc[8 * (size_t)w + 2];
+    }
+    out[S.n_aug] = 0.0;  // the dummy
+    for (long long t = 0; t < S.n_tasks; ++t) {
         const int w = (int)(t % W);
-        if (w == 0) done = 0;
+        if (left[w]-- <= 0) throw std::runtime_error("stream plan: task count mismatch");
         const unsigned char* r = S.data.data() + cur[w];
         const int w0 = get<int>(r);
-        if (w0 == 0) {  // this warp has finished (all later rounds too)
-            ++done;
-            continue;
-        }
-        const int cnt = w0 & 0xFF, lg = (w0 >> 8) & 0xFF, nq = (w0 >> 16) & 0xFF, lpr = 1 << lg;
-        cur[w] += get<int>(r + 4);
-        const unsigned char* meta = r + 16;
-        const unsigned char* cols = meta + (size_t)cnt * MS;
+        const int cnt = w0 & 0xFF, lg = (w0 >> 8) & 0xF, nq = (w0 >> 12) & 0xF, lpr = 1 << lg;
+        if (get<int>(r + 12) != (int)t) throw std::runtime_error("stream plan: record order mismatch");
+        cur[w] += (16 + nq * 384 + cnt * MS + 15) / 16 * 16;
+        const unsigned char* cols = r + 16;
         const unsigned char* vals = cols + (size_t)nq * 128;
+        const unsigned char* meta = vals + (size_t)nq * 256;
         double acc[32];
         for (int lane = 0; lane < 32; ++lane) {
             double a = 0.0;
             for (int q = 0; q < nq; ++q) {
                 const int c = get<int>(cols + 4 * (size_t)(q * 32 + lane));
-                if (c >= 0) a = std::fma(get<double>(vals + 8 * (size_t)(q * 32 + lane)), out[c], a);
+                a = std::fma(get<double>(vals + 8 * (size_t)(q * 32 + lane)), out[c], a);
             }
             acc[lane] = a;
         }

@@ -38,6 +38,7 @@ struct AugPlan {
     long long block_rows = 0;
     int max_block = 0;
     long long n_partials = 0;
+    long long fold_ext = 0, fold_union = 0;  // development statistics (EXG_FOLD_STATS)
     // per level-order position: {out id, in index or -1, k0, k1}
     std::vector<int> meta;   // 4 ints per position
     std::vector<int> col;    // dependency ids (into the augmented unknowns)
@@ -71,43 +72,49 @@ void build_aug_plan(bool upper, int n, const int* ptr, const int* col, const dou
 void eval_aug_plan(const AugPlan& P, bool upper, const double* in, double* out);
 
 // ---------------------------------------------------------------------------
-// Per-warp record streams for k_trsv4 (kernels.cu).
+// Per-warp record streams for k_trsv4 (trsv_stream.cu).
 //
 // The augmented rows (every one <= 128 entries: AugParams.cap) are cut, level
 // by level, into warp tasks of at most 32 lanes x 4 entries; task t belongs to
 // warp t mod W (W = co-resident warps of the launch), and each warp's tasks
-// are serialised, in order, into ONE contiguous byte stream that the warp
-// pulls through a shared-memory ring with bulk async copies (TMA), several
-// KB ahead.  Nothing on a task's path is a dependent global load any more:
-// its descriptor, row metadata, column ids and values arrive together.
+// are serialised, in order, into ONE contiguous byte stream.  The warp pulls
+// its stream through a shared-memory ring of kStreamRing record slots, one
+// bulk async copy (TMA) per record, a few records ahead: nothing on a task's
+// path is a dependent global load any more, and every field sits at a fixed
+// offset of its slot.
 //
-// Record (8-byte aligned):
-//   header 16 B  {cnt | lg << 8 | nq << 16, record bytes, level, task id}
-//                cnt rows (1..32), 2^lg lanes per row, nq (0..4) entry batches;
-//                word 0 == 0 ends the stream
-//   cnt metas    L: {out id, rhs index or -1}                      (8 B)
+// Record (16-byte multiple, <= kStreamSlot bytes):
+//   header 16 B  {cnt | lg << 8 | nq << 12 | level << 16,
+//                 bytes of this warp's record kStreamRing - 1 places ahead (0: none),
+//                 flag, task id}
+//                cnt rows (1..32), 2^lg lanes per row, nq (0..4) value batches;
+//                flag = the dependency produced by the latest task (the one
+//                value a waiting task polls)
+//   nq x 32 column ids (int32); an empty slot holds the dummy id n_aug, whose
+//                value is always 0.0
+//   nq x 32 values (fp64)
+//   cnt metas    L: {out id, rhs index or -1}                                 (8 B)
 //                U: {out id, rhs index or -1, epilogue index or -1, 0, diag}  (24 B)
-//   nq x 32 column ids (int32, -1 = empty slot), nq x 32 values (fp64)
 // Lane l = seg * 2^lg + sl owns entries sl, sl + 2^lg, ... of row seg, stored
 // at slot q * 32 + l (conflict-free shared-memory reads, coalesced in HBM).
-// Streams are padded to whole pages; warp_off[w] is the byte offset of warp
-// w's stream in `data`.
+// desc holds 8 ints per warp: {stream offset (lo, hi), tasks, bytes of its
+// first kStreamRing - 1 records, 0, 0}.
+constexpr int kStreamRing = 4;     // record slots per warp
+constexpr int kStreamSlot = 2048;  // bytes per slot
+
 struct StreamParams {
     int n_warps = 0;              // co-resident warps of the launch (upper bound)
-    int page = 1024;
-    int ring = 8192;
     int min_tasks_per_warp = 4;   // small systems use fewer warps (a multiple of 8)
 };
 
 struct StreamPlan {
     int n = 0;
     int n_warps = 0;
-    int page = 0;
     int levels = 0;
-    long long n_aug = 0;
+    long long n_aug = 0;          // unknowns; out[n_aug] is the dummy (0.0)
     long long n_tasks = 0, n_rows = 0, n_entries = 0, n_slots = 0;
     int max_record = 0;
-    std::vector<long long> warp_off;  // n_warps + 1
+    std::vector<int> desc;        // 8 ints per warp
     std::vector<unsigned char> data;
 };
 
@@ -130,7 +137,7 @@ void build_stream_plan(const AugPlan& P, bool upper, const int* out_index, const
 
 // CPU evaluation of the streams in global task order with the kernel's
 // arithmetic (per-lane fused multiply-adds, xor-butterfly over the row's
-// lanes, b - acc, U: / diag).  out: n_aug entries.  final_out (may be null):
+// lanes, b - acc, U: / diag).  out: n_aug + 1 entries (the dummy last).  final_out (may be null):
 // final_out[q] = (add ? add[q] : 0) + coef * x for rows carrying an epilogue index.
 void eval_stream_plan(const StreamPlan& S, bool upper, const double* in, double* out, double* final_out,
                       double coef, const double* add);

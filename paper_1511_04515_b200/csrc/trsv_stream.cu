@@ -4,18 +4,20 @@
 //
 // One persistent, co-resident grid.  Warp w owns tasks w, w + W, w + 2W, ...
 // of the level-ordered task list; the host serialised them into ONE contiguous
-// byte stream per warp.  The warp pulls its stream through a private
-// shared-memory ring with bulk async copies (cp.async.bulk + mbarrier
-// complete_tx, 1 KB pages, up to kPages in flight), so a task's descriptor,
-// row metadata, column ids and values are in shared memory long before the
-// task runs: the only global accesses on a task's path are the gathers of
-// the solution values it depends on, and those are issued one task ahead.
-// The solution value is the ready flag (all-ones sentinel pre-fill, one 64-bit
-// relaxed store to publish, warp-uniform polling for the rare entry that is
-// not there yet).  A task only waits on earlier tasks and every warp is
-// resident (cooperative launch), so the earliest unfinished task always
-// progresses: no deadlock, no atomics, no grid barriers.
+// byte stream per warp.  The warp pulls its stream through a private ring of
+// kStreamRing record slots in shared memory, one bulk async copy per record
+// (cp.async.bulk + mbarrier complete_tx), issued kStreamRing - 1 records
+// ahead: a task's descriptor, row metadata, column ids and values sit at
+// fixed offsets of a slot before the task runs, and the only global accesses
+// on a task's path are the gathers of the solution values it depends on,
+// requested one task ahead.  The solution value is the ready flag (all-ones
+// sentinel pre-fill, one 64-bit relaxed store to publish); a task that is
+// early polls ONE value, the dependency its latest producer writes, and only
+// then re-reads whatever else was missing.  A task only waits on earlier
+// tasks and every warp is resident (cooperative launch), so the earliest
+// unfinished task always progresses: no deadlock, no atomics, no grid barriers.
 #include <algorithm>
+#include <cstdlib>
 
 #include "device.hpp"
 #include "kernels.cuh"
@@ -26,11 +28,12 @@ namespace dev {
 
 namespace {
 
-constexpr int kRing = 8192;  // bytes per warp (StreamParams.ring)
-constexpr int kPage = 1024;  // StreamParams.page
-constexpr int kPages = kRing / kPage;
-constexpr int kWarps = 8;    // warps per CTA
-constexpr size_t kSmem = (size_t)kWarps * kRing + (size_t)kWarps * kPages * 8;
+constexpr int kR = kStreamRing;
+constexpr int kSlot = kStreamSlot;
+constexpr int kWarps = 8;  // warps per CTA
+constexpr int kMinB = 3;   // CTAs per SM
+constexpr size_t kSmem = (size_t)kWarps * kR * kSlot + (size_t)kWarps * kR * 8;
+static_assert(kR == 4, "ring: the task being reduced, the one whose gathers are in flight, two records in flight");
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
@@ -44,21 +47,35 @@ __device__ __forceinline__ bool mbar_try_wait(unsigned bar, unsigned parity) {
     return ok != 0;
 }
 
+// st_relaxed never publishes a value whose high word is all ones
+__device__ __forceinline__ bool is_sentinel(double v) { return __double2hiint(v) == -1; }
+__device__ __forceinline__ double ld_val(const double* p) { return __longlong_as_double(ld_relaxed(p)); }
+
+// one task's registers
 struct Rec {
-    int w0;       // cnt | lg << 8 | nq << 16; 0 = end of stream
-    int o;        // stream offset of the record
-    int bytes;
-    int c[4];     // this lane's column ids (-1 = empty slot)
-    double y[4];  // gathered dependencies (sentinel = not solved when read)
-    // epilogue operands, valid in the first lane of each row
-    int out, qq;
-    double b, dg, ad;
+    unsigned base;  // shared-memory address of its slot
+    int c[4];       // this lane's column ids
+    double y[4];    // gathered dependencies (sentinel = not solved when read)
+    double fy;      // the flag dependency
+    int out;        // row this lane publishes, or -1
+    double b;       // its right-hand side
 };
+
+__device__ __forceinline__ int lds_i(unsigned addr) {
+    int v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ double lds_d(unsigned addr) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+    return v;
+}
 
 }  // namespace
 
 template <bool UPPER>
-__global__ void __launch_bounds__(kWarps * 32, 3)
+__global__ void __launch_bounds__(kWarps * 32, kMinB)
     k_trsv4(StreamArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     if (a.ctrl && (a.ctrl->converged || a.ctrl->status)) return;
@@ -67,155 +84,153 @@ __global__ void __launch_bounds__(kWarps * 32, 3)
     const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
     const int gw = blockIdx.x * kWarps + wi;
     if (gw >= a.n_warps) return;
-    const unsigned char* ring = smem + (size_t)wi * kRing;
-    const unsigned ring_s = smem_u32(ring);
-    const unsigned bar_s = smem_u32(smem + (size_t)kWarps * kRing) + (unsigned)wi * kPages * 8;
-    const long long off0 = a.warp_off[gw];
-    const unsigned char* src = a.data + off0;
-    const int n_pages = (int)((a.warp_off[gw + 1] - off0) / kPage);
+    const int4 d0 = reinterpret_cast<const int4*>(a.desc)[2 * gw];
+    const int4 d1 = reinterpret_cast<const int4*>(a.desc)[2 * gw + 1];
+    const int n_tasks = d0.z;
+    if (n_tasks <= 0) return;
+    const unsigned char* src = a.data + (((long long)(unsigned)d0.x) | ((long long)d0.y << 32));
+    const unsigned ring_s = smem_u32(smem + (size_t)wi * kR * kSlot);
+    const unsigned bar_s = smem_u32(smem + (size_t)kWarps * kR * kSlot) + (unsigned)wi * kR * 8;
+    double* const out = a.out;
+    if (gw == 0 && lane == 0) st_relaxed(out + a.n_aug, 0.0);  // the dummy every empty entry points at
     if (lane == 0) {
 #pragma unroll
-        for (int q = 0; q < kPages; ++q) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_s + 8 * q));
+        for (int q = 0; q < kR; ++q) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_s + 8 * q));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
-    // lane 0 keeps the ring full: page p goes to slot p % kPages once every
-    // page below p - kPages + 1 has been released
-    int issued = 0;
-    auto issue = [&](int released) {
-        const int lim = min(n_pages, released + kPages);
-        while (issued < lim) {
-            const unsigned slot = (unsigned)issued % kPages;
-            const unsigned bar = bar_s + 8 * slot;
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(kPage) : "memory");
+    // the warp's records go round the ring in order; lane 0 requests them
+    long long o_issue = 0;
+    int rq_slot = 0;  // slot of the next record to request
+    auto request = [&](int bytes) {
+        if (lane == 0 && bytes > 0) {
+            const unsigned bar = bar_s + 8 * rq_slot;
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
             asm volatile(
                 "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                    ring_s + slot * kPage),
-                "l"(src + (size_t)issued * kPage), "r"(kPage), "r"(bar)
+                    ring_s + rq_slot * kSlot),
+                "l"(src + o_issue), "r"(bytes), "r"(bar)
                 : "memory");
-            ++issued;
         }
+        o_issue += bytes;
+        rq_slot = rq_slot == kR - 1 ? 0 : rq_slot + 1;
     };
-    if (lane == 0) issue(0);
-    int ready = 0;  // pages known to have landed (warp-uniform)
-    auto need = [&](int end_off) {
-        const int pg = (end_off + kPage - 1) / kPage;
-        while (ready < pg) {
-            const unsigned bar = bar_s + 8 * ((unsigned)ready % kPages);
-            const unsigned parity = ((unsigned)ready / kPages) & 1u;
-            while (!mbar_try_wait(bar, parity)) {
+    request(d0.w);
+    request(d1.x);
+    request(d1.y);
+    // the next record out of the ring: column ids from its slot, then the
+    // dependency gathers and the right-hand side are requested (consumed one
+    // task later; two tasks ahead with a five-slot ring and 20 warps per SM
+    // measured slower, profiles/r02)
+    int ld_slot = 0;
+    unsigned ld_parity = 0;
+    auto load = [&](Rec& r) {
+        const unsigned bar = bar_s + 8 * ld_slot;
+        while (!mbar_try_wait(bar, ld_parity)) {
+        }
+        const unsigned base = ring_s + ld_slot * kSlot;
+        if (ld_slot == kR - 1) {
+            ld_slot = 0;
+            ld_parity ^= 1u;
+        } else {
+            ++ld_slot;
+        }
+        r.base = base;
+        int w0, ahead, fc, tid;
+        asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(w0), "=r"(ahead), "=r"(fc), "=r"(tid) : "r"(base));
+        const int cnt = w0 & 0xFF, lg = (w0 >> 8) & 0xF, nq = (w0 >> 12) & 0xF;
+        r.fy = ld_val(out + fc);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            r.y[q] = 0.0;
+            r.c[q] = 0;
+            if (q < nq) {
+                r.c[q] = lds_i(base + 16 + (q * 32 + lane) * 4);
+                r.y[q] = ld_val(out + r.c[q]);
             }
-            ++ready;
         }
-    };
-    auto ld_i = [&](int off) { return *reinterpret_cast<const int*>(ring + (off & (kRing - 1))); };
-    auto ld_d = [&](int off) { return *reinterpret_cast<const double*>(ring + (off & (kRing - 1))); };
-    // header, column ids and row metadata from the ring; dependency gathers
-    // and epilogue operands issued (consumed one task later)
-    auto load = [&](int o, Rec& r) {
-        r.o = o;
-        need(o + 16);
-        const int2 h = *reinterpret_cast<const int2*>(ring + (o & (kRing - 1)));
-        r.w0 = h.x;
-        r.bytes = h.y;
-        if (r.w0 == 0) return;
-        need(o + r.bytes);
-        const int cnt = r.w0 & 0xFF, lg = (r.w0 >> 8) & 0xFF, nq = (r.w0 >> 16) & 0xFF;
-        const int col_off = o + 16 + cnt * MS;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) r.c[q] = q < nq ? ld_i(col_off + (q * 32 + lane) * 4) : -1;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) r.y[q] = r.c[q] >= 0 ? __ldca(a.out + r.c[q]) : 0.0;
-        const int seg = lane >> lg;
         r.out = -1;
-        r.qq = -1;
         r.b = 0.0;
-        r.dg = 1.0;
-        r.ad = 0.0;
-        if (seg < cnt && (lane & ((1 << lg) - 1)) == 0) {
-            const int m = o + 16 + seg * MS;
-            const int2 oi = *reinterpret_cast<const int2*>(ring + (m & (kRing - 1)));
-            r.out = oi.x;
-            if (oi.y >= 0) r.b = a.in[oi.y];
-            if (UPPER) {
-                r.qq = ld_i(m + 8);
-                r.dg = ld_d(m + 16);
-                if (a.add && r.qq >= 0) r.ad = a.add[r.qq];
-            }
+        if ((lane & ((1 << lg) - 1)) == 0 && (lane >> lg) < cnt) {
+            const unsigned m = base + 16 + nq * 384 + (lane >> lg) * MS;
+            r.out = lds_i(m);
+            const int in = lds_i(m + 4);
+            if (in >= 0) r.b = a.in[in];
         }
     };
-    // one task: prefetch the next record (its gathers fly while this task
-    // runs), wait for this task's dependencies, reduce, publish, free pages.
-    // The two record states alternate roles (no register copies: a copy of a
+    // task k: request the record kR - 1 ahead into the slot task k - 1 just
+    // left, start task k + 1, wait for this task's dependencies, reduce,
+    // publish.  Two register sets alternate (no register copies: a copy of a
     // register with a load in flight would wait for that load).
-    auto step = [&](Rec& cur, Rec& nxt) {
-        const int o_next = cur.o + cur.bytes;
-        unsigned long long t_begin = 0, t_ready = 0, t_loaded = 0;
-        int polls = 0;
+    auto step = [&](int k, Rec& cur, Rec& far) {
+        __syncwarp();  // every lane is done with task k - 1's slot
+        request(lds_i(cur.base + 4));
+        if (k + 1 < n_tasks) load(far);
+        unsigned long long t_begin = 0, t_ready = 0;
         if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
-        load(o_next, nxt);
-        if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_loaded));
-        // ---- the current task: wait for its dependencies (warp-uniform)
-        {
-            bool rd = true;
+        if (!a.nodeps) {
+            if (is_sentinel(cur.fy)) {
+                // early: poll the one value the latest producer writes
+                const double* fp = out + lds_i(cur.base + 8);
+                do {
+                    cur.fy = ld_val(fp);
+                } while (is_sentinel(cur.fy));
+            }
+            // then whatever else was not there when it was gathered
+            while (__any_sync(FULL, is_sentinel(cur.y[0]) | is_sentinel(cur.y[1]) | is_sentinel(cur.y[2]) |
+                                        is_sentinel(cur.y[3]))) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) rd = rd && __double_as_longlong(cur.y[q]) != (long long)kSentinel;
-            while (!__all_sync(FULL, rd)) {
-                rd = true;
-                ++polls;
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    if (__double_as_longlong(cur.y[q]) == (long long)kSentinel) {
-                        cur.y[q] = __longlong_as_double(ld_relaxed(a.out + cur.c[q]));
-                        rd = rd && __double_as_longlong(cur.y[q]) != (long long)kSentinel;
-                    }
-                }
+                for (int q = 0; q < 4; ++q)
+                    if (is_sentinel(cur.y[q])) cur.y[q] = ld_val(out + cur.c[q]);
             }
         }
         if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_ready));
-        const int cnt = cur.w0 & 0xFF, lg = (cur.w0 >> 8) & 0xFF, nq = (cur.w0 >> 16) & 0xFF;
-        const int val_off = cur.o + 16 + cnt * MS + nq * 128;
+        const int w0 = lds_i(cur.base);
+        const int lg = (w0 >> 8) & 0xF, nq = (w0 >> 12) & 0xF;
+        const unsigned vals = cur.base + 16 + nq * 128 + lane * 8;
         double acc = 0.0;
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-            if (q < nq) acc = __fma_rn(ld_d(val_off + (q * 32 + lane) * 8), cur.y[q], acc);
+            if (q < nq) acc = __fma_rn(lds_d(vals + q * 256), cur.y[q], acc);
         for (int s = (1 << lg) >> 1; s > 0; s >>= 1) acc += __shfl_xor_sync(FULL, acc, s);
         if (cur.out >= 0) {
             double s = cur.b - acc;
-            if (UPPER) s = s / cur.dg;
-            st_relaxed(a.out + cur.out, s);
-            if (UPPER && a.final_out && cur.qq >= 0) {
-                const double yv = a.coef * s;
-                a.final_out[cur.qq] = a.add ? cur.ad + yv : yv;
+            if (UPPER) {
+                const unsigned m = cur.base + 16 + nq * 384 + (lane >> lg) * MS;
+                s = s / lds_d(m + 16);
+                st_relaxed(out + cur.out, s);
+                const int qq = lds_i(m + 8);
+                if (a.final_out && qq >= 0) {
+                    const double yv = a.coef * s;
+                    a.final_out[qq] = a.add ? a.add[qq] + yv : yv;
+                }
+            } else {
+                st_relaxed(out + cur.out, s);
             }
         }
         if (a.trace && lane == 0) {  // debug: {level, begin, dependencies ready, published, warp}
             unsigned long long t_end;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
-            unsigned long long* tr = a.trace + 5 * (size_t)ld_i(cur.o + 12);
-            tr[0] = (unsigned long long)ld_i(cur.o + 8);
+            unsigned long long* tr = a.trace + 5 * (size_t)lds_i(cur.base + 12);
+            tr[0] = (unsigned long long)((unsigned)w0 >> 16);
             tr[1] = t_begin;
             tr[2] = t_ready;
             tr[3] = t_end;
-            tr[4] = (unsigned long long)gw | ((unsigned long long)polls << 32) |
-                    ((t_loaded - t_begin) << 44);
+            tr[4] = (unsigned long long)gw;
         }
-        // ---- pages wholly before the next record are free again
-        __syncwarp();
-        if (lane == 0) issue(o_next / kPage);
     };
     Rec ra, rb;
-    load(0, ra);
-    while (ra.w0 != 0) {
-        step(ra, rb);
-        if (rb.w0 == 0) break;
-        step(rb, ra);
+    load(ra);
+    for (int k = 0; k < n_tasks; k += 2) {
+        step(k, ra, rb);
+        if (k + 1 < n_tasks) step(k + 1, rb, ra);
     }
 }
 
-static_assert(kRing == 8192 && kPage == 1024, "StreamParams defaults (trsv_plan.hpp) must match the kernel");
+// ---- launch ------------------------------------------------------------------
+namespace {
 
-static cudaError_t stream_setup(bool upper, int num_sms, int* occ_out) {
+cudaError_t stream_setup(bool upper, int* occ_out) {
     static int occ[2] = {0, 0};
     if (!occ[upper]) {
         auto fn = upper ? (const void*)k_trsv4<true> : (const void*)k_trsv4<false>;
@@ -223,25 +238,27 @@ static cudaError_t stream_setup(bool upper, int num_sms, int* occ_out) {
         if (e != cudaSuccess) return e;
         int o = 0;
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, kWarps * 32, kSmem);
+        if (o > kMinB) o = kMinB;
         if (e != cudaSuccess) return e;
         if (o < 1) return cudaErrorLaunchOutOfResources;
         occ[upper] = o;
     }
-    (void)num_sms;
     *occ_out = occ[upper];
     return cudaSuccess;
 }
 
+}  // namespace
+
 int trsv_stream_warps(bool upper, int num_sms) {
     int occ = 0;
-    if (stream_setup(upper, num_sms, &occ) != cudaSuccess) return 0;
+    if (stream_setup(upper, &occ) != cudaSuccess) return 0;
     return num_sms * occ * kWarps;
 }
 
 cudaError_t trsv_stream(const Launch& L, bool upper, const StreamArgs& a) {
     if (a.n_warps <= 0) return cudaSuccess;
     int occ = 0;
-    cudaError_t e = stream_setup(upper, L.num_sms, &occ);
+    cudaError_t e = stream_setup(upper, &occ);
     if (e != cudaSuccess) return e;
     const unsigned grid = (unsigned)((a.n_warps + kWarps - 1) / kWarps);
     if ((long long)grid > (long long)L.num_sms * occ) return cudaErrorCooperativeLaunchTooLarge;

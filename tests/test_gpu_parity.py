@@ -10,6 +10,8 @@ Bars:
 * Transient: identical step times and per-step Krylov dimensions, waveforms
   within 1e-8 of each node's full scale (north_star tolerance).
 """
+import ctypes as C
+
 import numpy as np
 import pytest
 
@@ -294,3 +296,31 @@ def test_graph_loop_equals_eager(case, trsv, weight):
             continue
         assert ia.m == ib.m and ia.happy == ib.happy
         assert bit_equal(a, b)
+
+
+# ---- dense block in isolation: k_dense against dense_expm --------------------------
+@pytest.mark.parametrize("m", [1, 2, 7, 13, 32, 33, 41, 64, 100])
+@pytest.mark.parametrize("norm", [1e-3, 0.2, 0.9, 2.0, 5.0, 40.0, 3000.0],
+                         ids=["pade3", "pade5", "pade7", "pade9", "pade13", "squarings3", "squarings10"])
+def test_dense_expm_bit_identical(ref, m, norm):
+    """dense_expm (dense_matrix.cpp:185-225) through the dense-block kernel: every Padé degree, the
+    scaling-and-squaring branch, the shared-memory scratch (m <= 32) and the global scratch above it
+    (m up to MMAX = 100, config 2) — the same bits as the reference."""
+    rng = np.random.default_rng(1000 * m + int(norm * 10))
+    a = rng.standard_normal((m, m))
+    a *= norm / np.abs(a).sum(axis=0).max()
+    with Context(0) as c:
+        e = np.empty((m, m))
+        c._check(F.lib.exg_debug_dense_expm(c.handle, m, F.as_ptr(np.ascontiguousarray(a), C.c_double),
+                                             F.as_ptr(e, C.c_double)))
+    want = ref.dense_expm(a)
+    assert np.array_equal(e.view(np.int64), np.asarray(want).view(np.int64))
+
+
+def test_dense_expm_rejects_non_finite():
+    a = np.eye(3)
+    a[1, 2] = np.inf
+    with Context(0) as c:
+        e = np.empty((3, 3))
+        with pytest.raises(ex.NonFiniteError):
+            c._check(F.lib.exg_debug_dense_expm(c.handle, 3, F.as_ptr(a, C.c_double), F.as_ptr(e, C.c_double)))

@@ -140,3 +140,27 @@ def test_config4_fast_mode_close(ref, method):
     assert got.times[-1] == want["times"][-1]
     err = full_scale_err(got.samples[-1:], want["samples"][-1:])
     assert err <= 1e-6, f"final-state full-scale error {err:.3e}"
+
+
+@pytest.mark.parametrize("kw", C4_CUTS, ids=["12x12-4x4", "20x20-16x8"])
+@pytest.mark.parametrize("method", [F.EXG_METHOD_ER, F.EXG_METHOD_ERC], ids=["er", "erc"])
+def test_config4_refactor_policy_matches_its_oracle(ref, kw, method):
+    """BASELINE.json config 4: refactor only when the Jacobian changed by more than 10%.  The
+    oracle is the restated loop with the same policy over the reference's public API
+    (ref_transient_cached, threshold 0 pinned to transient() by tests/test_oracle.py): the same
+    steps, rejections, refactorizations and Krylov dimensions, waveforms within 1e-8 of full scale."""
+    s = ex.System.generate(4, **kw)
+    ctl = s.step_control()
+    ctl.method = method
+    ctl.refactor_threshold = 0.1
+    rec = probes(s)
+    rh = ref_system(ref, s)
+    try:
+        want = ref.transient_policy(rh, ctl, s.options().tran_stop, rec, method=method, threshold=0.1)
+    finally:
+        ref.system_free(rh)
+    with Context(0, trsv_mode=F.EXG_TRSV_EXACT, weight_mode=F.EXG_WEIGHT_APPLY) as c:
+        got = c.transient(s, ctl, s.options().tran_stop, rec)
+    assert 0 < int(np.sum(want["lu"])) < len(want["lu"]), "the policy skipped no factorization"
+    assert np.array_equal(got.lu, want["lu"]), "refactorization sequence differs"
+    compare_nonlinear(got, want)

@@ -206,3 +206,29 @@ def test_known_answer_transient_rc(ref):
         max_err = max(max_err, abs(v - v_ref))
         t_prev = t
     assert max_err <= GOLDEN["transient_rc"]["tol"]
+
+
+def test_refactor_policy_oracle_pins(ref):
+    """The restated loop with the refactor policy (exg_step_control.refactor_threshold):
+    threshold 0 is transient() as shipped bit for bit (nonlinear circuit, a factorization per
+    step); threshold 0.1 freezes the Linearization between refactorizations: fewer lu_factor
+    calls, same physics to the policy's accuracy."""
+    s = ex.System.generate(4, width=12, chains=4, stages=4)
+    ctl = s.step_control()
+    rec = np.arange(0, s.n_nodes, 5, dtype=np.int32)
+    t_stop = s.options().tran_stop
+    rh = ref_system(ref, s)
+    try:
+        a = ref.transient(rh, ctl, t_stop, rec)
+        b = ref.transient_policy(rh, ctl, t_stop, rec, threshold=0.0)
+        c = ref.transient_policy(rh, ctl, t_stop, rec, threshold=0.1)
+    finally:
+        ref.system_free(rh)
+    assert np.array_equal(a["times"], b["times"]) and bit_equal(a["samples"], b["samples"])
+    assert np.array_equal(a["dims"], b["dims"]) and np.array_equal(a["rejects"], b["rejects"])
+    assert np.all(b["lu"] == 1)
+    assert 0 < int(np.sum(c["lu"])) < int(np.sum(b["lu"])), "the policy skipped no factorization"
+    assert c["lu"][0] == 1
+    assert c["times"][-1] == a["times"][-1]
+    scale = np.max(np.abs(a["samples"]))
+    assert np.max(np.abs(c["samples"][-1] - a["samples"][-1])) <= 2e-2 * scale

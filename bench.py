@@ -395,6 +395,10 @@ def run_ours(args, rank, world, local):
                 "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                 "frac": roof[dom_roof]["frac"] if dom_roof else None, "traffic": traffic,
                 "per_kernel": roof, "l_levels": cn.l_levels, "u_levels": cn.u_levels,
+                "fast_plan": {"kind": "record streams" if cn.fast_tasks_l else "level runs",
+                              "l_levels": cn.fast_levels_l, "u_levels": cn.fast_levels_u,
+                              "l_tasks": cn.fast_tasks_l, "u_tasks": cn.fast_tasks_u,
+                              "l_stream_bytes": cn.fast_bytes_l, "u_stream_bytes": cn.fast_bytes_u},
                 "kernel_ms": ktimes}
 
     # ---- e2e: the public per-step call with HOST buffers over the SAME steps

@@ -109,6 +109,11 @@ typedef struct exg_counters {
     int64_t mgs_passes;      /* algorithmic n-vector passes of orthogonalize: J + 2 per call
                                 with J basis vectors, + J + 1 per reorthogonalisation */
     int64_t reorths;         /* reorthogonalisation passes (krylov.cpp:59) */
+    /* FAST plan actually run (0 where the level-run plan is used): dependent
+     * levels, warp tasks and stream bytes of the blocked augmented system */
+    int32_t fast_levels_l, fast_levels_u;
+    int64_t fast_tasks_l, fast_tasks_u;
+    int64_t fast_bytes_l, fast_bytes_u;
 } exg_counters;
 
 exg_status exg_create(int device, exg_ctx** out);
@@ -197,6 +202,13 @@ exg_status exg_profile_enable(exg_ctx* ctx, int on);
  * (start, end) of the warp-task sweeps for L then U (4n), then (start,
  * far-done, end) of the cluster sweeps for L then U (6n); zero = not run there */
 exg_status exg_debug_trace_solve(exg_ctx* ctx, const double* b, unsigned long long* times);
+/* debug / test: one orthogonalize step (krylov.cpp:46-78) in isolation: V is a
+ * host n x (j + 1) column-major orthonormal basis, w the vector to
+ * orthogonalise; hcol receives the j + 2 Hessenberg entries, v_next the
+ * normalised remainder (untouched on a happy breakdown), info = {happy,
+ * reorthogonalised}.  The kernel is the one the context's mode runs. */
+exg_status exg_debug_orthogonalize(exg_ctx* ctx, int n, int j, const double* V, const double* w,
+                                   double breakdown_tol, double* hcol, double* v_next, int* info);
 /* debug / test: dense_expm (dense_matrix.cpp:185-225) of a host m x m row-major
  * matrix through the dense-block kernel, bit-identical to the reference. */
 exg_status exg_debug_dense_expm(exg_ctx* ctx, int m, const double* A, double* E);

@@ -200,9 +200,10 @@ typedef struct exg_step_control {
     int32_t fixed_step;
     int32_t method;
     double gamma; /* ERC correction */
-    /* Nonlinear circuits: re-linearise and refactor G_k only when a device
-     * conductance (gm, gds) moved by more than this relative amount since the
-     * last factorization; the whole Linearization (G_k, C_k, operating points)
+    /* Nonlinear circuits: re-linearise and refactor G_k only when the device
+     * Jacobian (the stamped conductances gm, gds of all devices) changed by
+     * more than this relative amount in the Euclidean norm since the last
+     * factorization; the whole Linearization (G_k, C_k, operating points)
      * stays frozen in between.  0 = every step, as the reference
      * (integrate.cpp:419-421).  BASELINE.json config 4 names 0.1. */
     double refactor_threshold;

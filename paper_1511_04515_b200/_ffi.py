@@ -98,7 +98,10 @@ class exg_counters(C.Structure):
                 ("u_levels", C.c_int32), ("nnz_l", C.c_int64), ("nnz_u", C.c_int64),
                 ("graph_launches", C.c_int64), ("graph_builds", C.c_int64),
                 ("l_schedule", C.c_int32), ("u_schedule", C.c_int32), ("mgs_passes", C.c_int64),
-                ("reorths", C.c_int64)]
+                ("reorths", C.c_int64),
+                ("fast_levels_l", C.c_int32), ("fast_levels_u", C.c_int32),
+                ("fast_tasks_l", C.c_int64), ("fast_tasks_u", C.c_int64),
+                ("fast_bytes_l", C.c_int64), ("fast_bytes_u", C.c_int64)]
 
 
 class exg_kernel_times(C.Structure):
@@ -172,6 +175,7 @@ _DEV_PROTOS = {
     "exg_profile_enable": (I, [P, I]),
     "exg_debug_trace_solve": (I, [P, PD, C.POINTER(C.c_uint64)]),
     "exg_debug_dense_expm": (I, [P, I, PD, PD]),
+    "exg_debug_orthogonalize": (I, [P, I, I, PD, PD, D, PD, PD, PI]),
     "exg_debug_trace_stream": (I, [P, PD, C.POINTER(C.c_uint64), C.POINTER(C.c_longlong)]),
     "exg_profile_get": (I, [P, C.POINTER(exg_kernel_times)]),
     "exg_synchronize": (I, [P]),

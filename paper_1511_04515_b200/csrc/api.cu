@@ -238,18 +238,6 @@ void solve_dev(exg_ctx* c, const double* b, double* final_out, double coef, cons
                 c->prof_end(upper ? EXG_K_TRSV_U : EXG_K_TRSV_L, e0);
                 continue;
             }
-            if (P.n_atasks) {
-                // blocked augmented system: one sync-free warp-task launch
-                a.tasks = P.atasks;
-                a.n_tasks = P.n_atasks;
-                a.meta = P.ameta;
-                a.col = P.acol;
-                a.val = P.aval;
-                a.diag = P.adiag;
-                ck(exg::dev::trsv_wide(c->L(), upper, a), "augmented solve launch");
-                c->prof_end(upper ? EXG_K_TRSV_U : EXG_K_TRSV_L, e0);
-                continue;
-            }
             const bool run_timing = getenv("EXG_RUN_TIMING") != nullptr && !c->capturing;
             std::vector<cudaEvent_t> rev;
             for (const TriPlan::Run& run : P.runs) {
@@ -1405,9 +1393,14 @@ exg_status exg_set_factors(exg_ctx* c, int n, const int* Lp, const int* Li, cons
     // levels (one thread-block cluster, DSMEM hand-offs)
     // FAST plan: the blocked augmented system (default, trsv_plan.hpp), or
     // the level-run plan (wide runs + cluster chain, EXG_FAST_PLAN=chain)
-    const char* fp_env = getenv("EXG_FAST_PLAN");  // stream (default) | aug | chain
-    const std::string fplan = fp_env ? fp_env : "stream";
-    const bool use_aug = fplan != "chain";
+    // FAST plan: per-warp record streams of the blocked augmented system
+    // (k_trsv4) for large systems, whose solves stream the factors from HBM;
+    // the level-run plan (wide runs + cluster chain) for small ones, where a
+    // solve is a chain of hand-offs and the chain's DSMEM hops are the shortest
+    // (measured: config 0 and 3 run 2-3x faster on it, config 1 on the streams)
+    const char* fp_env = getenv("EXG_FAST_PLAN");  // auto (default) | stream | chain
+    std::string fplan = fp_env ? fp_env : "auto";
+    if (fplan != "stream" && fplan != "chain") fplan = n >= kStreamPlanMinRows ? "stream" : "chain";
     if (fplan == "stream") {
         // per-warp record streams (k_trsv4) over the augmented system with
         // every row cut to <= 128 entries
@@ -1451,51 +1444,11 @@ exg_status exg_set_factors(exg_ctx* c, int n, const int* Lp, const int* Li, cons
             c->cnt_aug[tri][6] = (long long)S.data.size();
             c->cnt_aug[tri][7] = S.n_warps;
         }
-    } else if (!use_aug) {
+    } else {
         plan_triangle(c, c->plan[0], false, lford, lflev, lnl_f, lp, lc, lv, ltasks_f, nullptr, nullptr, l_sub);
         plan_triangle(c, c->plan[1], true, uford, uflev, unl_f, up, uc, uv, utasks_f, &ud, col_perm, u_sub);
         build_sub(c, c->plan[0].sub, false, lcomp, lncomp, lp, lc, lv, row_perm);
         build_sub(c, c->plan[1].sub, true, ucomp, uncomp, up, uc, uv, row_perm);
-    } else {
-        exg::AugParams prm;
-        if (const char* e = getenv("EXG_AUG")) {  // min_block,max_block,chunk_over,recent,chunk
-            int v[5] = {prm.min_block, prm.max_block, prm.chunk_over, prm.recent, prm.chunk};
-            sscanf(e, "%d,%d,%d,%d,%d", &v[0], &v[1], &v[2], &v[3], &v[4]);
-            prm = exg::AugParams{v[0], v[1], v[2], v[3], v[4]};
-        }
-        std::vector<int> ident(n);
-        for (int i = 0; i < n; ++i) ident[i] = i;
-        for (int tri = 0; tri < 2; ++tri) {
-            TriPlan& P = c->plan[tri];
-            P.free_dev();
-            P.runs.clear();
-            exg::AugPlan A;
-            if (tri == 0)
-                exg::build_aug_plan(false, n, lp.data(), lc.data(), lv.data(), nullptr, row_perm, prm, A);
-            else
-                exg::build_aug_plan(true, n, up.data(), uc.data(), uv.data(), ud.data(), ident.data(), prm, A);
-            P.ameta = reinterpret_cast<int4*>(dalloc<int>(A.meta.size()));
-            P.atasks = reinterpret_cast<int2*>(dalloc<int>(std::max<size_t>(A.tasks.size(), 2)));
-            P.acol = dalloc<int>(std::max<size_t>(A.col.size(), 1));
-            P.aval = dalloc<double>(std::max<size_t>(A.val.size(), 1));
-            P.adiag = dalloc<double>(A.diag.size());
-            ck(cudaMemcpyAsync(P.ameta, A.meta.data(), A.meta.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream), "aug plan");
-            ck(cudaMemcpyAsync(P.atasks, A.tasks.data(), A.tasks.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream), "aug plan");
-            if (!A.col.empty()) {
-                ck(cudaMemcpyAsync(P.acol, A.col.data(), A.col.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream), "aug plan");
-                ck(cudaMemcpyAsync(P.aval, A.val.data(), A.val.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream), "aug plan");
-            }
-            ck(cudaMemcpyAsync(P.adiag, A.diag.data(), A.diag.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream), "aug plan");
-            ck(cudaStreamSynchronize(c->stream), "aug plan sync");  // A is released below
-            P.n_atasks = (int)(A.tasks.size() / 2);
-            P.n_aug = A.n_aug;
-            P.aug_levels = A.levels;
-            c->cnt_aug[tri][0] = A.levels;
-            c->cnt_aug[tri][1] = A.n_blocks;
-            c->cnt_aug[tri][2] = A.block_rows;
-            c->cnt_aug[tri][3] = A.n_partials;
-            c->cnt_aug[tri][4] = (long long)A.col.size();
-        }
     }
     {
         std::vector<int4> lm(n), um(n);
@@ -1531,6 +1484,13 @@ exg_status exg_set_factors(exg_ctx* c, int n, const int* Lp, const int* Li, cons
     c->cnt.u_schedule = c->alap[1];
     c->cnt.nnz_l = (long long)lc.size();
     c->cnt.nnz_u = (long long)uc.size();
+    const bool streams = c->plan[0].s_warps > 0;
+    c->cnt.fast_levels_l = streams ? (int)c->cnt_aug[0][0] : 0;
+    c->cnt.fast_levels_u = streams ? (int)c->cnt_aug[1][0] : 0;
+    c->cnt.fast_tasks_l = streams ? c->cnt_aug[0][5] : 0;
+    c->cnt.fast_tasks_u = streams ? c->cnt_aug[1][5] : 0;
+    c->cnt.fast_bytes_l = streams ? c->cnt_aug[0][6] : 0;
+    c->cnt.fast_bytes_u = streams ? c->cnt_aug[1][6] : 0;
     c->mmax_alloc = 0;  // Krylov workspace re-sized on next use
     dfree(c->V);
     c->basis_valid = false;
@@ -1975,6 +1935,68 @@ exg_status exg_debug_trace_stream(exg_ctx* c, const double* b, unsigned long lon
         ck(cudaStreamSynchronize(c->stream), "sync");
         cudaFree(tr);
     }
+    API_END(c)
+}
+
+// debug / test: one orthogonalize step (krylov.cpp:46-78) in isolation.  V:
+// host n x (j + 1) column-major orthonormal basis, w: the vector to
+// orthogonalise.  Outputs: hcol (j + 2 Hessenberg entries), v_next (n; the
+// normalised remainder, untouched on a happy breakdown), info = {happy,
+// reorthogonalised}.  FAST mode runs the grouped kernel (k_mgs2), EXACT mode
+// the column-by-column one (k_mgs).
+exg_status exg_debug_orthogonalize(exg_ctx* c, int n, int j, const double* V, const double* w,
+                                   double breakdown_tol, double* hcol, double* v_next, int* info) {
+    API_BEGIN
+    if (n < 1 || j < 0 || !V || !w || !hcol || !v_next) throw ApiError{EXG_E_CONTRACT, "exg_debug_orthogonalize: bad arguments"};
+    ensure_vectors(c, std::max(n, c->vec_n));
+    const long long ldv = ((long long)n + 31) / 32 * 32;
+    const int hld = j + 3;
+    double* dV = dalloc<double>((size_t)(j + 2) * ldv);
+    double* dw = dalloc<double>(n);
+    double* dh = dalloc<double>((size_t)(j + 1) * hld);
+    Ctrl* dc = reinterpret_cast<Ctrl*>(dalloc<char>(sizeof(Ctrl)));
+    ck(cudaMemsetAsync(dV, 0, (size_t)(j + 2) * ldv * sizeof(double), c->stream), "memset");
+    ck(cudaMemsetAsync(dh, 0, (size_t)(j + 1) * hld * sizeof(double), c->stream), "memset");
+    for (int i = 0; i <= j; ++i)
+        ck(cudaMemcpyAsync(dV + (size_t)i * ldv, V + (size_t)i * n, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream), "h2d");
+    ck(cudaMemcpyAsync(dw, w, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream), "h2d");
+    Ctrl hc;
+    std::memset(&hc, 0, sizeof hc);
+    hc.j = j;
+    hc.breakdown_tol = breakdown_tol;
+    ck(cudaMemcpyAsync(dc, &hc, sizeof hc, cudaMemcpyHostToDevice, c->stream), "h2d");
+    exg::dev::Mgs2Shape ms{};
+    if (c->opt.trsv_mode == EXG_TRSV_FAST && exg::dev::mgs2_shape(n, c->num_sms, 0, &ms)) {
+        ensure_mgs_slots(c, j + 1);
+        exg::dev::Mgs2Args a2{n, ldv, dV, dw, dh, hld, c->mgs_slots + 8, reinterpret_cast<unsigned int*>(c->mgs_slots),
+                              dc, c->mgs_inst_cap, 0, 0, 0};
+        ck(exg::dev::mgs2(c->L(), a2, ms), "mgs2 launch");
+    } else {
+        int K = 1, blocks = 1;
+        const int ks[] = {1, 2, 4, 8, 16};
+        for (int kk : ks) {
+            K = kk;
+            const long long cap = (long long)c->num_sms * std::max(1, exg::dev::mgs_max_blocks(kk));
+            blocks = (int)std::min<long long>(cap, ((long long)n + 1024LL * kk - 1) / (1024LL * kk));
+            if ((long long)blocks * 1024 * kk >= n) break;
+        }
+        if ((long long)blocks * 1024 * K < n) throw ApiError{EXG_E_CONTRACT, "vector too long for the MGS kernel"};
+        exg::dev::MgsArgs a1{n, ldv, dV, dw, dh, hld, c->partials + c->mgs_partials_off, c->bar, dc};
+        ck(exg::dev::mgs(c->L(), a1, std::min(blocks, 4096), K), "mgs launch");
+    }
+    ck(cudaMemcpyAsync(hcol, dh + (size_t)j * hld, sizeof(double) * (j + 2), cudaMemcpyDeviceToHost, c->stream), "d2h");
+    ck(cudaMemcpyAsync(&hc, dc, sizeof hc, cudaMemcpyDeviceToHost, c->stream), "d2h");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    if (!hc.happy)
+        ck(cudaMemcpy(v_next, dV + (size_t)(j + 1) * ldv, sizeof(double) * n, cudaMemcpyDeviceToHost), "d2h");
+    if (info) {
+        info[0] = hc.happy;
+        info[1] = (int)hc.reorths;
+    }
+    cudaFree(dV);
+    cudaFree(dw);
+    cudaFree(dh);
+    cudaFree(dc);
     API_END(c)
 }
 

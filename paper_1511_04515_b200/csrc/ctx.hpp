@@ -18,6 +18,7 @@ struct DCsr {
 
 constexpr size_t kTrsvHdr = 1024;  // ticket counters ahead of the solve scratch
 constexpr int kMaxTickets = 256;
+constexpr int kStreamPlanMinRows = 250000;  // FAST plan: record streams from this size up, level runs below
 
 // FAST-mode execution plan of one triangle (see plan_triangle, api.cu)
 // subtree phase of one triangle (k_trsv_sub): components of the bottom of
@@ -73,15 +74,7 @@ struct TriPlan {
     int2* crq = nullptr;
     long long chain_rows = 0, chain_slots = 0;  // scratch of the chain runs (s values, partial slots)
     SubPlan sub;
-    // blocked augmented system (trsv_plan.hpp): one k_trsv3 launch over
-    // n_aug unknowns; used when aug_tasks > 0
-    int4* ameta = nullptr;
-    int2* atasks = nullptr;
-    int* acol = nullptr;
-    double* aval = nullptr;
-    double* adiag = nullptr;
-    int n_atasks = 0;
-    long long n_aug = 0;
+    long long n_aug = 0;   // unknowns of the augmented system (stream plan)
     int aug_levels = 0;
     // per-warp record streams of the augmented system (k_trsv4); used when s_warps > 0
     unsigned char* sdata = nullptr;
@@ -95,14 +88,6 @@ struct TriPlan {
         sdesc = nullptr;
         s_warps = 0;
         s_bytes = 0;
-        void* ps[] = {ameta, atasks, acol, aval, adiag};
-        for (void* p : ps)
-            if (p) cudaFree(p);
-        ameta = nullptr;
-        atasks = nullptr;
-        acol = nullptr;
-        aval = adiag = nullptr;
-        n_atasks = 0;
         n_aug = 0;
         aug_levels = 0;
     }

@@ -1,5 +1,6 @@
 // extern "C" glue for the host-side API declared in include/exg_host.h.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 

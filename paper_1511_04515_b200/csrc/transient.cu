@@ -120,21 +120,25 @@ void upload_linearization(exg_ctx* ctx, const exg::Linearization& lin, const exg
     chk(ctx, exg_set_oppoints(ctx, op.data()));
 }
 
-// largest relative move of a device conductance (gm, gds) between two
-// linearizations of the same circuit: the "Jacobian change" of the refactor
+// relative change of the device Jacobian (the stamped conductances gm, gds of
+// every device) between two linearizations of the same circuit, in the
+// Euclidean norm: the "Jacobian change" of the refactor
 // policy (exg_step_control.refactor_threshold; restated identically in
 // oracle/ref_shim.cpp)
 double jacobian_change(const exg::Linearization& a, const exg::Linearization& b) {
-    double worst = 0.0;
-    auto rel = [&](double x, double y) {
-        const double d = std::fabs(x - y), m = std::max(std::fabs(x), std::fabs(y));
-        if (d > 0.0) worst = std::max(worst, d / m);
-    };
+    // || (gm, gds)_b - (gm, gds)_a ||_2 / || (gm, gds)_a ||_2 over all devices,
+    // summed in device order (the same arithmetic in the product and its oracle)
+    double num = 0.0, den = 0.0;
     for (size_t i = 0; i < a.op.size(); ++i) {
-        rel(a.op[i].gm, b.op[i].gm);
-        rel(a.op[i].gds, b.op[i].gds);
+        const double dm = b.op[i].gm - a.op[i].gm, dd = b.op[i].gds - a.op[i].gds;
+        num += dm * dm;
+        num += dd * dd;
+        den += a.op[i].gm * a.op[i].gm;
+        den += a.op[i].gds * a.op[i].gds;
     }
-    return worst;
+    if (num == 0.0) return 0.0;
+    if (den == 0.0) return std::numeric_limits<double>::infinity();
+    return std::sqrt(num / den);
 }
 
 // integrate.cpp:368-480 with nonlinear devices

@@ -199,10 +199,17 @@ void build_aug_plan(bool upper, int n, const int* ptr, const int* col, const dou
                 const int pid = new_id();
                 Row pr{pid, -1, 1.0, (long long)ecol.size(), 0};
                 int pl = 0;
+                for (int z = c0; z < c1; ++z) pl = std::max(pl, tmp[z].first + 1);
+                // within a row the order is free: by column where the rows
+                // are cut for the stream kernel, so that neighbouring lanes
+                // gather neighbouring values (4 per 32-byte sector)
+                if (prm.cap > 0)
+                    std::sort(tmp.begin() + c0, tmp.begin() + c1, [&](const std::pair<int, int>& x, const std::pair<int, int>& y) {
+                        return tcol[x.second] < tcol[y.second];
+                    });
                 for (int z = c0; z < c1; ++z) {
                     ecol.push_back(tcol[tmp[z].second]);
                     eval.push_back(tval[tmp[z].second]);
-                    pl = std::max(pl, tmp[z].first + 1);
                 }
                 pr.e1 = (long long)ecol.size();
                 level[pid] = pl;
@@ -229,9 +236,14 @@ void build_aug_plan(bool upper, int n, const int* ptr, const int* col, const dou
             tmp[k] = {level[tcol[k]], k};
             lmax = std::max(lmax, tmp[k].first);
         }
-        std::stable_sort(tmp.begin(), tmp.end(), [&](const std::pair<int, int>& x, const std::pair<int, int>& y) {
-            return upper ? x.first > y.first : x.first < y.first;
-        });
+        if (prm.cap > 0)
+            std::sort(tmp.begin(), tmp.end(), [&](const std::pair<int, int>& x, const std::pair<int, int>& y) {
+                return tcol[x.second] < tcol[y.second];
+            });
+        else
+            std::stable_sort(tmp.begin(), tmp.end(), [&](const std::pair<int, int>& x, const std::pair<int, int>& y) {
+                return upper ? x.first > y.first : x.first < y.first;
+            });
         for (int k = 0; k < m; ++k) {
             ecol.push_back(tcol[tmp[k].second]);
             eval.push_back(tval[tmp[k].second]);
@@ -262,28 +274,6 @@ void build_aug_plan(bool upper, int n, const int* ptr, const int* col, const dou
         const int s = B.b - B.a;
         ++P.n_blocks;
         P.block_rows += s;
-        if (getenv("EXG_FOLD_STATS")) {  // development: pattern growth of inv(T_BB) * T_B,ext
-            static std::vector<int> mark;
-            if ((int)mark.size() < n) mark.assign(n, -1);
-            long long uni = 0, run = 0, ext = 0;
-            for (int z = 0; z < s; ++z) {
-                const int i = upper ? s - 1 - z : z;
-                const int rr = B.a + i;
-                for (int k = ptr[rr]; k < ptr[rr + 1]; ++k) {
-                    const int c = col[k];
-                    if (c >= B.a && c < B.b) continue;
-                    ++ext;
-                    if (mark[c] != B.a) {
-                        mark[c] = B.a;
-                        ++run;
-                    }
-                }
-                uni += run;
-            }
-            P.fold_ext += ext;
-            P.fold_union += uni;
-            if (s >= 256) fprintf(stderr, "block rows %d ext %lld union %lld inv %lld\n", s, ext, uni, (long long)s * s / 2);
-        }
         P.max_block = std::max(P.max_block, s);
         yid.assign(s, -1);
         // y rows: the external part of every block row
@@ -540,7 +530,18 @@ void build_stream_plan(const AugPlan& P, bool upper, const int* out_index, const
             S.n_entries += k1 - k0;
         }
         S.n_slots += T.nq * 32;
+        // distinct 32-byte sectors the task's gather instructions touch
+        for (int q = 0; q < T.nq; ++q) {
+            int sec[32];
+            for (int l = 0; l < 32; ++l) sec[l] = get<int>(S.data.data() + col_at + 4 * (size_t)(q * 32 + l)) >> 2;
+            std::sort(sec, sec + 32);
+            S.n_gather_sectors += std::unique(sec, sec + 32) - sec;
+        }
     }
+    if (getenv("EXG_PLAN_VERBOSE"))
+        fprintf(stderr, "stream plan %s: tasks %lld entries %lld gather sectors %lld (%.2f per entry) bytes %zu levels %d\n",
+                upper ? "U" : "L", S.n_tasks, S.n_entries, S.n_gather_sectors,
+                (double)S.n_gather_sectors / (double)std::max<long long>(1, S.n_entries), S.data.size(), S.levels);
 }
 
 void eval_stream_plan(const StreamPlan& S, bool upper, const double* in, double* out, double* final_out,

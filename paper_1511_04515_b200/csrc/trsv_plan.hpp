@@ -38,7 +38,6 @@ struct AugPlan {
     long long block_rows = 0;
     int max_block = 0;
     long long n_partials = 0;
-    long long fold_ext = 0, fold_union = 0;  // development statistics (EXG_FOLD_STATS)
     // per level-order position: {out id, in index or -1, k0, k1}
     std::vector<int> meta;   // 4 ints per position
     std::vector<int> col;    // dependency ids (into the augmented unknowns)
@@ -113,6 +112,7 @@ struct StreamPlan {
     int levels = 0;
     long long n_aug = 0;          // unknowns; out[n_aug] is the dummy (0.0)
     long long n_tasks = 0, n_rows = 0, n_entries = 0, n_slots = 0;
+    long long n_gather_sectors = 0;  // distinct 32-byte sectors over all gather instructions
     int max_record = 0;
     std::vector<int> desc;        // 8 ints per warp
     std::vector<unsigned char> data;

@@ -324,3 +324,62 @@ def test_dense_expm_rejects_non_finite():
         e = np.empty((3, 3))
         with pytest.raises(ex.NonFiniteError):
             c._check(F.lib.exg_debug_dense_expm(c.handle, 3, F.as_ptr(a, C.c_double), F.as_ptr(e, C.c_double)))
+
+
+# ---- orthogonalize in isolation: k_mgs / k_mgs2 against krylov.cpp:46-78 --------
+def _orthogonalize_ref(V, w, tol):
+    """The reference's modified Gram-Schmidt with one conditional re-orthogonalisation."""
+    w = w.copy()
+    j = V.shape[1] - 1
+    pre = np.sqrt(np.dot(w, w))
+    h = np.zeros(j + 2)
+    for i in range(j + 1):
+        h[i] = np.dot(w, V[:, i])
+        w -= h[i] * V[:, i]
+    post = np.sqrt(np.dot(w, w))
+    re = post < 0.70710678118654752 * pre
+    if re:
+        for i in range(j + 1):
+            s = np.dot(w, V[:, i])
+            w -= s * V[:, i]
+            h[i] += s
+        post = np.sqrt(np.dot(w, w))
+    h[j + 1] = post
+    happy = post <= tol * pre
+    return h, (None if happy else w / post), happy, re
+
+
+@pytest.mark.parametrize("mode", [F.EXG_TRSV_EXACT, F.EXG_TRSV_FAST], ids=["k_mgs", "k_mgs2"])
+@pytest.mark.parametrize("n,j", [(1024, 0), (1024, 5), (11417, 12), (44640, 7), (300000, 3), (300000, 17),
+                                 (1000800, 9)])
+@pytest.mark.parametrize("kind", ["generic", "reorth", "happy"])
+def test_orthogonalize_matches_reference(mode, n, j, kind):
+    """One Arnoldi orthogonalisation step: Hessenberg column, next basis vector, the
+    re-orthogonalisation trigger and the happy-breakdown flag, for one-CTA, few-CTA and full-grid
+    shapes (k_mgs2's groups of 1..4 columns and its tile ring)."""
+    rng = np.random.default_rng(n + 31 * j)
+    V, _ = np.linalg.qr(rng.standard_normal((n, j + 1)))
+    if kind == "generic":
+        w = rng.standard_normal(n)
+    elif kind == "reorth":  # mostly inside span(V): the norm drops by far more than 1/sqrt(2)
+        w = V @ rng.standard_normal(j + 1) + 1e-3 * rng.standard_normal(n)
+    else:  # inside span(V) to rounding: happy breakdown
+        w = V @ rng.standard_normal(j + 1)
+    tol = 1e-9 if kind == "happy" else 1e-12
+    h_want, v_want, happy_want, re_want = _orthogonalize_ref(V, w, tol)
+    with Context(0, trsv_mode=mode) as c:
+        h = np.zeros(j + 2)
+        v = np.zeros(n)
+        info = np.zeros(2, np.int32)
+        Vf = np.asfortranarray(V)
+        c._check(F.lib.exg_debug_orthogonalize(c.handle, n, j, F.as_ptr(Vf, C.c_double), F.as_ptr(w, C.c_double), tol,
+                                                F.as_ptr(h, C.c_double), F.as_ptr(v, C.c_double),
+                                                F.as_ptr(info, C.c_int)))
+    assert bool(info[0]) == happy_want
+    assert bool(info[1]) == re_want
+    scale = np.linalg.norm(w)
+    assert np.max(np.abs(h[: j + 1] - h_want[: j + 1])) <= 1e-12 * scale
+    if not happy_want:
+        assert abs(h[j + 1] - h_want[j + 1]) <= 1e-9 * max(h_want[j + 1], 1e-300) + 1e-13 * scale
+        assert np.max(np.abs(v - v_want)) <= 1e-8
+        assert np.max(np.abs(V.T @ v)) <= 1e-10

@@ -33,6 +33,9 @@ from paper_1511_04515_b200.device import Context  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--configs", default="0,1,2,3,4")
 ap.add_argument("--cpu-seconds", type=float, default=20.0)
+ap.add_argument("--threshold", type=float, default=0.1,
+                help="config 4: refactor threshold (BASELINE.json names 0.1; 0 = every step, the reference)")
+ap.add_argument("--exact4", action="store_true", help="config 4 in EXACT + APPLY mode (the parity modes)")
 ap.add_argument("--out", default=str(ROOT / "gpurun_out" / "configs.json"))
 args = ap.parse_args()
 
@@ -50,7 +53,11 @@ for cfg in [int(x) for x in args.configs.split(",")]:
     rng = np.random.default_rng(5)
     rec = np.sort(rng.choice(s.n_nodes, size=min(16, s.n_nodes), replace=False)).astype(np.int32)
     print(f"config {cfg}: n={n}, GPU transient to {t_stop:g} s ...", file=sys.stderr, flush=True)
-    with Context(0, trsv_mode=F.EXG_TRSV_FAST, weight_mode=F.EXG_WEIGHT_GSPMV) as c:
+    if cfg == 4:
+        ctl.refactor_threshold = args.threshold
+    exact = cfg == 4 and args.exact4
+    with Context(0, trsv_mode=F.EXG_TRSV_EXACT if exact else F.EXG_TRSV_FAST,
+                 weight_mode=F.EXG_WEIGHT_APPLY if exact else F.EXG_WEIGHT_GSPMV) as c:
         c.reset_counters()
         got = c.transient(s, ctl, t_stop, rec)
         cn = c.counters()
@@ -67,6 +74,31 @@ for cfg in [int(x) for x in args.configs.split(",")]:
          "dc_s": round(got.dc_s, 3), "gen_s": round(gen_s, 2), "l_levels": cn.l_levels,
          "u_levels": cn.u_levels, "gpu_launches": int(cn.kernel_launches),
          "graph_launches": int(cn.graph_launches)}
+    if cfg == 4:
+        # parity against the committed golden transient of the same policy (tools/make_golden.py:
+        # the restated loop over the unmodified reference, full size)
+        r["modes"] = "exact+apply" if exact else "fast+gspmv"
+        r["refactor_threshold"] = args.threshold
+        r["lu_count"] = int(np.sum(got.lu_count))
+        name = "config4_er_full.npz" if args.threshold == 0 else f"config4_er_th{args.threshold:g}_full.npz"
+        gp = ROOT / "tests" / "golden" / name
+        if gp.exists():
+            z = np.load(gp)
+            m = min(len(z["times"]), len(got.times))
+            same_t = bool(len(z["times"]) == len(got.times) and np.array_equal(z["times"], got.times))
+            fs = np.max(np.abs(z["samples"]), axis=0)
+            fs[fs == 0] = 1.0
+            same_rec = bool(np.array_equal(z["rec"], rec))
+            err = float(np.max(np.abs(got.samples[:m] - z["samples"][:m]) / fs)) if (m and same_rec) else None
+            gd = [d for ds in got.krylov_dims for d in ds]
+            r["parity"] = {"golden": name, "same_times": same_t, "same_rejects": bool(np.array_equal(z["rejects"], got.rejects)) if same_t else False,
+                           "krylov_dims_equal": bool(np.array_equal(z["dims"], np.asarray(gd))), "full_scale_err": err,
+                           "tol": 1e-8, "golden_wall_s": json.loads(str(z["meta"])).get("wall_s")}
+            gw = json.loads(str(z["meta"])).get("wall_s")
+            if gw:
+                r["cpu_baseline"] = {"steps_per_s": round(len(z["t"]) / gw, 4), "cores": 1, "kind": "reference",
+                                     "sample": "the whole golden transient (restated loop over the unmodified "
+                                               "reference, same policy), wall time of tools/make_golden.py here"}
     # ---- CPU reference sample (linear configs)
     if s.n_mos == 0:
         from helpers_bench import ref_system_for

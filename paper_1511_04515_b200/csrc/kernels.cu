@@ -107,7 +107,24 @@ __global__ void __launch_bounds__(256)
     double acc = 0.0;
     if (r < n_rows) {
         const int k1 = __ldg(rowptr + r + 1);
-        for (int k = __ldg(rowptr + r) + sub; k < k1; k += 4) acc = __fma_rn(__ldcs(val + k), xs[__ldcs(col + k)], acc);
+        int k = __ldg(rowptr + r) + sub;
+        // the first four entries of the lane (a 16-entry row) are requested
+        // together, then their gathers, then the multiply-adds in order: four
+        // loads in flight per lane instead of one dependent chain
+        int c[4];
+        double v[4], xv[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const bool ok = k + 4 * q < k1;
+            c[q] = ok ? __ldcs(col + k + 4 * q) : -1;
+            v[q] = ok ? __ldcs(val + k + 4 * q) : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) xv[q] = c[q] >= 0 ? xs[c[q]] : 0.0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (c[q] >= 0) acc = __fma_rn(v[q], xv[q], acc);
+        for (k += 16; k < k1; k += 4) acc = __fma_rn(__ldcs(val + k), xs[__ldcs(col + k)], acc);
     }
     acc += __shfl_xor_sync(0xffffffffu, acc, 1);
     acc += __shfl_xor_sync(0xffffffffu, acc, 2);

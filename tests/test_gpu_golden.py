@@ -85,3 +85,17 @@ def test_config4_full_size(method):
         got = c.transient(s, ctl, s.options().tran_stop, want["rec"])
     assert np.array_equal(got.t, want["t"]), "accepted step times differ"
     compare(got, want)
+
+
+def test_config4_refactor_policy_full_size():
+    """Config 4 as BASELINE.json states it (refactor when the Jacobian changed by more than 10%)
+    against the golden transient of the restated loop with the same policy."""
+    want = fixture("config4_er_th0.1_full.npz")
+    s = ex.System.generate(4)
+    ctl = control(s, 4, F.EXG_METHOD_ER)
+    ctl.refactor_threshold = 0.1
+    with Context(0, trsv_mode=F.EXG_TRSV_EXACT, weight_mode=F.EXG_WEIGHT_APPLY) as c:
+        got = c.transient(s, ctl, s.options().tran_stop, want["rec"])
+    assert np.array_equal(got.t, want["t"]), "accepted step times differ"
+    assert int(np.sum(got.lu_count)) < len(got.t), "the policy skipped no factorization"
+    compare(got, want)

@@ -129,6 +129,7 @@ def main():
     meta["steps"] = int(len(want["t"]))
     meta["mevps"] = int(len(want["dims"]))
     meta["rejects"] = int(np.sum(want["rejects"]))
+    meta["lu_factor_calls"] = int(np.sum(want["lu"])) if "lu" in want else None
     meta["threshold"] = args.threshold
     suffix = f"_{args.method}" if cfg == 4 else ""
     if cfg == 4 and args.threshold:
@@ -136,7 +137,7 @@ def main():
     out = Path(args.out) if args.out else GOLDEN / f"config{cfg}{suffix}_full.npz"
     np.savez_compressed(out, times=want["times"], samples=want["samples"], t=want["t"], h=want["h"],
                         rejects=want["rejects"], dims=want["dims"], dims_off=want["dims_off"],
-                        err=want["err"], rec=rec, lu_sha=np.array(lu_sha), meta=np.array(json.dumps(meta)))
+                        err=want["err"], lu=want.get("lu", np.zeros(0, np.int32)), rec=rec, lu_sha=np.array(lu_sha), meta=np.array(json.dumps(meta)))
     print(f"[golden c{cfg}] wrote {out} {json.dumps(meta)}", flush=True)
 
 

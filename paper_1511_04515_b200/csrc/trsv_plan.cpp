@@ -519,7 +519,7 @@ void build_stream_plan(const AugPlan& P, bool upper, const int* out_index, const
             if (upper) {
                 put<int>(S.data, m + 8, (out_index && out < P.n) ? out_index[out] : -1);
                 put<int>(S.data, m + 12, 0);
-                put<double>(S.data, m + 16, P.diag[out]);
+                put<double>(S.data, m + 16, 1.0 / P.diag[out]);  // FAST: multiply by the reciprocal
             }
             for (int e = 0; e < k1 - k0; ++e) {
                 const int sl = e & (lpr - 1), q = e >> T.lg;
@@ -558,9 +558,16 @@ void eval_stream_plan(const StreamPlan& S, bool upper, const double* in, double*
         if (left[w]-- <= 0) throw std::runtime_error("stream plan: task count mismatch");
         const unsigned char* r = S.data.data() + cur[w];
         const int w0 = get<int>(r);
-        const int cnt = w0 & 0xFF, lg = (w0 >> 8) & 0xF, nq = (w0 >> 12) & 0xF, lpr = 1 << lg;
+        const int cnt = w0 & 0xFF, lg = (w0 >> 8) & 0xF, nq = (w0 >> 12) & 0x7, lpr = 1 << lg;
         if (get<int>(r + 12) != (int)t) throw std::runtime_error("stream plan: record order mismatch");
-        cur[w] += (16 + nq * 384 + cnt * MS + 15) / 16 * 16;
+        const int rb = (16 + nq * 384 + cnt * MS + 15) / 16 * 16;
+        // integrity of what the kernel will trust: sizes, ids, the look-ahead size
+        if (cnt < 1 || cnt > 32 || lg > 5 || (cnt << lg) > 32 || nq > 4 || rb > kStreamSlot ||
+            (size_t)(cur[w] + rb) > S.data.size())
+            throw std::runtime_error("stream plan: malformed record header");
+        const int fc = get<int>(r + 8);
+        if (fc < 0 || fc > S.n_aug) throw std::runtime_error("stream plan: flag column out of range");
+        cur[w] += rb;
         const unsigned char* cols = r + 16;
         const unsigned char* vals = cols + (size_t)nq * 128;
         const unsigned char* meta = vals + (size_t)nq * 256;
@@ -569,6 +576,7 @@ void eval_stream_plan(const StreamPlan& S, bool upper, const double* in, double*
             double a = 0.0;
             for (int q = 0; q < nq; ++q) {
                 const int c = get<int>(cols + 4 * (size_t)(q * 32 + lane));
+                if (c < 0 || c > S.n_aug) throw std::runtime_error("stream plan: column id out of range");
                 a = std::fma(get<double>(vals + 8 * (size_t)(q * 32 + lane)), out[c], a);
             }
             acc[lane] = a;
@@ -581,8 +589,9 @@ void eval_stream_plan(const StreamPlan& S, bool upper, const double* in, double*
         for (int seg = 0; seg < cnt; ++seg) {
             const unsigned char* m = meta + (size_t)seg * MS;
             const int o = get<int>(m), i = get<int>(m + 4);
+            if (o < 0 || o >= S.n_aug || i >= S.n) throw std::runtime_error("stream plan: row id out of range");
             double s = (i >= 0 ? in[i] : 0.0) - acc[seg * lpr];
-            if (upper) s = s / get<double>(m + 16);
+            if (upper) s = s * get<double>(m + 16);
             out[o] = s;
             if (upper && final_out) {
                 const int qq = get<int>(m + 8);

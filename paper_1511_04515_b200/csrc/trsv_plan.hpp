@@ -93,7 +93,7 @@ void eval_aug_plan(const AugPlan& P, bool upper, const double* in, double* out);
 //                value is always 0.0
 //   nq x 32 values (fp64)
 //   cnt metas    L: {out id, rhs index or -1}                                 (8 B)
-//                U: {out id, rhs index or -1, epilogue index or -1, 0, diag}  (24 B)
+//                U: {out id, rhs index or -1, epilogue index or -1, 0, 1 / diag}  (24 B)
 // Lane l = seg * 2^lg + sl owns entries sl, sl + 2^lg, ... of row seg, stored
 // at slot q * 32 + l (conflict-free shared-memory reads, coalesced in HBM).
 // desc holds 8 ints per warp: {stream offset (lo, hi), tasks, bytes of its

@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinB)
         r.base = base;
         int w0, ahead, fc, tid;
         asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(w0), "=r"(ahead), "=r"(fc), "=r"(tid) : "r"(base));
-        const int cnt = w0 & 0xFF, lg = (w0 >> 8) & 0xF, nq = (w0 >> 12) & 0xF;
+        const int cnt = w0 & 0xFF, lg = (w0 >> 8) & 0xF, nq = (w0 >> 12) & 0x7;
         r.fy = ld_val(out + fc);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -171,6 +171,9 @@ __global__ void __launch_bounds__(kWarps * 32, kMinB)
         if (!a.nodeps) {
             if (is_sentinel(cur.fy)) {
                 // early: poll the one value the latest producer writes
+                // (re-reading every missing value on thin levels while polling,
+                // and issuing the first re-read before the next task's load, both
+                // measured slower: profiles/r02)
                 const double* fp = out + lds_i(cur.base + 8);
                 do {
                     cur.fy = ld_val(fp);
@@ -186,7 +189,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinB)
         }
         if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_ready));
         const int w0 = lds_i(cur.base);
-        const int lg = (w0 >> 8) & 0xF, nq = (w0 >> 12) & 0xF;
+        const int lg = (w0 >> 8) & 0xF, nq = (w0 >> 12) & 0x7;
         const unsigned vals = cur.base + 16 + nq * 128 + lane * 8;
         double acc = 0.0;
 #pragma unroll
@@ -197,7 +200,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinB)
             double s = cur.b - acc;
             if (UPPER) {
                 const unsigned m = cur.base + 16 + nq * 384 + (lane >> lg) * MS;
-                s = s / lds_d(m + 16);
+                s = s * lds_d(m + 16);  // 1 / diag (FAST mode)
                 st_relaxed(out + cur.out, s);
                 const int qq = lds_i(m + 8);
                 if (a.final_out && qq >= 0) {

@@ -383,3 +383,31 @@ def test_orthogonalize_matches_reference(mode, n, j, kind):
         assert abs(h[j + 1] - h_want[j + 1]) <= 1e-9 * max(h_want[j + 1], 1e-300) + 1e-13 * scale
         assert np.max(np.abs(v - v_want)) <= 1e-8
         assert np.max(np.abs(V.T @ v)) <= 1e-10
+
+
+# ---- run-to-run determinism of the polling / mbarrier kernels (compute-sanitizer is not available on
+# the GPU pool: a data race or a read of a not-yet-published value would show up here as differing bits)
+@pytest.mark.parametrize("cfg,kw", [(1, dict(width=64)), (1, dict(width=600)), (3, dict(n=3000))],
+                         ids=["c1-64-levelruns", "c1-600-streams", "c3-3000"])
+def test_fast_path_bits_repeat(cfg, kw):
+    s = ex.System.generate(cfg, **kw)
+    f = ex.lu_factor(s.G)
+    rng = np.random.default_rng(3)
+    b = rng.uniform(-1, 1, s.n)
+    v = rng.uniform(-1, 1, s.n)
+    outs, mevps = [], []
+    for rep in range(3):
+        with _ctx(s, f, F.EXG_TRSV_FAST) as c:
+            c.set_options(trsv_mode=F.EXG_TRSV_FAST, weight_mode=F.EXG_WEIGHT_GSPMV,
+                          loop_mode=F.EXG_LOOP_GRAPH if rep != 1 else F.EXG_LOOP_EAGER)
+            xs = [c.solve(b) for _ in range(4)]
+            for x in xs[1:]:
+                assert np.array_equal(x.view(np.int64), xs[0].view(np.int64)), "FAST solve bits differ run to run"
+            outs.append(xs[0])
+            val, info = c.mevp_iks(v, 2e-12, eps=1e-9, m_max=40)
+            mevps.append((val, info.m))
+    for x in outs[1:]:
+        assert np.array_equal(x.view(np.int64), outs[0].view(np.int64)), "FAST solve bits differ between contexts"
+    for val, m in mevps[1:]:
+        assert m == mevps[0][1]
+        assert np.array_equal(val.view(np.int64), mevps[0][0].view(np.int64)), "MEVP bits differ between runs / loop modes"

@@ -52,6 +52,10 @@ for cfg in [int(x) for x in args.configs.split(",")]:
     n = s.n
     rng = np.random.default_rng(5)
     rec = np.sort(rng.choice(s.n_nodes, size=min(16, s.n_nodes), replace=False)).astype(np.int32)
+    if cfg == 4:  # probe the unknowns the golden transient of the same policy recorded
+        name = "config4_er_full.npz" if args.threshold == 0 else f"config4_er_th{args.threshold:g}_full.npz"
+        if (ROOT / "tests" / "golden" / name).exists():
+            rec = np.load(ROOT / "tests" / "golden" / name)["rec"].astype(np.int32)
     print(f"config {cfg}: n={n}, GPU transient to {t_stop:g} s ...", file=sys.stderr, flush=True)
     if cfg == 4:
         ctl.refactor_threshold = args.threshold

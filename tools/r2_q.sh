@@ -14,9 +14,9 @@ c.set_system(s); c.set_factors(f)
 b = np.random.default_rng(0).uniform(-1, 1, s.n)
 import ctypes as C
 F.lib.exg_profile_enable(c.handle, 1)
-for _ in range(20): c.solve(b)
+for _ in range(30): c.solve(b)
 kt = F.exg_kernel_times()
 F.lib.exg_profile_get(c.handle, C.byref(kt))
-print(os.environ.get("EXG_STREAM_SHAPE"), os.environ.get("EXG_STREAM_NODEPS"), "ms per launch:", [round(kt.ms[k]/max(1,kt.count[k]),4) for k in range(len(kt.ms)) if kt.count[k]])
+print("thin", os.environ.get("EXG_STREAM_THIN"), "opts", os.environ.get("EXG_STREAM_OPTS"), "ms per launch:", [round(kt.ms[k]/max(1,kt.count[k]),4) for k in range(len(kt.ms)) if kt.count[k]])
 PY
-for sh in 0 1 3; do for nd in 1 0; do EXG_STREAM_SHAPE=$sh EXG_STREAM_NODEPS=$nd timeout 600 python /tmp/solve_time.py 2>&1 | tail -1; done; done
+for th in 0 2000 500; do for op in 0 1; do EXG_STREAM_THIN=$th EXG_STREAM_OPTS=$op timeout 600 python /tmp/solve_time.py 2>&1 | tail -1; done; done

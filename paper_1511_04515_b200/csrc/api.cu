@@ -1414,6 +1414,7 @@ exg_status exg_set_factors(exg_ctx* c, int n, const int* Lp, const int* Li, cons
             P.runs.clear();
             exg::StreamParams sp;
             sp.n_warps = exg::dev::trsv_stream_warps(tri == 1, c->num_sms);
+            exg::stream_params_env(sp);
             if (sp.n_warps <= 0) throw ApiError{EXG_E_CUDA, "k_trsv4 cannot be launched on this device"};
             exg::StreamPlan S;
             {

@@ -289,6 +289,7 @@ exg_status exg_stream_plan_solve(int upper, int n, const int* ptr, const int* co
     exg::StreamParams sp;
     sp.n_warps = n_warps;
     sp.min_tasks_per_warp = 0;  // exactly the caller's warp count
+    exg::stream_params_env(sp);
     exg::StreamPlan S;
     exg::build_stream_plan(P, upper != 0, out_index, sp, S);
     if (b && x) {

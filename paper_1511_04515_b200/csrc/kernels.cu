@@ -131,6 +131,50 @@ __global__ void __launch_bounds__(256)
     if (r < n_rows && sub == 0) y[r] = acc;
 }
 
+// The same rows, lanes and arithmetic as k_spmv_v4, with the rows laid out for
+// the L1: CTA b owns ONE contiguous slice of rows and walks it strip by strip,
+// so the x values a strip gathers (a window of a few grid rows either side:
+// the reach of the coupling capacitors) were mostly fetched by the strips
+// just before it and are still in this SM's L1.  k_spmv_v4's grid order puts
+// co-resident CTAs ~10k rows apart: every gather sector then comes from L2
+// (3.5x the DRAM bytes of the launch, ncu profiles/r02), which is what bounds it.
+constexpr int kSpmvStripThreads = 1024;
+__global__ void __launch_bounds__(kSpmvStripThreads, 1)
+    k_spmv_v4s(const int* __restrict__ rowptr, const int* __restrict__ col,
+               const double* __restrict__ val, int n_rows, int rows_per_cta, double* __restrict__ y,
+               const Ctrl* ctrl, const double* __restrict__ xcol_base, long long ldv) {
+    if (ctrl->converged || ctrl->status) return;
+    const double* xs = xcol_base + (long long)ctrl->j * ldv;
+    const int sub = threadIdx.x & 3;
+    const int r0 = blockIdx.x * rows_per_cta;
+    const int r1 = min(n_rows, r0 + rows_per_cta);
+    for (int rb = r0; rb < r1; rb += kSpmvStripThreads / 4) {  // whole warps stay in the loop (shuffles)
+        const int r = rb + (threadIdx.x >> 2);
+        double acc = 0.0;
+        if (r < r1) {
+            const int k1 = __ldg(rowptr + r + 1);
+            int k = __ldg(rowptr + r) + sub;
+            int c[4];
+            double v[4], xv[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const bool ok = k + 4 * q < k1;
+                c[q] = ok ? __ldcs(col + k + 4 * q) : -1;
+                v[q] = ok ? __ldcs(val + k + 4 * q) : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) xv[q] = c[q] >= 0 ? xs[c[q]] : 0.0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (c[q] >= 0) acc = __fma_rn(v[q], xv[q], acc);
+            for (k += 16; k < k1; k += 4) acc = __fma_rn(__ldcs(val + k), xs[__ldcs(col + k)], acc);
+        }
+        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+        if (r < r1 && sub == 0) y[r] = acc;
+    }
+}
+
 // y = A x - z (FAST-mode er_begin: C gb_slope - rhs in one pass)
 __global__ void __launch_bounds__(kSpmvWarps * 32)
     k_spmv_sub(const int* __restrict__ rowptr, const int* __restrict__ col,
@@ -2193,8 +2237,19 @@ void spmv(const Launch& L, const int* rowptr, const int* col, const double* val,
 void spmv_v4(const Launch& L, const int* rowptr, const int* col, const double* val, int n_rows,
              double* y, const Ctrl* ctrl, const double* vbase, long long ldv) {
     if (n_rows <= 0) return;
-    const unsigned int grid = cdiv(n_rows, 64);
-    k_spmv_v4<<<grid, 256, 0, L.stream>>>(rowptr, col, val, n_rows, y, ctrl, vbase, ldv);
+    // large matrices: one contiguous row slice per CTA (L1 reuse of the gathers); EXG_SPMV_STRIPS=0
+    // keeps the plain grid order, =k sets CTAs per SM
+    static const int strips = getenv("EXG_SPMV_STRIPS") ? atoi(getenv("EXG_SPMV_STRIPS")) : 1;
+    if (strips > 0 && n_rows >= 64 * 1024) {
+        const int ctas = L.num_sms * strips;
+        const int per = (int)(((long long)n_rows + ctas - 1) / ctas);
+        const int rows_per_cta = (per + 7) / 8 * 8;
+        k_spmv_v4s<<<cdiv(n_rows, rows_per_cta), kSpmvStripThreads, 0, L.stream>>>(rowptr, col, val, n_rows, rows_per_cta, y,
+                                                                                ctrl, vbase, ldv);
+    } else {
+        const unsigned int grid = cdiv(n_rows, 64);
+        k_spmv_v4<<<grid, 256, 0, L.stream>>>(rowptr, col, val, n_rows, y, ctrl, vbase, ldv);
+    }
     count(L);
 }
 

@@ -8,6 +8,7 @@
 #include <cstdlib>
 #include <atomic>
 #include <numeric>
+#include <queue>
 #include <stdexcept>
 #include <thread>
 
@@ -409,6 +410,11 @@ inline T get(const unsigned char* p) {
 
 }  // namespace
 
+void stream_params_env(StreamParams& p) {
+    if (const char* e = getenv("EXG_STREAM_SCHED")) p.sched = atoi(e);
+    if (const char* e = getenv("EXG_STREAM_HOP")) p.hop = atof(e);
+}
+
 void build_stream_plan(const AugPlan& P, bool upper, const int* out_index, const StreamParams& prm,
                        StreamPlan& S) {
     S = StreamPlan{};
@@ -421,8 +427,23 @@ void build_stream_plan(const AugPlan& P, bool upper, const int* out_index, const
     const int dummy = (int)P.n_aug;
     const size_t np = P.meta.size() / 4;
     S.n_rows = (long long)np;
-    // ---- tasks: within a level rows are independent, so they are taken
-    // longest first and grouped by lane class
+    // ---- row heights: the longest chain of dependent rows below each row
+    // (positions are in level order, so a reverse sweep sees every consumer
+    // before its producers)
+    std::vector<int> pos_of((size_t)P.n_aug, -1);
+    for (size_t p = 0; p < np; ++p) pos_of[P.meta[4 * p]] = (int)p;
+    std::vector<int> height(np, 0);
+    if (prm.sched != 0) {
+        for (size_t p = np; p-- > 0;)
+            for (int k = P.meta[4 * p + 2]; k < P.meta[4 * p + 3]; ++k) {
+                const int pp = pos_of[P.col[k]];
+                if (pp < 0 || (size_t)pp >= p) throw std::runtime_error("stream plan: rows not in dependency order");
+                height[pp] = std::max(height[pp], height[p] + 1);
+            }
+    }
+    // ---- tasks: within a level rows are independent, so they are grouped by
+    // lane class, longest first; the list schedule also keeps rows of like
+    // height together (a task is as urgent as its most urgent row)
     struct Task {
         long long first;  // index into `ord`
         int cnt, lg, nq, level;
@@ -433,36 +454,179 @@ void build_stream_plan(const AugPlan& P, bool upper, const int* out_index, const
     std::vector<Task> tasks;
     for (int l = 0; l < P.levels; ++l) {
         const long long a = P.level_first_pos[l], b = P.level_first_pos[l + 1];
-        std::stable_sort(ord.begin() + a, ord.begin() + b, [&](int x, int y) { return len_of(x) > len_of(y); });
+        if (prm.sched != 0)
+            std::stable_sort(ord.begin() + a, ord.begin() + b, [&](int x, int y) {
+                const int lx = lanes_log2_for(len_of(x)), ly = lanes_log2_for(len_of(y));
+                if (lx != ly) return lx > ly;
+                if (height[x] != height[y]) return height[x] > height[y];
+                return len_of(x) > len_of(y);
+            });
+        else
+            std::stable_sort(ord.begin() + a, ord.begin() + b, [&](int x, int y) { return len_of(x) > len_of(y); });
         long long i = a;
         while (i < b) {
             const int len = len_of(ord[i]);
             if (len > 128) throw std::runtime_error("stream plan: a row exceeds 128 entries (AugParams.cap)");
             const int lg = lanes_log2_for(len);
-            Task t{i, 0, lg, (len + (1 << lg) - 1) >> lg, l};
+            Task t{i, 0, lg, 0, l};
             // rows per task: the lane count, and the record must fit its slot
-            const int per = std::max(1, std::min(32 >> lg, (kStreamSlot - 16 - t.nq * 384) / MS));
-            while (i < b && t.cnt < per && lanes_log2_for(len_of(ord[i])) == lg) {
+            int longest = 0;
+            while (i < b && (t.cnt << lg) < 32 && lanes_log2_for(len_of(ord[i])) == lg) {
+                const int lo = std::max(longest, len_of(ord[i]));
+                const int nq = (lo + (1 << lg) - 1) >> lg;
+                if (t.cnt > 0 && 16 + nq * 384 + (t.cnt + 1) * MS > kStreamSlot) break;
+                longest = lo;
                 ++t.cnt;
                 ++i;
             }
+            t.nq = (longest + (1 << lg) - 1) >> lg;
             tasks.push_back(t);
         }
     }
-    S.n_tasks = (long long)tasks.size();
+    const size_t NT = tasks.size();
+    S.n_tasks = (long long)NT;
     int W = prm.n_warps;
     if (prm.min_tasks_per_warp > 0) {
-        const long long want = ((long long)tasks.size() / prm.min_tasks_per_warp + 7) / 8 * 8;
+        const long long want = ((long long)NT / prm.min_tasks_per_warp + 7) / 8 * 8;
         W = (int)std::max<long long>(8, std::min<long long>(W, want));  // a multiple of 8 (and of any CTA's warps)
         W = std::min(W, prm.n_warps);
     }
     S.n_warps = W;
+    // the task that produces each unknown
+    std::vector<int> prod((size_t)P.n_aug, -1);
+    for (size_t t = 0; t < NT; ++t)
+        for (int seg = 0; seg < tasks[t].cnt; ++seg) prod[P.meta[4 * (size_t)ord[tasks[t].first + seg]]] = (int)t;
+    // ---- the order of execution: rank r runs tasks[by_rank[r]] on warp
+    // warp_of[r]; a warp runs its tasks by ascending rank and every dependency
+    // of a task has a smaller rank, so the unfinished task of smallest rank can
+    // always run (no deadlock whatever the timing).
+    std::vector<int> by_rank(NT), warp_of(NT);
+    std::vector<double> fin(NT, 0.0);  // modelled finish time, in task costs
+    const double hop = prm.hop;
+    auto model_level_order = [&]() {  // level order, round-robin: the modelled makespan
+        std::vector<double> wfree(W, 0.0);
+        double span = 0.0;
+        for (size_t t = 0; t < NT; ++t) {
+            double rdy = 0.0;
+            for (int seg = 0; seg < tasks[t].cnt; ++seg) {
+                const int p = ord[tasks[t].first + seg];
+                for (int k = P.meta[4 * (size_t)p + 2]; k < P.meta[4 * (size_t)p + 3]; ++k)
+                    rdy = std::max(rdy, fin[prod[P.col[k]]] + hop);
+            }
+            double& wf = wfree[t % W];
+            fin[t] = wf = std::max(wf, rdy) + 1.0;
+            span = std::max(span, wf);
+        }
+        return span;
+    };
+    double span_level = 0.0, span_list = 0.0;
+    if (prm.sched == 0) {
+        for (size_t t = 0; t < NT; ++t) {
+            by_rank[t] = (int)t;
+            warp_of[t] = (int)(t % W);
+        }
+        if (getenv("EXG_PLAN_VERBOSE")) span_level = model_level_order();
+    } else {
+        if (getenv("EXG_PLAN_VERBOSE")) span_level = model_level_order();
+        // list schedule (highest level first): simulate W warps with unit task
+        // cost and a hand-off of `hop` costs between a producer's finish and a
+        // consumer's start.  A free warp takes the most urgent task (largest
+        // height) whose dependencies are `hop` old, or else waits for the one
+        // that becomes ready first.
+        std::vector<int> theight(NT, 0), ndep(NT, 0);
+        std::vector<long long> sptr(NT + 1, 0);
+        std::vector<int> deps;  // scratch: a task's distinct producers
+        auto producers = [&](size_t t) {
+            deps.clear();
+            for (int seg = 0; seg < tasks[t].cnt; ++seg) {
+                const int p = ord[tasks[t].first + seg];
+                theight[t] = std::max(theight[t], height[p]);
+                for (int k = P.meta[4 * (size_t)p + 2]; k < P.meta[4 * (size_t)p + 3]; ++k) deps.push_back(prod[P.col[k]]);
+            }
+            std::sort(deps.begin(), deps.end());
+            deps.erase(std::unique(deps.begin(), deps.end()), deps.end());
+        };
+        for (size_t t = 0; t < NT; ++t) {
+            producers(t);
+            ndep[t] = (int)deps.size();
+            for (int d : deps) ++sptr[d + 1];
+        }
+        for (size_t t = 0; t < NT; ++t) sptr[t + 1] += sptr[t];
+        std::vector<int> succ((size_t)sptr[NT]);
+        {
+            std::vector<long long> at(sptr.begin(), sptr.end() - 1);
+            for (size_t t = 0; t < NT; ++t) {
+                producers(t);
+                for (int d : deps) succ[(size_t)at[d]++] = (int)t;
+            }
+        }
+        using TE = std::pair<double, int>;   // {ready time, task}: earliest first
+        using AE = std::pair<long long, int>;  // {urgency, -task}: most urgent first
+        std::priority_queue<TE, std::vector<TE>, std::greater<TE>> pending, warps;
+        std::priority_queue<AE> avail;
+        std::vector<double> rdy(NT, 0.0), start(NT, 0.0);
+        for (size_t t = 0; t < NT; ++t)
+            if (ndep[t] == 0) pending.push({0.0, (int)t});
+        for (int w = 0; w < W; ++w) warps.push({0.0, w});
+        auto urgency = [&](int t) { return ((long long)theight[t] << 20) - tasks[t].level; };
+        size_t done = 0;
+        std::vector<int> w_of_task(NT, 0);
+        while (done < NT) {
+            auto [tau, w] = warps.top();
+            warps.pop();
+            while (!pending.empty() && pending.top().first <= tau) {
+                const int t = pending.top().second;
+                pending.pop();
+                avail.push({urgency(t), -t});
+            }
+            int t;
+            double st = tau;
+            if (!avail.empty()) {
+                t = -avail.top().second;
+                avail.pop();
+            } else {
+                if (pending.empty()) throw std::runtime_error("stream plan: dependency cycle");
+                t = pending.top().second;
+                st = pending.top().first;
+                pending.pop();
+            }
+            start[t] = st;
+            fin[t] = st + 1.0;
+            w_of_task[t] = w;
+            warps.push({fin[t], w});
+            span_list = std::max(span_list, fin[t]);
+            ++done;
+            for (long long e = sptr[t]; e < sptr[t + 1]; ++e) {
+                const int s = succ[(size_t)e];
+                rdy[s] = std::max(rdy[s], fin[t] + hop);
+                if (--ndep[s] == 0) pending.push({rdy[s], s});
+            }
+        }
+        std::iota(by_rank.begin(), by_rank.end(), 0);
+        std::stable_sort(by_rank.begin(), by_rank.end(), [&](int x, int y) { return start[x] < start[y]; });
+        for (size_t r = 0; r < NT; ++r) warp_of[r] = w_of_task[by_rank[r]];
+    }
+    S.task_warp = warp_of;
+    std::vector<int> rank_of(NT);
+    for (size_t r = 0; r < NT; ++r) rank_of[by_rank[r]] = (int)r;
+    // per-warp sequences
+    std::vector<long long> wptr(W + 1, 0);
+    for (size_t r = 0; r < NT; ++r) ++wptr[warp_of[r] + 1];
+    for (int w = 0; w < W; ++w) wptr[w + 1] += wptr[w];
+    std::vector<int> wseq(NT), wpos(NT);
+    {
+        std::vector<long long> at(wptr.begin(), wptr.end() - 1);
+        for (size_t r = 0; r < NT; ++r) {
+            wpos[r] = (int)(at[warp_of[r]] - wptr[warp_of[r]]);
+            wseq[(size_t)at[warp_of[r]]++] = (int)r;
+        }
+    }
     // ---- stream sizes
     auto rec_bytes = [&](const Task& t) { return (16 + t.nq * 384 + t.cnt * MS + 15) / 16 * 16; };
     std::vector<long long> bytes(W, 0);
-    for (size_t t = 0; t < tasks.size(); ++t) {
-        const int rb = rec_bytes(tasks[t]);
-        bytes[t % W] += rb;
+    for (size_t r = 0; r < NT; ++r) {
+        const int rb = rec_bytes(tasks[by_rank[r]]);
+        bytes[warp_of[r]] += rb;
         S.max_record = std::max(S.max_record, rb);
     }
     if (S.max_record > kStreamSlot) throw std::runtime_error("stream plan: record larger than its slot");
@@ -474,38 +638,36 @@ void build_stream_plan(const AugPlan& P, bool upper, const int* out_index, const
     for (int w = 0; w < W; ++w) {
         S.desc[8 * (size_t)w] = (int)(off[w] & 0xFFFFFFFFll);
         S.desc[8 * (size_t)w + 1] = (int)(off[w] >> 32);
-        const long long nt = ((long long)tasks.size() - w + W - 1) / W;
-        S.desc[8 * (size_t)w + 2] = (int)std::max<long long>(0, nt);
-        for (int k = 0; k < kStreamRing - 1; ++k) {
-            const size_t t = (size_t)w + (size_t)k * W;
-            S.desc[8 * (size_t)w + 3 + k] = t < tasks.size() ? rec_bytes(tasks[t]) : 0;
-        }
+        const long long nt = wptr[w + 1] - wptr[w];
+        S.desc[8 * (size_t)w + 2] = (int)nt;
+        for (int k = 0; k < kStreamRing - 1; ++k)
+            S.desc[8 * (size_t)w + 3 + k] = k < nt ? rec_bytes(tasks[by_rank[wseq[(size_t)wptr[w] + k]]]) : 0;
     }
-    // the task that produces each unknown: a task's flag is its dependency
-    // with the latest producer
-    std::vector<int> prod((size_t)P.n_aug, -1);
-    for (size_t t = 0; t < tasks.size(); ++t)
-        for (int seg = 0; seg < tasks[t].cnt; ++seg) prod[P.meta[4 * (size_t)ord[tasks[t].first + seg]]] = (int)t;
     std::vector<long long> cur(off.begin(), off.end() - 1);
-    for (size_t t = 0; t < tasks.size(); ++t) {
-        const Task& T = tasks[t];
+    for (size_t r = 0; r < NT; ++r) {
+        const Task& T = tasks[by_rank[r]];
+        const int w = warp_of[r];
         const int rb = rec_bytes(T);
-        size_t at = (size_t)cur[t % W];
-        cur[t % W] += rb;
-        int flag = dummy, flag_task = -1;
+        size_t at = (size_t)cur[w];
+        cur[w] += rb;
+        // the flag: the dependency whose producer runs last (largest rank)
+        int flag = dummy, flag_rank = -1;
         for (int seg = 0; seg < T.cnt; ++seg) {
             const int p = ord[T.first + seg];
-            for (int k = P.meta[4 * (size_t)p + 2]; k < P.meta[4 * (size_t)p + 3]; ++k)
-                if (prod[P.col[k]] > flag_task) {
-                    flag_task = prod[P.col[k]];
+            for (int k = P.meta[4 * (size_t)p + 2]; k < P.meta[4 * (size_t)p + 3]; ++k) {
+                const int pr = rank_of[prod[P.col[k]]];
+                if (pr >= (int)r) throw std::runtime_error("stream plan: a dependency is not ranked earlier");
+                if (pr > flag_rank) {
+                    flag_rank = pr;
                     flag = P.col[k];
                 }
+            }
         }
-        const size_t ahead = t + (size_t)(kStreamRing - 1) * W;
+        const long long ahead = wptr[w] + wpos[r] + (kStreamRing - 1);
         put<int>(S.data, at, T.cnt | (T.lg << 8) | (T.nq << 12) | (T.level << 16));
-        put<int>(S.data, at + 4, ahead < tasks.size() ? rec_bytes(tasks[ahead]) : 0);
+        put<int>(S.data, at + 4, ahead < wptr[w + 1] ? rec_bytes(tasks[by_rank[wseq[(size_t)ahead]]]) : 0);
         put<int>(S.data, at + 8, flag);
-        put<int>(S.data, at + 12, (int)t);
+        put<int>(S.data, at + 12, (int)r);
         const size_t col_at = at + 16, val_at = col_at + (size_t)T.nq * 128, meta_at = val_at + (size_t)T.nq * 256;
         for (int q = 0; q < T.nq * 32; ++q) put<int>(S.data, col_at + 4 * (size_t)q, dummy);
         const int lpr = 1 << T.lg;
@@ -539,6 +701,9 @@ void build_stream_plan(const AugPlan& P, bool upper, const int* out_index, const
         }
     }
     if (getenv("EXG_PLAN_VERBOSE"))
+        fprintf(stderr, "stream plan %s: schedule %s, warps %d, modelled span (task costs, hop %.2f): level order %.1f, list %.1f; tasks/warp %.1f\n",
+                upper ? "U" : "L", prm.sched ? "list" : "level order", W, hop, span_level, span_list, (double)NT / W);
+    if (getenv("EXG_PLAN_VERBOSE"))
         fprintf(stderr, "stream plan %s: tasks %lld entries %lld gather sectors %lld (%.2f per entry) bytes %zu levels %d\n",
                 upper ? "U" : "L", S.n_tasks, S.n_entries, S.n_gather_sectors,
                 (double)S.n_gather_sectors / (double)std::max<long long>(1, S.n_entries), S.data.size(), S.levels);
@@ -554,7 +719,8 @@ void eval_stream_plan(const StreamPlan& S, bool upper, const double* in, double*
     }
     out[S.n_aug] = 0.0;  // the dummy
     for (long long t = 0; t < S.n_tasks; ++t) {
-        const int w = (int)(t % W);
+        const int w = S.task_warp[(size_t)t];
+        if (w < 0 || w >= W) throw std::runtime_error("stream plan: bad warp of a task");
         if (left[w]-- <= 0) throw std::runtime_error("stream plan: task count mismatch");
         const unsigned char* r = S.data.data() + cur[w];
         const int w0 = get<int>(r);

@@ -104,6 +104,12 @@ constexpr int kStreamSlot = 2048;  // bytes per slot
 struct StreamParams {
     int n_warps = 0;              // co-resident warps of the launch (upper bound)
     int min_tasks_per_warp = 4;   // small systems use fewer warps (a multiple of 8)
+    // order of execution: 0 = level by level, task t on warp t mod W;
+    // 1 = list schedule (most urgent ready task first on the warp that frees
+    // first), simulated with unit task cost and a producer-to-consumer
+    // hand-off of `hop` task costs
+    int sched = 1;
+    double hop = 3.0;
 };
 
 struct StreamPlan {
@@ -116,7 +122,11 @@ struct StreamPlan {
     int max_record = 0;
     std::vector<int> desc;        // 8 ints per warp
     std::vector<unsigned char> data;
+    std::vector<int> task_warp;   // warp of the task of each rank (host only: eval_stream_plan)
 };
+
+// debug overrides: EXG_STREAM_SCHED=0|1, EXG_STREAM_HOP=<task costs>
+void stream_params_env(StreamParams& p);
 
 constexpr int kStreamMetaL = 8, kStreamMetaU = 24;
 

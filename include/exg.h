@@ -209,6 +209,10 @@ exg_status exg_debug_trace_solve(exg_ctx* ctx, const double* b, unsigned long lo
  * reorthogonalised}.  The kernel is the one the context's mode runs. */
 exg_status exg_debug_orthogonalize(exg_ctx* ctx, int n, int j, const double* V, const double* w,
                                    double breakdown_tol, double* hcol, double* v_next, int* info);
+/* debug / test: y = C x on host vectors through the FAST-mode SpMV kernel of
+ * the Arnoldi loop (sparse_matrix.cpp:69-82 up to the order of the additions:
+ * four lanes per row); C must be square. */
+exg_status exg_debug_spmv_fast(exg_ctx* ctx, const double* x, double* y);
 /* debug / test: dense_expm (dense_matrix.cpp:185-225) of a host m x m row-major
  * matrix through the dense-block kernel, bit-identical to the reference. */
 exg_status exg_debug_dense_expm(exg_ctx* ctx, int m, const double* A, double* E);

@@ -175,6 +175,7 @@ _DEV_PROTOS = {
     "exg_profile_enable": (I, [P, I]),
     "exg_debug_trace_solve": (I, [P, PD, C.POINTER(C.c_uint64)]),
     "exg_debug_dense_expm": (I, [P, I, PD, PD]),
+    "exg_debug_spmv_fast": (I, [P, PD, PD]),
     "exg_debug_orthogonalize": (I, [P, I, I, PD, PD, D, PD, PD, PI]),
     "exg_debug_trace_stream": (I, [P, PD, C.POINTER(C.c_uint64), C.POINTER(C.c_longlong)]),
     "exg_profile_get": (I, [P, C.POINTER(exg_kernel_times)]),

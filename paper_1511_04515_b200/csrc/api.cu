@@ -89,8 +89,14 @@ void upload_csr(exg_ctx* c, DCsr& m, int n_rows, int n_cols, int nnz, const int*
     m.n_cols = n_cols;
     m.nnz = nnz;
     m.rowptr = dalloc<int>(n_rows + 1);
-    m.col = dalloc<int>(nnz);
-    m.val = dalloc<double>(nnz);
+    // 8 zero entries past the end: k_spmv_v4t copies 16-byte aligned ranges
+    m.col = dalloc<int>((size_t)nnz + 8);
+    m.val = dalloc<double>((size_t)nnz + 8);
+    ck(cudaMemsetAsync(m.col + nnz, 0, 8 * sizeof(int), c->stream), "upload");
+    ck(cudaMemsetAsync(m.val + nnz, 0, 8 * sizeof(double), c->stream), "upload");
+    m.max_strip = 0;
+    const int sr = exg::dev::spmv_strip_rows();
+    for (int r = 0; r < n_rows; ++r) m.max_strip = std::max(m.max_strip, rowptr[std::min(r + sr, n_rows)] - rowptr[r]);
     ck(cudaMemcpyAsync(m.rowptr, rowptr, sizeof(int) * (n_rows + 1), cudaMemcpyHostToDevice, c->stream), "upload");
     if (nnz) {
         ck(cudaMemcpyAsync(m.col, col, sizeof(int) * nnz, cudaMemcpyHostToDevice, c->stream), "upload");
@@ -234,6 +240,10 @@ void solve_dev(exg_ctx* c, const double* b, double* final_out, double coef, cons
                 sa.trace = a.trace;
                 static const int nodeps = getenv("EXG_STREAM_NODEPS") ? atoi(getenv("EXG_STREAM_NODEPS")) : 0;
                 sa.nodeps = nodeps;
+                static const int poll_ns = getenv("EXG_STREAM_POLL_NS") ? atoi(getenv("EXG_STREAM_POLL_NS")) : 0;
+                static const int poll_cap = getenv("EXG_STREAM_POLL_CAP") ? atoi(getenv("EXG_STREAM_POLL_CAP")) : 0;
+                sa.poll_ns = poll_ns;
+                sa.poll_cap = poll_cap;
                 ck(exg::dev::trsv_stream(c->L(), upper, sa), "stream solve launch");
                 c->prof_end(upper ? EXG_K_TRSV_U : EXG_K_TRSV_L, e0);
                 continue;
@@ -432,7 +442,7 @@ void mevp_dev(exg_ctx* c, const double* v, double h, const exg_mevp_cfg& cfg, in
         // w = -G^{-1}(C v_j)   (krylov.cpp:120-121)
         cudaEvent_t p0 = c->prof_begin();
         if (c->opt.trsv_mode == EXG_TRSV_FAST)
-            exg::dev::spmv_v4(L, C.rowptr, C.col, C.val, C.n_rows, c->t, c->ctrl, c->V, c->ldv);
+            exg::dev::spmv_v4(L, C.rowptr, C.col, C.val, C.n_rows, C.max_strip, c->t, c->ctrl, c->V, c->ldv);
         else
             exg::dev::spmv(L, C.rowptr, C.col, C.val, C.n_rows, nullptr, c->t, c->ctrl, c->V, c->ldv);
         c->prof_end(EXG_K_SPMV, p0);
@@ -1415,6 +1425,10 @@ exg_status exg_set_factors(exg_ctx* c, int n, const int* Lp, const int* Li, cons
             exg::StreamParams sp;
             sp.n_warps = exg::dev::trsv_stream_warps(tri == 1, c->num_sms);
             exg::stream_params_env(sp);
+            if (const char* e = getenv("EXG_STREAM_WARPS")) {  // debug: fewer co-resident warps (a multiple of 8)
+                const int wcap = atoi(e) / 8 * 8;
+                if (wcap >= 8 && wcap < sp.n_warps) sp.n_warps = wcap;
+            }
             if (sp.n_warps <= 0) throw ApiError{EXG_E_CUDA, "k_trsv4 cannot be launched on this device"};
             exg::StreamPlan S;
             {
@@ -1997,6 +2011,34 @@ exg_status exg_debug_orthogonalize(exg_ctx* c, int n, int j, const double* V, co
     cudaFree(dV);
     cudaFree(dw);
     cudaFree(dh);
+    cudaFree(dc);
+    API_END(c)
+}
+
+// debug / test: y = C x through the FAST-mode SpMV of the Arnoldi loop
+// (k_spmv_v4 / k_spmv_v4w: four lanes per row, sparse_matrix.cpp:69-82 up to
+// the order of the additions), on host vectors
+exg_status exg_debug_spmv_fast(exg_ctx* c, const double* x, double* y) {
+    API_BEGIN
+    const DCsr& Cm = mat(c, EXG_MAT_C);
+    if (!x || !y || Cm.n_rows != Cm.n_cols) throw ApiError{EXG_E_CONTRACT, "exg_debug_spmv_fast: bad arguments"};
+    const int n = Cm.n_rows;
+    const long long ldv = ((long long)n + 31) / 32 * 32;
+    double* dx = dalloc<double>((size_t)2 * ldv);  // column 1 is read (j = 1): a non-zero column offset
+    double* dy = dalloc<double>(n);
+    Ctrl* dc = reinterpret_cast<Ctrl*>(dalloc<char>(sizeof(Ctrl)));
+    Ctrl hc;
+    std::memset(&hc, 0, sizeof hc);
+    hc.j = 1;
+    ck(cudaMemsetAsync(dx, 0, (size_t)2 * ldv * sizeof(double), c->stream), "memset");
+    ck(cudaMemcpyAsync(dx + ldv, x, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream), "h2d");
+    ck(cudaMemcpyAsync(dc, &hc, sizeof hc, cudaMemcpyHostToDevice, c->stream), "h2d");
+    exg::dev::spmv_v4(c->L(), Cm.rowptr, Cm.col, Cm.val, n, Cm.max_strip, dy, dc, dx, ldv);
+    ck(cudaGetLastError(), "spmv launch");
+    ck(cudaMemcpyAsync(y, dy, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream), "d2h");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    cudaFree(dx);
+    cudaFree(dy);
     cudaFree(dc);
     API_END(c)
 }

@@ -11,6 +11,7 @@
 
 struct DCsr {
     int n_rows = 0, n_cols = 0, nnz = 0;
+    int max_strip = 0;  // most entries in any spmv_strip_rows() consecutive rows (k_spmv_v4t stage fit)
     int* rowptr = nullptr;
     int* col = nullptr;
     double* val = nullptr;

@@ -46,6 +46,8 @@ struct StreamArgs {
     const Ctrl* ctrl;
     unsigned long long* trace;   // debug: 5 values per task, or null
     int nodeps;                  // debug (EXG_STREAM_NODEPS): ignore readiness, wrong results: throughput bound only
+    int poll_ns;                 // back-off of a waiting task between polls: first sleep (ns), doubling up to poll_cap
+    int poll_cap;
 };
 
 struct SubArgs {
@@ -151,7 +153,10 @@ struct Launch {
 
 void spmv(const Launch& L, const int* rowptr, const int* col, const double* val, int n_rows,
           const double* x, double* y, const Ctrl* ctrl, const double* vbase, long long ldv);
-void spmv_v4(const Launch& L, const int* rowptr, const int* col, const double* val, int n_rows,
+// FAST-mode SpMV of the Arnoldi loop.  max_strip: the most entries any spmv_strip_rows() consecutive
+// rows hold (0: unknown, direct loads); col/val must be readable 8 entries past nnz (upload_csr pads).
+int spmv_strip_rows();
+void spmv_v4(const Launch& L, const int* rowptr, const int* col, const double* val, int n_rows, int max_strip,
              double* y, const Ctrl* ctrl, const double* vbase, long long ldv);
 void spmv_sub(const Launch& L, const int* rowptr, const int* col, const double* val, int n_rows,
               const double* x, const double* z, double* y);

@@ -131,47 +131,143 @@ __global__ void __launch_bounds__(256)
     if (r < n_rows && sub == 0) y[r] = acc;
 }
 
-// The same rows, lanes and arithmetic as k_spmv_v4, with the rows laid out for
-// the L1: CTA b owns ONE contiguous slice of rows and walks it strip by strip,
-// so the x values a strip gathers (a window of a few grid rows either side:
-// the reach of the coupling capacitors) were mostly fetched by the strips
-// just before it and are still in this SM's L1.  k_spmv_v4's grid order puts
-// co-resident CTAs ~10k rows apart: every gather sector then comes from L2
-// (3.5x the DRAM bytes of the launch, ncu profiles/r02), which is what bounds it.
-constexpr int kSpmvStripThreads = 1024;
-__global__ void __launch_bounds__(kSpmvStripThreads, 1)
-    k_spmv_v4s(const int* __restrict__ rowptr, const int* __restrict__ col,
+// The same rows, lanes and arithmetic as k_spmv_v4, with col/val streamed
+// through shared memory.  k_spmv_v4 chains three dependent global loads per
+// row (rowptr -> col/val -> x) with nothing of the next rows in flight behind
+// them: ~80 KB per SM per ~2.5 us of chained latency, 3 TB/s at config 1
+// whatever the gathers cost (laying rows out for L1 reuse and serving the
+// gathers from a shared-memory window of x both left the 56 us launch where it
+// was, profiles/r02).  Here CTA b owns ONE contiguous slice of rows, cut into
+// strips of 248 rows; a producer warp pulls each strip's col and val ranges
+// (contiguous in CSR) into a ring of kSpmvStages shared-memory stages with bulk
+// async copies (cp.async.bulk + mbarrier complete_tx), up to four strips
+// (~190 KB per SM) ahead of the 31 consumer warps, which read col/val from shared
+// memory and only gather x from global memory.  The HBM stream no longer waits
+// for the gathers.  max_strip (host, at upload): the most entries any 248
+// consecutive rows hold; the launcher keeps k_spmv_v4 when a strip would not fit.
+constexpr int kSpmvStages = 4;
+constexpr int kSpmvStageCap = 4096;  // entries per stage (16 KB of col + 32 KB of val)
+constexpr int kSpmvConsumers = 31;   // warps; 8 rows each per strip
+constexpr int kSpmvStripRows = kSpmvConsumers * 8;
+constexpr int kSpmvMaxStrips = 256;
+constexpr size_t kSpmvStreamSmem = (size_t)kSpmvStages * kSpmvStageCap * 12;
+__global__ void __launch_bounds__((kSpmvConsumers + 1) * 32, 1)
+    k_spmv_v4t(const int* __restrict__ rowptr, const int* __restrict__ col,
                const double* __restrict__ val, int n_rows, int rows_per_cta, double* __restrict__ y,
                const Ctrl* ctrl, const double* __restrict__ xcol_base, long long ldv) {
+    extern __shared__ __align__(128) unsigned char ring[];
+    __shared__ __align__(8) unsigned long long bars[2 * kSpmvStages];  // full[], empty[]
+    __shared__ int kb[kSpmvMaxStrips + 1];                             // first entry of each strip (and the end)
     if (ctrl->converged || ctrl->status) return;
     const double* xs = xcol_base + (long long)ctrl->j * ldv;
-    const int sub = threadIdx.x & 3;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int r0 = blockIdx.x * rows_per_cta;
     const int r1 = min(n_rows, r0 + rows_per_cta);
-    for (int rb = r0; rb < r1; rb += kSpmvStripThreads / 4) {  // whole warps stay in the loop (shuffles)
-        const int r = rb + (threadIdx.x >> 2);
-        double acc = 0.0;
-        if (r < r1) {
-            const int k1 = __ldg(rowptr + r + 1);
-            int k = __ldg(rowptr + r) + sub;
-            int c[4];
-            double v[4], xv[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const bool ok = k + 4 * q < k1;
-                c[q] = ok ? __ldcs(col + k + 4 * q) : -1;
-                v[q] = ok ? __ldcs(val + k + 4 * q) : 0.0;
-            }
-#pragma unroll
-            for (int q = 0; q < 4; ++q) xv[q] = c[q] >= 0 ? xs[c[q]] : 0.0;
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-                if (c[q] >= 0) acc = __fma_rn(v[q], xv[q], acc);
-            for (k += 16; k < k1; k += 4) acc = __fma_rn(__ldcs(val + k), xs[__ldcs(col + k)], acc);
+    const int n_strips = (r1 - r0 + kSpmvStripRows - 1) / kSpmvStripRows;
+    const unsigned bar0 = (unsigned)__cvta_generic_to_shared(bars);
+    const unsigned ring0 = (unsigned)__cvta_generic_to_shared(ring);
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < kSpmvStages; ++q) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8 * q));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar0 + 8 * (kSpmvStages + q)), "r"(kSpmvConsumers));
         }
-        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-        if (r < r1 && sub == 0) y[r] = acc;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (int q = threadIdx.x; q <= n_strips; q += blockDim.x) kb[q] = __ldg(rowptr + min(r0 + q * kSpmvStripRows, r1));
+    __syncthreads();
+    auto wait = [&](unsigned bar, unsigned parity) {
+        unsigned ok = 0;
+        while (!ok)
+            asm volatile(
+                "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                : "=r"(ok)
+                : "r"(bar), "r"(parity)
+                : "memory");
+    };
+    if (warp == kSpmvConsumers) {
+        // producer: strip s goes to stage s mod kSpmvStages once strip s - kSpmvStages left it
+        if (lane == 0)
+            for (int s = 0; s < n_strips; ++s) {
+                const int st = s % kSpmvStages;
+                if (s >= kSpmvStages) wait(bar0 + 8 * (kSpmvStages + st), (unsigned)(s / kSpmvStages - 1) & 1u);
+                const int k0 = kb[s] & ~3, k1 = (kb[s + 1] + 3) & ~3;  // 16-byte aligned ranges (the arrays are padded)
+                const unsigned cnt = (unsigned)(k1 - k0), full = bar0 + 8 * st;
+                if (cnt == 0) {
+                    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(full) : "memory");
+                    continue;
+                }
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full), "r"(cnt * 12u) : "memory");
+                const unsigned dst = ring0 + (unsigned)st * (kSpmvStageCap * 12);
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                    "l"(col + k0), "r"(cnt * 4u), "r"(full)
+                    : "memory");
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        dst + kSpmvStageCap * 4),
+                    "l"(val + k0), "r"(cnt * 8u), "r"(full)
+                    : "memory");
+            }
+        return;
+    }
+    // two strips per round: the gathers of 2 x kSpmvBatch entries per lane are in flight together (the
+    // gathers' latency, not their count, is what a round costs)
+    constexpr int kSpmvBatch = 6;
+    const int sub = lane & 3;
+    const int rq = r0 + warp * 8 + (lane >> 2);
+    for (int s = 0; s < n_strips; s += 2) {
+        int o[2], o1[2], rr[2];
+        const int* cs[2];
+        const double* vs[2];
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+            rr[t] = rq + (s + t) * kSpmvStripRows;
+            o[t] = o1[t] = 0;
+            if (rr[t] < r1) {
+                o1[t] = __ldg(rowptr + rr[t] + 1);
+                o[t] = __ldg(rowptr + rr[t]) + sub;
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+            const int st = (s + t) % kSpmvStages;
+            if (s + t < n_strips) {
+                wait(bar0 + 8 * st, (unsigned)((s + t) / kSpmvStages) & 1u);
+                const int base = kb[s + t] & ~3;  // the row's entries inside the stage
+                o[t] -= base;
+                o1[t] -= base;
+            }
+            cs[t] = reinterpret_cast<const int*>(ring + (size_t)st * (kSpmvStageCap * 12));
+            vs[t] = reinterpret_cast<const double*>(ring + (size_t)st * (kSpmvStageCap * 12) + kSpmvStageCap * 4);
+        }
+        int c[2][kSpmvBatch];
+        double xv[2][kSpmvBatch];
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+#pragma unroll
+            for (int q = 0; q < kSpmvBatch; ++q) c[t][q] = o[t] + 4 * q < o1[t] ? cs[t][o[t] + 4 * q] : -1;
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+#pragma unroll
+            for (int q = 0; q < kSpmvBatch; ++q) xv[t][q] = c[t][q] >= 0 ? xs[c[t][q]] : 0.0;
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+            double acc = 0.0;
+#pragma unroll
+            for (int q = 0; q < kSpmvBatch; ++q)
+                if (c[t][q] >= 0) acc = __fma_rn(vs[t][o[t] + 4 * q], xv[t][q], acc);
+            for (int kk = o[t] + 4 * kSpmvBatch; kk < o1[t]; kk += 4) acc = __fma_rn(vs[t][kk], xs[cs[t][kk]], acc);
+            acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+            acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+            if (rr[t] < r1 && sub == 0) y[rr[t]] = acc;
+        }
+        __syncwarp();
+        if (lane == 0) {
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar0 + 8 * (kSpmvStages + s % kSpmvStages)) : "memory");
+            if (s + 1 < n_strips)
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar0 + 8 * (kSpmvStages + (s + 1) % kSpmvStages))
+                             : "memory");
+        }
     }
 }
 
@@ -2234,18 +2330,24 @@ void spmv(const Launch& L, const int* rowptr, const int* col, const double* val,
     count(L);
 }
 
-void spmv_v4(const Launch& L, const int* rowptr, const int* col, const double* val, int n_rows,
+int spmv_strip_rows() { return kSpmvStripRows; }
+
+void spmv_v4(const Launch& L, const int* rowptr, const int* col, const double* val, int n_rows, int max_strip,
              double* y, const Ctrl* ctrl, const double* vbase, long long ldv) {
     if (n_rows <= 0) return;
-    // large matrices: one contiguous row slice per CTA (L1 reuse of the gathers); EXG_SPMV_STRIPS=0
-    // keeps the plain grid order, =k sets CTAs per SM
-    static const int strips = getenv("EXG_SPMV_STRIPS") ? atoi(getenv("EXG_SPMV_STRIPS")) : 1;
-    if (strips > 0 && n_rows >= 64 * 1024) {
-        const int ctas = L.num_sms * strips;
-        const int per = (int)(((long long)n_rows + ctas - 1) / ctas);
-        const int rows_per_cta = (per + 7) / 8 * 8;
-        k_spmv_v4s<<<cdiv(n_rows, rows_per_cta), kSpmvStripThreads, 0, L.stream>>>(rowptr, col, val, n_rows, rows_per_cta, y,
-                                                                                ctrl, vbase, ldv);
+    // large matrices whose strips fit a stage: col/val through a shared-memory ring (EXG_SPMV_STREAM=0
+    // keeps the direct loads)
+    static const int stream = getenv("EXG_SPMV_STREAM") ? atoi(getenv("EXG_SPMV_STREAM")) : 1;
+    const int per = (int)(((long long)n_rows + L.num_sms - 1) / L.num_sms);
+    if (stream > 0 && n_rows >= 64 * 1024 && max_strip > 0 && max_strip + 8 <= kSpmvStageCap &&
+        per <= kSpmvMaxStrips * kSpmvStripRows) {
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_spmv_v4t, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSpmvStreamSmem);
+            attr = true;
+        }
+        k_spmv_v4t<<<cdiv(n_rows, per), (kSpmvConsumers + 1) * 32, kSpmvStreamSmem, L.stream>>>(rowptr, col, val, n_rows, per,
+                                                                                            y, ctrl, vbase, ldv);
     } else {
         const unsigned int grid = cdiv(n_rows, 64);
         k_spmv_v4<<<grid, 256, 0, L.stream>>>(rowptr, col, val, n_rows, y, ctrl, vbase, ldv);

@@ -175,9 +175,15 @@ __global__ void __launch_bounds__(kWarps * 32, kMinB)
                 // and issuing the first re-read before the next task's load, both
                 // measured slower: profiles/r02)
                 const double* fp = out + lds_i(cur.base + 8);
-                do {
+                unsigned ns = (unsigned)a.poll_ns;
+                for (;;) {
                     cur.fy = ld_val(fp);
-                } while (is_sentinel(cur.fy));
+                    if (!is_sentinel(cur.fy)) break;
+                    if (ns) {
+                        __nanosleep(ns);
+                        ns = min(2u * ns, (unsigned)a.poll_cap);
+                    }
+                }
             }
             // then whatever else was not there when it was gathered
             while (__any_sync(FULL, is_sentinel(cur.y[0]) | is_sentinel(cur.y[1]) | is_sentinel(cur.y[2]) |

@@ -326,6 +326,29 @@ def test_dense_expm_rejects_non_finite():
             c._check(F.lib.exg_debug_dense_expm(c.handle, 3, F.as_ptr(a, C.c_double), F.as_ptr(e, C.c_double)))
 
 
+# ---- the FAST-mode SpMV in isolation: k_spmv_v4 (small) and k_spmv_v4t (col/val through a shared-memory ring) ----
+@pytest.mark.parametrize("cfg,kw", [(1, dict(width=64)), (1, dict(width=300)), (1, dict(width=420)),
+                                    (2, dict(width=200)), (3, dict(n=3000))],
+                         ids=["c1-4k", "c1-90k", "c1-176k", "c2-250k", "c3-3k"])
+def test_fast_spmv_matches_reference(ref, cfg, kw):
+    """sparse_matrix.cpp:69-82 with the row's products summed by four lanes: <= a few ulp of sum |c_ik x_k|.
+    Systems above 64k rows take k_spmv_v4t (col/val through the shared-memory ring)."""
+    s = ex.System.generate(cfg, **kw)
+    x = np.random.default_rng(cfg).uniform(-1, 1, s.n)
+    with Context(0, trsv_mode=F.EXG_TRSV_FAST) as c:
+        c.set_system(s)
+        y = np.zeros(s.n)
+        c._check(F.lib.exg_debug_spmv_fast(c.handle, F.as_ptr(x, C.c_double), F.as_ptr(y, C.c_double)))
+        y2 = np.zeros(s.n)
+        c._check(F.lib.exg_debug_spmv_fast(c.handle, F.as_ptr(x, C.c_double), F.as_ptr(y2, C.c_double)))
+    want = np.asarray(ref.spmv(s.C, x))
+    rp = np.asarray(s.C.rowptr)
+    rows = np.repeat(np.arange(s.n), np.diff(rp))
+    mag = np.bincount(rows, np.abs(np.asarray(s.C.val) * x[np.asarray(s.C.col)]), minlength=s.n)
+    assert np.all(np.abs(y - want) <= 8 * np.finfo(float).eps * mag)
+    assert bit_equal(y, y2)
+
+
 # ---- orthogonalize in isolation (SURVEY §8 a8): k_mgs / k_mgs2 against krylov.cpp:46-78 --------
 def _orthogonalize_ref(V, w, tol):
     """The reference's modified Gram-Schmidt with one conditional re-orthogonalisation."""

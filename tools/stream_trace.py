@@ -72,5 +72,8 @@ for name, arr, warps, nbytes in (("L", t[:5 * nl], cnt[2], cnt[4]), ("U", t[5 * 
         if st > 2.0 or r[0] < 3 or r[0] >= nlev - 3:
             print(f"   {r[0]:5d} {r[1]:7d} {r[2]:10.1f} {r[3]:10.1f} {st:8.1f} {r[4]:8.0f} {r[5]:8.0f}")
     res[name] = {"span_us": span, "levels": rows, "front_step_us": step.tolist()}
+    if out_path:  # raw per-task stamps (ns from the first begin) for offline analysis
+        np.savez_compressed(str(out_path) + f".{name}.npz", level=lev.astype(np.int32), begin=(tb - t0).astype(np.int32),
+                            ready=(tr - t0).astype(np.int32), end=(te - t0).astype(np.int32), warp=wp.astype(np.int32))
 if out_path:
     json.dump(res, open(out_path, "w"))

@@ -413,6 +413,7 @@ inline T get(const unsigned char* p) {
 void stream_params_env(StreamParams& p) {
     if (const char* e = getenv("EXG_STREAM_SCHED")) p.sched = atoi(e);
     if (const char* e = getenv("EXG_STREAM_HOP")) p.hop = atof(e);
+    if (const char* e = getenv("EXG_STREAM_BUNDLE")) p.bundle = atoi(e);
 }
 
 void build_stream_plan(const AugPlan& P, bool upper, const int* out_index, const StreamParams& prm,
@@ -447,17 +448,33 @@ void build_stream_plan(const AugPlan& P, bool upper, const int* out_index, const
     struct Task {
         long long first;  // index into `ord`
         int cnt, lg, nq, level;
+        int cont;         // 1: same column list as the task before it (same warp, right behind it)
     };
     std::vector<int> ord(np);
     std::iota(ord.begin(), ord.end(), 0);
     auto len_of = [&](int p) { return P.meta[4 * (size_t)p + 3] - P.meta[4 * (size_t)p + 2]; };
     std::vector<Task> tasks;
+    // rows of 65..128 entries are tasks of their own; many repeat the column
+    // list of another row of their level (the rows of a block inverse over one
+    // 128-column chunk, the rows of a supernode over its ancestors): up to
+    // `bundle` of them run back to back on one warp, the first gathers the
+    // dependencies, the others (cont) reuse its registers
+    const int bundle = prm.sched != 0 ? std::max(1, prm.bundle) : 1;
+    auto cmp_cols = [&](int x, int y) {
+        const int lx = len_of(x), ly = len_of(y);
+        if (lx != ly) return lx > ly ? -1 : 1;  // longest first
+        return std::memcmp(&P.col[P.meta[4 * (size_t)x + 2]], &P.col[P.meta[4 * (size_t)y + 2]], sizeof(int) * lx);
+    };
     for (int l = 0; l < P.levels; ++l) {
         const long long a = P.level_first_pos[l], b = P.level_first_pos[l + 1];
         if (prm.sched != 0)
             std::stable_sort(ord.begin() + a, ord.begin() + b, [&](int x, int y) {
                 const int lx = lanes_log2_for(len_of(x)), ly = lanes_log2_for(len_of(y));
                 if (lx != ly) return lx > ly;
+                if (lx == 5 && bundle > 1) {  // single-row tasks: equal column lists side by side
+                    const int c = cmp_cols(x, y);
+                    if (c != 0) return c < 0;
+                }
                 if (height[x] != height[y]) return height[x] > height[y];
                 return len_of(x) > len_of(y);
             });
@@ -468,7 +485,7 @@ void build_stream_plan(const AugPlan& P, bool upper, const int* out_index, const
             const int len = len_of(ord[i]);
             if (len > 128) throw std::runtime_error("stream plan: a row exceeds 128 entries (AugParams.cap)");
             const int lg = lanes_log2_for(len);
-            Task t{i, 0, lg, 0, l};
+            Task t{i, 0, lg, 0, l, 0};
             // rows per task: the lane count, and the record must fit its slot
             int longest = 0;
             while (i < b && (t.cnt << lg) < 32 && lanes_log2_for(len_of(ord[i])) == lg) {
@@ -480,8 +497,38 @@ void build_stream_plan(const AugPlan& P, bool upper, const int* out_index, const
                 ++i;
             }
             t.nq = (longest + (1 << lg) - 1) >> lg;
+            if (lg == 5 && bundle > 1 && !tasks.empty()) {
+                const Task& pv = tasks.back();
+                if (pv.level == l && pv.lg == 5 && cmp_cols(ord[pv.first], ord[t.first]) == 0) {
+                    int run = 1;  // tasks of the bundle so far
+                    for (size_t q = tasks.size(); q-- > 0 && tasks[q].cont;) ++run;
+                    if (run < bundle) t.cont = 1;
+                }
+            }
             tasks.push_back(t);
         }
+    }
+    if (getenv("EXG_PLAN_VERBOSE")) {  // how many single-row tasks repeat the previous one's column list?
+        long long wide = 0, same = 0, wide_entries = 0;
+        std::vector<int> idx;
+        for (int l = 0; l < P.levels; ++l) {
+            idx.clear();
+            for (long long i = P.level_first_pos[l]; i < P.level_first_pos[l + 1]; ++i)
+                if (lanes_log2_for(len_of(ord[i])) == 5) idx.push_back(ord[i]);
+            auto cmp = [&](int x, int y) {
+                const int lx = len_of(x), ly = len_of(y);
+                if (lx != ly) return lx < ly ? -1 : 1;
+                return std::memcmp(&P.col[P.meta[4 * (size_t)x + 2]], &P.col[P.meta[4 * (size_t)y + 2]], sizeof(int) * lx);
+            };
+            std::sort(idx.begin(), idx.end(), [&](int x, int y) { return cmp(x, y) < 0; });
+            wide += (long long)idx.size();
+            for (size_t i = 0; i < idx.size(); ++i) {
+                wide_entries += len_of(idx[i]);
+                if (i && cmp(idx[i - 1], idx[i]) == 0) ++same;
+            }
+        }
+        fprintf(stderr, "stream plan %s: single-row tasks %lld (%lld entries), %lld repeat another row's columns\n",
+                upper ? "U" : "L", wide, wide_entries, same);
     }
     const size_t NT = tasks.size();
     S.n_tasks = (long long)NT;
@@ -533,20 +580,33 @@ void build_stream_plan(const AugPlan& P, bool upper, const int* out_index, const
         // consumer's start.  A free warp takes the most urgent task (largest
         // height) whose dependencies are `hop` old, or else waits for the one
         // that becomes ready first.
+        // a bundle (a task and the cont tasks behind it) is one unit of the
+        // schedule: `size` costs on one warp; head[t] = its first task
+        std::vector<int> head(NT), bsize(NT, 0);
+        for (size_t t = 0; t < NT; ++t) {
+            head[t] = tasks[t].cont ? head[t - 1] : (int)t;
+            ++bsize[head[t]];
+        }
         std::vector<int> theight(NT, 0), ndep(NT, 0);
         std::vector<long long> sptr(NT + 1, 0);
-        std::vector<int> deps;  // scratch: a task's distinct producers
-        auto producers = [&](size_t t) {
+        std::vector<int> deps;  // scratch: a unit's distinct producer units
+        auto producers = [&](size_t h) {
             deps.clear();
-            for (int seg = 0; seg < tasks[t].cnt; ++seg) {
-                const int p = ord[tasks[t].first + seg];
-                theight[t] = std::max(theight[t], height[p]);
-                for (int k = P.meta[4 * (size_t)p + 2]; k < P.meta[4 * (size_t)p + 3]; ++k) deps.push_back(prod[P.col[k]]);
-            }
+            for (size_t t = h; t < h + (size_t)bsize[h]; ++t)
+                for (int seg = 0; seg < tasks[t].cnt; ++seg) {
+                    const int p = ord[tasks[t].first + seg];
+                    theight[h] = std::max(theight[h], height[p]);
+                    if (t == h)  // cont tasks repeat the head's columns
+                        for (int k = P.meta[4 * (size_t)p + 2]; k < P.meta[4 * (size_t)p + 3]; ++k)
+                            deps.push_back(head[prod[P.col[k]]]);
+                }
             std::sort(deps.begin(), deps.end());
             deps.erase(std::unique(deps.begin(), deps.end()), deps.end());
         };
+        size_t n_units = 0;
         for (size_t t = 0; t < NT; ++t) {
+            if (head[t] != (int)t) continue;
+            ++n_units;
             producers(t);
             ndep[t] = (int)deps.size();
             for (int d : deps) ++sptr[d + 1];
@@ -556,22 +616,23 @@ void build_stream_plan(const AugPlan& P, bool upper, const int* out_index, const
         {
             std::vector<long long> at(sptr.begin(), sptr.end() - 1);
             for (size_t t = 0; t < NT; ++t) {
+                if (head[t] != (int)t) continue;
                 producers(t);
                 for (int d : deps) succ[(size_t)at[d]++] = (int)t;
             }
         }
-        using TE = std::pair<double, int>;   // {ready time, task}: earliest first
-        using AE = std::pair<long long, int>;  // {urgency, -task}: most urgent first
+        using TE = std::pair<double, int>;   // {ready time, unit}: earliest first
+        using AE = std::pair<long long, int>;  // {urgency, -unit}: most urgent first
         std::priority_queue<TE, std::vector<TE>, std::greater<TE>> pending, warps;
         std::priority_queue<AE> avail;
         std::vector<double> rdy(NT, 0.0), start(NT, 0.0);
         for (size_t t = 0; t < NT; ++t)
-            if (ndep[t] == 0) pending.push({0.0, (int)t});
+            if (head[t] == (int)t && ndep[t] == 0) pending.push({0.0, (int)t});
         for (int w = 0; w < W; ++w) warps.push({0.0, w});
         auto urgency = [&](int t) { return ((long long)theight[t] << 20) - tasks[t].level; };
         size_t done = 0;
         std::vector<int> w_of_task(NT, 0);
-        while (done < NT) {
+        while (done < n_units) {
             auto [tau, w] = warps.top();
             warps.pop();
             while (!pending.empty() && pending.top().first <= tau) {
@@ -590,15 +651,18 @@ void build_stream_plan(const AugPlan& P, bool upper, const int* out_index, const
                 st = pending.top().first;
                 pending.pop();
             }
-            start[t] = st;
-            fin[t] = st + 1.0;
-            w_of_task[t] = w;
-            warps.push({fin[t], w});
-            span_list = std::max(span_list, fin[t]);
+            const double f = st + (double)bsize[t];
+            for (int q = 0; q < bsize[t]; ++q) {
+                start[t + q] = st + q;
+                fin[t + q] = f;
+                w_of_task[t + q] = w;
+            }
+            warps.push({f, w});
+            span_list = std::max(span_list, f);
             ++done;
             for (long long e = sptr[t]; e < sptr[t + 1]; ++e) {
                 const int s = succ[(size_t)e];
-                rdy[s] = std::max(rdy[s], fin[t] + hop);
+                rdy[s] = std::max(rdy[s], f + hop);
                 if (--ndep[s] == 0) pending.push({rdy[s], s});
             }
         }
@@ -622,7 +686,7 @@ void build_stream_plan(const AugPlan& P, bool upper, const int* out_index, const
         }
     }
     // ---- stream sizes
-    auto rec_bytes = [&](const Task& t) { return (16 + t.nq * 384 + t.cnt * MS + 15) / 16 * 16; };
+    auto rec_bytes = [&](const Task& t) { return (16 + t.nq * (t.cont ? 256 : 384) + t.cnt * MS + 15) / 16 * 16; };
     std::vector<long long> bytes(W, 0);
     for (size_t r = 0; r < NT; ++r) {
         const int rb = rec_bytes(tasks[by_rank[r]]);
@@ -663,13 +727,22 @@ void build_stream_plan(const AugPlan& P, bool upper, const int* out_index, const
                 }
             }
         }
+        if (T.cont) {  // right behind the task whose columns it repeats, on the same warp
+            if (wpos[r] == 0) throw std::runtime_error("stream plan: a cont task opens a stream");
+            const Task& pv = tasks[by_rank[wseq[(size_t)(wptr[w] + wpos[r] - 1)]]];
+            if (pv.nq != T.nq || pv.lg != T.lg || pv.cnt != 1 || T.cnt != 1)
+                throw std::runtime_error("stream plan: a cont task does not match its predecessor");
+        }
         const long long ahead = wptr[w] + wpos[r] + (kStreamRing - 1);
-        put<int>(S.data, at, T.cnt | (T.lg << 8) | (T.nq << 12) | (T.level << 16));
+        put<int>(S.data, at, T.cnt | (T.lg << 8) | (T.nq << 12) | (T.cont << 15) | (T.level << 16));
         put<int>(S.data, at + 4, ahead < wptr[w + 1] ? rec_bytes(tasks[by_rank[wseq[(size_t)ahead]]]) : 0);
         put<int>(S.data, at + 8, flag);
         put<int>(S.data, at + 12, (int)r);
-        const size_t col_at = at + 16, val_at = col_at + (size_t)T.nq * 128, meta_at = val_at + (size_t)T.nq * 256;
-        for (int q = 0; q < T.nq * 32; ++q) put<int>(S.data, col_at + 4 * (size_t)q, dummy);
+        // cont records carry no column ids
+        const size_t col_at = at + 16, val_at = col_at + (T.cont ? 0 : (size_t)T.nq * 128),
+                     meta_at = val_at + (size_t)T.nq * 256;
+        if (!T.cont)
+            for (int q = 0; q < T.nq * 32; ++q) put<int>(S.data, col_at + 4 * (size_t)q, dummy);
         const int lpr = 1 << T.lg;
         for (int seg = 0; seg < T.cnt; ++seg) {
             const int p = ord[T.first + seg];
@@ -686,14 +759,15 @@ void build_stream_plan(const AugPlan& P, bool upper, const int* out_index, const
             for (int e = 0; e < k1 - k0; ++e) {
                 const int sl = e & (lpr - 1), q = e >> T.lg;
                 const int slot = q * 32 + seg * lpr + sl;
-                put<int>(S.data, col_at + 4 * (size_t)slot, P.col[k0 + e]);
+                if (!T.cont) put<int>(S.data, col_at + 4 * (size_t)slot, P.col[k0 + e]);
                 put<double>(S.data, val_at + 8 * (size_t)slot, P.val[k0 + e]);
             }
             S.n_entries += k1 - k0;
         }
         S.n_slots += T.nq * 32;
+        S.n_cont += T.cont;
         // distinct 32-byte sectors the task's gather instructions touch
-        for (int q = 0; q < T.nq; ++q) {
+        for (int q = 0; q < (T.cont ? 0 : T.nq); ++q) {
             int sec[32];
             for (int l = 0; l < 32; ++l) sec[l] = get<int>(S.data.data() + col_at + 4 * (size_t)(q * 32 + l)) >> 2;
             std::sort(sec, sec + 32);
@@ -704,8 +778,8 @@ void build_stream_plan(const AugPlan& P, bool upper, const int* out_index, const
         fprintf(stderr, "stream plan %s: schedule %s, warps %d, modelled span (task costs, hop %.2f): level order %.1f, list %.1f; tasks/warp %.1f\n",
                 upper ? "U" : "L", prm.sched ? "list" : "level order", W, hop, span_level, span_list, (double)NT / W);
     if (getenv("EXG_PLAN_VERBOSE"))
-        fprintf(stderr, "stream plan %s: tasks %lld entries %lld gather sectors %lld (%.2f per entry) bytes %zu levels %d\n",
-                upper ? "U" : "L", S.n_tasks, S.n_entries, S.n_gather_sectors,
+        fprintf(stderr, "stream plan %s: tasks %lld (%lld reuse the columns of the task before) entries %lld gather sectors %lld (%.2f per entry) bytes %zu levels %d\n",
+                upper ? "U" : "L", S.n_tasks, S.n_cont, S.n_entries, S.n_gather_sectors,
                 (double)S.n_gather_sectors / (double)std::max<long long>(1, S.n_entries), S.data.size(), S.levels);
 }
 
@@ -713,6 +787,8 @@ void eval_stream_plan(const StreamPlan& S, bool upper, const double* in, double*
                       double coef, const double* add) {
     const int W = S.n_warps, MS = upper ? kStreamMetaU : kStreamMetaL;
     std::vector<long long> cur(W), left(W);
+    std::vector<const unsigned char*> last_cols(W, nullptr);  // column ids of the warp's last non-cont record
+    std::vector<int> last_nq(W, -1);
     for (int w = 0; w < W; ++w) {
         cur[w] = ((long long)(unsigned)S.desc[8 * (size_t)w]) | ((long long)S.desc[8 * (size_t)w + 1] << 32);
         left[w] = S.desc[8 * (size_t)w + 2];
@@ -725,8 +801,11 @@ void eval_stream_plan(const StreamPlan& S, bool upper, const double* in, double*
         const unsigned char* r = S.data.data() + cur[w];
         const int w0 = get<int>(r);
         const int cnt = w0 & 0xFF, lg = (w0 >> 8) & 0xF, nq = (w0 >> 12) & 0x7, lpr = 1 << lg;
+        const bool cont = (w0 >> 15) & 1;
         if (get<int>(r + 12) != (int)t) throw std::runtime_error("stream plan: record order mismatch");
-        const int rb = (16 + nq * 384 + cnt * MS + 15) / 16 * 16;
+        const int rb = (16 + nq * (cont ? 256 : 384) + cnt * MS + 15) / 16 * 16;
+        if (cont && (last_nq[w] != nq || cnt != 1 || lg != 5))
+            throw std::runtime_error("stream plan: a cont record does not follow a matching record");
         // integrity of what the kernel will trust: sizes, ids, the look-ahead size
         if (cnt < 1 || cnt > 32 || lg > 5 || (cnt << lg) > 32 || nq > 4 || rb > kStreamSlot ||
             (size_t)(cur[w] + rb) > S.data.size())
@@ -734,8 +813,10 @@ void eval_stream_plan(const StreamPlan& S, bool upper, const double* in, double*
         const int fc = get<int>(r + 8);
         if (fc < 0 || fc > S.n_aug) throw std::runtime_error("stream plan: flag column out of range");
         cur[w] += rb;
-        const unsigned char* cols = r + 16;
-        const unsigned char* vals = cols + (size_t)nq * 128;
+        const unsigned char* cols = cont ? last_cols[w] : r + 16;
+        const unsigned char* vals = r + 16 + (cont ? 0 : (size_t)nq * 128);
+        last_cols[w] = cols;
+        last_nq[w] = (cnt == 1 && lg == 5) ? nq : -1;
         const unsigned char* meta = vals + (size_t)nq * 256;
         double acc[32];
         for (int lane = 0; lane < 32; ++lane) {

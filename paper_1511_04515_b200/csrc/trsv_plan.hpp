@@ -110,6 +110,11 @@ struct StreamParams {
     // hand-off of `hop` task costs
     int sched = 1;
     double hop = 3.0;
+    // list schedule only: up to `bundle` single-row tasks with one column list
+    // run back to back on one warp and share the gathered dependencies
+    // (measured at config 1: 3 is best; from 8 up the serial bundle costs more
+    // than the shared gathers save, also when only rows with slack are bundled)
+    int bundle = 3;
 };
 
 struct StreamPlan {
@@ -118,6 +123,7 @@ struct StreamPlan {
     int levels = 0;
     long long n_aug = 0;          // unknowns; out[n_aug] is the dummy (0.0)
     long long n_tasks = 0, n_rows = 0, n_entries = 0, n_slots = 0;
+    long long n_cont = 0;            // tasks that reuse the columns (and gathered values) of the task before
     long long n_gather_sectors = 0;  // distinct 32-byte sectors over all gather instructions
     int max_record = 0;
     std::vector<int> desc;        // 8 ints per warp

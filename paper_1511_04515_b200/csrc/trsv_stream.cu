@@ -139,20 +139,25 @@ __global__ void __launch_bounds__(kWarps * 32, kMinB)
         int w0, ahead, fc, tid;
         asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(w0), "=r"(ahead), "=r"(fc), "=r"(tid) : "r"(base));
         const int cnt = w0 & 0xFF, lg = (w0 >> 8) & 0xF, nq = (w0 >> 12) & 0x7;
-        r.fy = ld_val(out + fc);
+        const bool cont = (w0 >> 15) & 1;
+        if (!cont) {
+            r.fy = ld_val(out + fc);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            r.y[q] = 0.0;
-            r.c[q] = 0;
-            if (q < nq) {
-                r.c[q] = lds_i(base + 16 + (q * 32 + lane) * 4);
-                r.y[q] = ld_val(out + r.c[q]);
+            for (int q = 0; q < 4; ++q) {
+                r.y[q] = 0.0;
+                r.c[q] = 0;
+                if (q < nq) {
+                    r.c[q] = lds_i(base + 16 + (q * 32 + lane) * 4);
+                    r.y[q] = ld_val(out + r.c[q]);
+                }
             }
         }
+        // a cont record repeats the column list of the task before it: it takes
+        // that task's gathered values when its turn comes (step), no loads here
         r.out = -1;
         r.b = 0.0;
         if ((lane & ((1 << lg) - 1)) == 0 && (lane >> lg) < cnt) {
-            const unsigned m = base + 16 + nq * 384 + (lane >> lg) * MS;
+            const unsigned m = base + 16 + nq * (cont ? 256 : 384) + (lane >> lg) * MS;
             r.out = lds_i(m);
             const int in = lds_i(m + 4);
             if (in >= 0) r.b = a.in[in];
@@ -165,10 +170,16 @@ __global__ void __launch_bounds__(kWarps * 32, kMinB)
     auto step = [&](int k, Rec& cur, Rec& far) {
         __syncwarp();  // every lane is done with task k - 1's slot
         request(lds_i(cur.base + 4));
+        const int w0 = lds_i(cur.base);
+        const bool cont = (w0 >> 15) & 1;
+        if (cont) {  // task k - 1 (in `far`, complete) gathered the same dependencies
+#pragma unroll
+            for (int q = 0; q < 4; ++q) cur.y[q] = far.y[q];
+        }
         if (k + 1 < n_tasks) load(far);
         unsigned long long t_begin = 0, t_ready = 0;
         if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
-        if (!a.nodeps) {
+        if (!a.nodeps && !cont) {
             if (is_sentinel(cur.fy)) {
                 // early: poll the one value the latest producer writes
                 // (re-reading every missing value on thin levels while polling,
@@ -194,9 +205,8 @@ __global__ void __launch_bounds__(kWarps * 32, kMinB)
             }
         }
         if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_ready));
-        const int w0 = lds_i(cur.base);
         const int lg = (w0 >> 8) & 0xF, nq = (w0 >> 12) & 0x7;
-        const unsigned vals = cur.base + 16 + nq * 128 + lane * 8;
+        const unsigned vals = cur.base + 16 + (cont ? 0 : nq * 128) + lane * 8;
         double acc = 0.0;
 #pragma unroll
         for (int q = 0; q < 4; ++q)
@@ -205,7 +215,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinB)
         if (cur.out >= 0) {
             double s = cur.b - acc;
             if (UPPER) {
-                const unsigned m = cur.base + 16 + nq * 384 + (lane >> lg) * MS;
+                const unsigned m = cur.base + 16 + nq * (cont ? 256 : 384) + (lane >> lg) * MS;
                 s = s * lds_d(m + 16);  // 1 / diag (FAST mode)
                 st_relaxed(out + cur.out, s);
                 const int qq = lds_i(m + 8);

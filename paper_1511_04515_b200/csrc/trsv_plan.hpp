@@ -74,23 +74,41 @@ void eval_aug_plan(const AugPlan& P, bool upper, const double* in, double* out);
 // Per-warp record streams for k_trsv4 (trsv_stream.cu).
 //
 // The augmented rows (every one <= 128 entries: AugParams.cap) are cut, level
-// by level, into warp tasks of at most 32 lanes x 4 entries; task t belongs to
-// warp t mod W (W = co-resident warps of the launch), and each warp's tasks
-// are serialised, in order, into ONE contiguous byte stream.  The warp pulls
-// its stream through a shared-memory ring of kStreamRing record slots, one
-// bulk async copy (TMA) per record, a few records ahead: nothing on a task's
-// path is a dependent global load any more, and every field sits at a fixed
-// offset of its slot.
+// by level, into warp tasks of at most 32 lanes x 4 entries, and each warp's
+// tasks are serialised, in order, into ONE contiguous byte stream.  The warp
+// pulls its stream through a shared-memory ring of kStreamRing record slots,
+// one bulk async copy (TMA) per record, a few records ahead: nothing on a
+// task's path is a dependent global load any more, and every field sits at a
+// fixed offset of its slot.
+//
+// Which warp runs which task, and when, is a list schedule (StreamParams.sched):
+// W warps with unit task cost and a hand-off of `hop` costs from a producer's
+// finish to a consumer's start are simulated; the warp that frees first takes
+// the ready task with the longest chain of dependent rows behind it (or waits
+// for the first to become ready).  Ranks follow the simulated start times, a
+// warp runs its tasks by ascending rank and every dependency has a smaller
+// rank, so whatever the real timing the unfinished task of smallest rank can
+// run: no deadlock.  (Level by level with task t on warp t mod W, the first
+// plan, left every critical task behind up to five rounds of its level's
+// other tasks: 0.99 ms per solve pair at config 1 against 0.84.)
+//
+// Rows of 65..128 entries are tasks of their own, and most of them repeat the
+// column list of another row of their level (the rows of a block inverse over
+// one 128-column chunk; in U the rows of a supernode over its ancestors: 54% of
+// L's and 82% of U's single-row tasks at config 1).  Up to StreamParams.bundle
+// of them run back to back on one warp; the first gathers the dependencies,
+// the others ("cont" records, no column ids) reuse its registers.
 //
 // Record (16-byte multiple, <= kStreamSlot bytes):
-//   header 16 B  {cnt | lg << 8 | nq << 12 | level << 16,
+//   header 16 B  {cnt | lg << 8 | nq << 12 | cont << 15 | level << 16,
 //                 bytes of this warp's record kStreamRing - 1 places ahead (0: none),
 //                 flag, task id}
 //                cnt rows (1..32), 2^lg lanes per row, nq (0..4) value batches;
 //                flag = the dependency produced by the latest task (the one
 //                value a waiting task polls)
 //   nq x 32 column ids (int32); an empty slot holds the dummy id n_aug, whose
-//                value is always 0.0
+//                value is always 0.0.  Absent in a cont record (cnt 1, lg 5): its
+//                columns are those of the record before it in the stream
 //   nq x 32 values (fp64)
 //   cnt metas    L: {out id, rhs index or -1}                                 (8 B)
 //                U: {out id, rhs index or -1, epilogue index or -1, 0, 1 / diag}  (24 B)

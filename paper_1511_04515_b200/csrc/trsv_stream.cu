@@ -30,9 +30,9 @@ namespace {
 
 constexpr int kR = kStreamRing;
 constexpr int kSlot = kStreamSlot;
-constexpr int kWarps = 8;  // warps per CTA
-constexpr int kMinB = 3;   // CTAs per SM
-constexpr size_t kSmem = (size_t)kWarps * kR * kSlot + (size_t)kWarps * kR * 8;
+// CTA shapes: {warps per CTA, CTAs per SM}; 8 KB of ring per warp, 72 registers per thread
+constexpr int kShapes[2][2] = {{8, 3}, {9, 3}};
+constexpr size_t smem_of(int warps) { return (size_t)warps * kR * kSlot + (size_t)warps * kR * 8; }
 static_assert(kR == 4, "ring: the task being reduced, the one whose gathers are in flight, two records in flight");
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -74,7 +74,7 @@ __device__ __forceinline__ double lds_d(unsigned addr) {
 
 }  // namespace
 
-template <bool UPPER>
+template <bool UPPER, int kWarps, int kMinB>
 __global__ void __launch_bounds__(kWarps * 32, kMinB)
     k_trsv4(StreamArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -249,15 +249,26 @@ __global__ void __launch_bounds__(kWarps * 32, kMinB)
 // ---- launch ------------------------------------------------------------------
 namespace {
 
+int shape_id() {  // EXG_STREAM_SHAPE=0: 8 warps x 3 CTAs per SM, 1: 9 x 3
+    static const int id = getenv("EXG_STREAM_SHAPE") ? std::max(0, std::min(1, atoi(getenv("EXG_STREAM_SHAPE")))) : 0;
+    return id;
+}
+
+const void* kernel_of(bool upper, int shape) {
+    if (shape == 0) return upper ? (const void*)k_trsv4<true, 8, 3> : (const void*)k_trsv4<false, 8, 3>;
+    return upper ? (const void*)k_trsv4<true, 9, 3> : (const void*)k_trsv4<false, 9, 3>;
+}
+
 cudaError_t stream_setup(bool upper, int* occ_out) {
     static int occ[2] = {0, 0};
+    const int sh = shape_id(), warps = kShapes[sh][0], minb = kShapes[sh][1];
     if (!occ[upper]) {
-        auto fn = upper ? (const void*)k_trsv4<true> : (const void*)k_trsv4<false>;
-        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
+        const void* fn = kernel_of(upper, sh);
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_of(warps));
         if (e != cudaSuccess) return e;
         int o = 0;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, kWarps * 32, kSmem);
-        if (o > kMinB) o = kMinB;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, warps * 32, smem_of(warps));
+        if (o > minb) o = minb;
         if (e != cudaSuccess) return e;
         if (o < 1) return cudaErrorLaunchOutOfResources;
         occ[upper] = o;
@@ -271,7 +282,7 @@ cudaError_t stream_setup(bool upper, int* occ_out) {
 int trsv_stream_warps(bool upper, int num_sms) {
     int occ = 0;
     if (stream_setup(upper, &occ) != cudaSuccess) return 0;
-    return num_sms * occ * kWarps;
+    return num_sms * occ * kShapes[shape_id()][0];
 }
 
 cudaError_t trsv_stream(const Launch& L, bool upper, const StreamArgs& a) {
@@ -279,13 +290,14 @@ cudaError_t trsv_stream(const Launch& L, bool upper, const StreamArgs& a) {
     int occ = 0;
     cudaError_t e = stream_setup(upper, &occ);
     if (e != cudaSuccess) return e;
-    const unsigned grid = (unsigned)((a.n_warps + kWarps - 1) / kWarps);
+    const int warps = kShapes[shape_id()][0];
+    const unsigned grid = (unsigned)((a.n_warps + warps - 1) / warps);
     if ((long long)grid > (long long)L.num_sms * occ) return cudaErrorCooperativeLaunchTooLarge;
     void* args[] = {(void*)&a};
     // cooperative: every warp's producers are resident (the hand-offs spin on
     // them); a refused launch must not leave later kernels waiting on sentinels
-    e = cudaLaunchCooperativeKernel(upper ? (void*)k_trsv4<true> : (void*)k_trsv4<false>, dim3(grid),
-                                    dim3(kWarps * 32), args, kSmem, L.stream);
+    e = cudaLaunchCooperativeKernel(const_cast<void*>(kernel_of(upper, shape_id())), dim3(grid), dim3(warps * 32), args,
+                                    smem_of(warps), L.stream);
     if (L.launches) ++*L.launches;
     return e;
 }

@@ -240,10 +240,6 @@ void solve_dev(exg_ctx* c, const double* b, double* final_out, double coef, cons
                 sa.trace = a.trace;
                 static const int nodeps = getenv("EXG_STREAM_NODEPS") ? atoi(getenv("EXG_STREAM_NODEPS")) : 0;
                 sa.nodeps = nodeps;
-                static const int poll_ns = getenv("EXG_STREAM_POLL_NS") ? atoi(getenv("EXG_STREAM_POLL_NS")) : 0;
-                static const int poll_cap = getenv("EXG_STREAM_POLL_CAP") ? atoi(getenv("EXG_STREAM_POLL_CAP")) : 0;
-                sa.poll_ns = poll_ns;
-                sa.poll_cap = poll_cap;
                 ck(exg::dev::trsv_stream(c->L(), upper, sa), "stream solve launch");
                 c->prof_end(upper ? EXG_K_TRSV_U : EXG_K_TRSV_L, e0);
                 continue;

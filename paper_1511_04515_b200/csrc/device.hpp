@@ -46,8 +46,6 @@ struct StreamArgs {
     const Ctrl* ctrl;
     unsigned long long* trace;   // debug: 5 values per task, or null
     int nodeps;                  // debug (EXG_STREAM_NODEPS): ignore readiness, wrong results: throughput bound only
-    int poll_ns;                 // back-off of a waiting task between polls: first sleep (ns), doubling up to poll_cap
-    int poll_cap;
 };
 
 struct SubArgs {

@@ -2,9 +2,9 @@
 // (trsv_plan.hpp; replaces the row-by-row sweeps of Factorization::solve,
 // sparse_lu.cpp:255-291, for one triangle of the blocked augmented system).
 //
-// One persistent, co-resident grid.  Warp w owns tasks w, w + W, w + 2W, ...
-// of the level-ordered task list; the host serialised them into ONE contiguous
-// byte stream per warp.  The warp pulls its stream through a private ring of
+// One persistent, co-resident grid.  The host's list schedule (trsv_plan.hpp)
+// gave every warp its tasks, in the order it will run them, as ONE contiguous
+// byte stream.  The warp pulls its stream through a private ring of
 // kStreamRing record slots in shared memory, one bulk async copy per record
 // (cp.async.bulk + mbarrier complete_tx), issued kStreamRing - 1 records
 // ahead: a task's descriptor, row metadata, column ids and values sit at
@@ -13,8 +13,10 @@
 // requested one task ahead.  The solution value is the ready flag (all-ones
 // sentinel pre-fill, one 64-bit relaxed store to publish); a task that is
 // early polls ONE value, the dependency its latest producer writes, and only
-// then re-reads whatever else was missing.  A task only waits on earlier
-// tasks and every warp is resident (cooperative launch), so the earliest
+// then re-reads whatever else was missing.  A "cont" record repeats the column
+// list of the record before it: it takes over that task's gathered values
+// (registers) and neither gathers nor waits.  A task only waits on tasks of
+// smaller rank and every warp is resident (cooperative launch), so the earliest
 // unfinished task always progresses: no deadlock, no atomics, no grid barriers.
 #include <algorithm>
 #include <cstdlib>
@@ -30,9 +32,11 @@ namespace {
 
 constexpr int kR = kStreamRing;
 constexpr int kSlot = kStreamSlot;
-// CTA shapes: {warps per CTA, CTAs per SM}; 8 KB of ring per warp, 72 registers per thread
-constexpr int kShapes[2][2] = {{8, 3}, {9, 3}};
-constexpr size_t smem_of(int warps) { return (size_t)warps * kR * kSlot + (size_t)warps * kR * 8; }
+// 8 warps per CTA, 3 CTAs per SM: 8 KB of ring per warp, 72 registers per thread (27 warps per SM as
+// 9 x 3 measured slower, 0.83 against 0.75 ms per solve pair at config 1; so did 16 and 12 per SM)
+constexpr int kWarps = 8;
+constexpr int kMinB = 3;
+constexpr size_t kSmem = (size_t)kWarps * kR * kSlot + (size_t)kWarps * kR * 8;
 static_assert(kR == 4, "ring: the task being reduced, the one whose gathers are in flight, two records in flight");
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -74,7 +78,7 @@ __device__ __forceinline__ double lds_d(unsigned addr) {
 
 }  // namespace
 
-template <bool UPPER, int kWarps, int kMinB>
+template <bool UPPER>
 __global__ void __launch_bounds__(kWarps * 32, kMinB)
     k_trsv4(StreamArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -183,18 +187,13 @@ __global__ void __launch_bounds__(kWarps * 32, kMinB)
             if (is_sentinel(cur.fy)) {
                 // early: poll the one value the latest producer writes
                 // (re-reading every missing value on thin levels while polling,
-                // and issuing the first re-read before the next task's load, both
-                // measured slower: profiles/r02)
+                // issuing the first re-read before the next task's load, a sleeping
+                // back-off between polls and patching the polled value into the lanes
+                // that gathered it all measured no faster or slower: profiles/r02)
                 const double* fp = out + lds_i(cur.base + 8);
-                unsigned ns = (unsigned)a.poll_ns;
-                for (;;) {
+                do {
                     cur.fy = ld_val(fp);
-                    if (!is_sentinel(cur.fy)) break;
-                    if (ns) {
-                        __nanosleep(ns);
-                        ns = min(2u * ns, (unsigned)a.poll_cap);
-                    }
-                }
+                } while (is_sentinel(cur.fy));
             }
             // then whatever else was not there when it was gathered
             while (__any_sync(FULL, is_sentinel(cur.y[0]) | is_sentinel(cur.y[1]) | is_sentinel(cur.y[2]) |
@@ -249,26 +248,15 @@ __global__ void __launch_bounds__(kWarps * 32, kMinB)
 // ---- launch ------------------------------------------------------------------
 namespace {
 
-int shape_id() {  // EXG_STREAM_SHAPE=0: 8 warps x 3 CTAs per SM, 1: 9 x 3
-    static const int id = getenv("EXG_STREAM_SHAPE") ? std::max(0, std::min(1, atoi(getenv("EXG_STREAM_SHAPE")))) : 0;
-    return id;
-}
-
-const void* kernel_of(bool upper, int shape) {
-    if (shape == 0) return upper ? (const void*)k_trsv4<true, 8, 3> : (const void*)k_trsv4<false, 8, 3>;
-    return upper ? (const void*)k_trsv4<true, 9, 3> : (const void*)k_trsv4<false, 9, 3>;
-}
-
 cudaError_t stream_setup(bool upper, int* occ_out) {
     static int occ[2] = {0, 0};
-    const int sh = shape_id(), warps = kShapes[sh][0], minb = kShapes[sh][1];
     if (!occ[upper]) {
-        const void* fn = kernel_of(upper, sh);
-        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_of(warps));
+        const void* fn = upper ? (const void*)k_trsv4<true> : (const void*)k_trsv4<false>;
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
         if (e != cudaSuccess) return e;
         int o = 0;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, warps * 32, smem_of(warps));
-        if (o > minb) o = minb;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, kWarps * 32, kSmem);
+        if (o > kMinB) o = kMinB;
         if (e != cudaSuccess) return e;
         if (o < 1) return cudaErrorLaunchOutOfResources;
         occ[upper] = o;
@@ -282,7 +270,7 @@ cudaError_t stream_setup(bool upper, int* occ_out) {
 int trsv_stream_warps(bool upper, int num_sms) {
     int occ = 0;
     if (stream_setup(upper, &occ) != cudaSuccess) return 0;
-    return num_sms * occ * kShapes[shape_id()][0];
+    return num_sms * occ * kWarps;
 }
 
 cudaError_t trsv_stream(const Launch& L, bool upper, const StreamArgs& a) {
@@ -290,14 +278,13 @@ cudaError_t trsv_stream(const Launch& L, bool upper, const StreamArgs& a) {
     int occ = 0;
     cudaError_t e = stream_setup(upper, &occ);
     if (e != cudaSuccess) return e;
-    const int warps = kShapes[shape_id()][0];
-    const unsigned grid = (unsigned)((a.n_warps + warps - 1) / warps);
+    const unsigned grid = (unsigned)((a.n_warps + kWarps - 1) / kWarps);
     if ((long long)grid > (long long)L.num_sms * occ) return cudaErrorCooperativeLaunchTooLarge;
     void* args[] = {(void*)&a};
     // cooperative: every warp's producers are resident (the hand-offs spin on
     // them); a refused launch must not leave later kernels waiting on sentinels
-    e = cudaLaunchCooperativeKernel(const_cast<void*>(kernel_of(upper, shape_id())), dim3(grid), dim3(warps * 32), args,
-                                    smem_of(warps), L.stream);
+    e = cudaLaunchCooperativeKernel(upper ? (void*)k_trsv4<true> : (void*)k_trsv4<false>, dim3(grid), dim3(kWarps * 32),
+                                    args, kSmem, L.stream);
     if (L.launches) ++*L.launches;
     return e;
 }

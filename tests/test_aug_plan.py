@@ -177,3 +177,49 @@ def test_stream_plan_long_rows_become_partials():
         assert st["partials"] > 0
         assert np.allclose(x, want, rtol=0, atol=1e-12)
     assert st["levels"] >= n  # no block rewrite: the dense triangle stays sequential
+
+
+@pytest.mark.parametrize("cfg,kw", [(1, dict(width=64)), (1, dict(width=160)), (3, dict(n=3000))],
+                         ids=["c1-4k", "c1-26k", "c3"])
+def test_stream_plan_orders_and_bundles_agree_bit_for_bit(monkeypatch, cfg, kw):
+    """A row's arithmetic depends on its own lanes only: level order (task t on warp t mod W), the
+    list schedule, and the list schedule with bundles of rows sharing a column list (cont records,
+    evaluated with the columns of the record before them) all give the same bits.  The dense
+    triangle below makes sure bundles exist and shrink the streams (no column ids in a cont record)."""
+    s = ex.System.generate(cfg, **kw)
+    f = ex.lu_factor(s.G)
+    n = f.n
+    parts = strict_parts(f)
+    b = np.random.default_rng(cfg).uniform(-1, 1, n)
+    for upper, part, in_index in ((False, parts[0], np.asarray(f.row_perm, np.int32)),
+                                  (True, parts[1], np.arange(n, dtype=np.int32))):
+        got = []
+        for sched, bundle in ((0, 1), (1, 1), (1, 3), (1, 16)):
+            monkeypatch.setenv("EXG_STREAM_SCHED", str(sched))
+            monkeypatch.setenv("EXG_STREAM_BUNDLE", str(bundle))
+            x, _, st = stream_solve(upper, n, part, in_index, b, 256)
+            got.append((x, st))
+        for x, st in got[1:]:
+            assert np.array_equal(x.view(np.int64), got[0][0].view(np.int64))
+            assert st["tasks"] >= got[0][1]["tasks"] - 64 and st["entries"] == got[0][1]["entries"]
+        assert got[3][1]["bytes"] <= got[2][1]["bytes"] <= got[1][1]["bytes"]
+
+
+def test_stream_plan_bundles_shrink_a_dense_block(monkeypatch):
+    """Rows of a 700-row block inverse over one 128-column chunk repeat a column list: bundled, they
+    drop their column ids (512 bytes of a 1.5 KB record)."""
+    n = 700
+    rng = np.random.default_rng(7)
+    ptr, col, val = [0], [], []
+    for r in range(n):
+        col += list(range(r))
+        val += list(rng.uniform(-0.01, 0.01, r))
+        ptr.append(len(col))
+    part = (np.array(ptr, np.int32), np.array(col, np.int32), np.array(val), np.ones(n))
+    b = rng.uniform(-1, 1, n)
+    res = {}
+    for bundle in (1, 3):
+        monkeypatch.setenv("EXG_STREAM_BUNDLE", str(bundle))
+        res[bundle] = stream_solve(False, n, part, np.arange(n, dtype=np.int32), b, 64)
+    assert np.array_equal(res[1][0].view(np.int64), res[3][0].view(np.int64))
+    assert res[3][2]["bytes"] < 0.9 * res[1][2]["bytes"]

@@ -44,6 +44,7 @@ def main():
     ap.add_argument("--config", type=int, default=1)
     ap.add_argument("--width", type=int, default=0)
     ap.add_argument("--warps", type=int, default=3552)
+    ap.add_argument("--block", default="", help="min_block,max_block of the augmented system (default 8,4096)")
     ap.add_argument("--solve", action="store_true", help="also evaluate the plan and compare both orders")
     args = ap.parse_args()
     kw = {"width": args.width} if args.width else {}
@@ -55,6 +56,7 @@ def main():
     parts = strict_parts(f)
     os.environ["EXG_PLAN_VERBOSE"] = "1"
     b = np.random.default_rng(0).uniform(-1, 1, n)
+    prm = (C.c_int * 2)(*[int(v) for v in args.block.split(",")]) if args.block else None
     for upper, part, in_index in ((False, parts[0], np.asarray(f.row_perm, np.int32)),
                                   (True, parts[1], np.arange(n, dtype=np.int32))):
         ptr, col, val, diag = part
@@ -66,7 +68,7 @@ def main():
             t0 = time.time()
             rc = F.lib.exg_stream_plan_solve(int(upper), n, F.as_ptr(ptr, C.c_int), F.as_ptr(col, C.c_int),
                                              F.as_ptr(val, C.c_double), F.as_ptr(diag, C.c_double),
-                                             F.as_ptr(in_index, C.c_int), None, None, args.warps,
+                                             F.as_ptr(in_index, C.c_int), None, prm, args.warps,
                                              F.as_ptr(b, C.c_double) if args.solve else None,
                                              F.as_ptr(x, C.c_double) if args.solve else None,
                                              None, 1.0, None, st)

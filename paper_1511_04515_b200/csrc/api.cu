@@ -88,8 +88,7 @@ void upload_csr(exg_ctx* c, DCsr& m, int n_rows, int n_cols, int nnz, const int*
     m.n_rows = n_rows;
     m.n_cols = n_cols;
     m.nnz = nnz;
-    m.rowptr = dalloc<int>((size_t)n_rows + 1 + 256);  // k_spmv_v4t copies whole strips of row bounds
-    ck(cudaMemsetAsync(m.rowptr + n_rows + 1, 0, 256 * sizeof(int), c->stream), "upload");
+    m.rowptr = dalloc<int>(n_rows + 1);
     // 8 zero entries past the end: k_spmv_v4t copies 16-byte aligned ranges
     m.col = dalloc<int>((size_t)nnz + 8);
     m.val = dalloc<double>((size_t)nnz + 8);

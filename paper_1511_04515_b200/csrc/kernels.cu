@@ -138,21 +138,20 @@ __global__ void __launch_bounds__(256)
 // whatever the gathers cost (laying rows out for L1 reuse and serving the
 // gathers from a shared-memory window of x both left the 56 us launch where it
 // was, profiles/r02).  Here CTA b owns ONE contiguous slice of rows, cut into
-// strips of 248 rows; a producer warp pulls each strip's rowptr slice and its col
-// and val ranges (contiguous in CSR) into a ring of kSpmvStages shared-memory stages with bulk
+// strips of 248 rows; a producer warp pulls each strip's col and val ranges
+// (contiguous in CSR) into a ring of kSpmvStages shared-memory stages with bulk
 // async copies (cp.async.bulk + mbarrier complete_tx), up to four strips
-// (~190 KB per SM) ahead of the 31 consumer warps, which read row bounds, col and val
-// from shared memory and only gather x from global memory.  The HBM stream no longer waits
-// for the gathers.  max_strip (host, at upload): the most entries any 248
+// (~190 KB per SM) ahead of the 31 consumer warps, which read col/val from shared
+// memory and only gather x from global memory.  The HBM stream no longer waits
+// for the gathers.  (Staging the strips' row bounds through the ring as well
+// measured slower, 60 against 51 us: one more copy per stage on the producer.)  max_strip (host, at upload): the most entries any 248
 // consecutive rows hold; the launcher keeps k_spmv_v4 when a strip would not fit.
 constexpr int kSpmvStages = 4;
 constexpr int kSpmvStageCap = 4096;  // entries per stage (16 KB of col + 32 KB of val)
 constexpr int kSpmvConsumers = 31;   // warps; 8 rows each per strip
 constexpr int kSpmvStripRows = kSpmvConsumers * 8;
 constexpr int kSpmvMaxStrips = 256;
-constexpr int kSpmvRowWords = (kSpmvStripRows + 1 + 3) / 4 * 4;          // row bounds of a strip, 16-byte multiple
-constexpr int kSpmvStageBytes = kSpmvStageCap * 12 + kSpmvRowWords * 4;  // col | val | rowptr slice
-constexpr size_t kSpmvStreamSmem = (size_t)kSpmvStages * kSpmvStageBytes;
+constexpr size_t kSpmvStreamSmem = (size_t)kSpmvStages * kSpmvStageCap * 12;
 __global__ void __launch_bounds__((kSpmvConsumers + 1) * 32, 1)
     k_spmv_v4t(const int* __restrict__ rowptr, const int* __restrict__ col,
                const double* __restrict__ val, int n_rows, int rows_per_cta, double* __restrict__ y,
@@ -194,17 +193,12 @@ __global__ void __launch_bounds__((kSpmvConsumers + 1) * 32, 1)
                 if (s >= kSpmvStages) wait(bar0 + 8 * (kSpmvStages + st), (unsigned)(s / kSpmvStages - 1) & 1u);
                 const int k0 = kb[s] & ~3, k1 = (kb[s + 1] + 3) & ~3;  // 16-byte aligned ranges (the arrays are padded)
                 const unsigned cnt = (unsigned)(k1 - k0), full = bar0 + 8 * st;
-                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full),
-                             "r"(cnt * 12u + kSpmvRowWords * 4u)
-                             : "memory");
-                const unsigned dst = ring0 + (unsigned)st * kSpmvStageBytes;
-                // the strip's row bounds (r0 and the strip length are multiples of 4: aligned)
-                asm volatile(
-                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                        dst + kSpmvStageCap * 12),
-                    "l"(rowptr + r0 + s * kSpmvStripRows), "r"(kSpmvRowWords * 4u), "r"(full)
-                    : "memory");
-                if (cnt == 0) continue;
+                if (cnt == 0) {
+                    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(full) : "memory");
+                    continue;
+                }
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full), "r"(cnt * 12u) : "memory");
+                const unsigned dst = ring0 + (unsigned)st * (kSpmvStageCap * 12);
                 asm volatile(
                     "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
                     "l"(col + k0), "r"(cnt * 4u), "r"(full)
@@ -228,21 +222,24 @@ __global__ void __launch_bounds__((kSpmvConsumers + 1) * 32, 1)
         const double* vs[2];
 #pragma unroll
         for (int t = 0; t < 2; ++t) {
-            const int st = (s + t) % kSpmvStages;
-            const unsigned char* stage = ring + (size_t)st * kSpmvStageBytes;
-            cs[t] = reinterpret_cast<const int*>(stage);
-            vs[t] = reinterpret_cast<const double*>(stage + kSpmvStageCap * 4);
             rr[t] = rq + (s + t) * kSpmvStripRows;
             o[t] = o1[t] = 0;
+            if (rr[t] < r1) {
+                o1[t] = __ldg(rowptr + rr[t] + 1);
+                o[t] = __ldg(rowptr + rr[t]) + sub;
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+            const int st = (s + t) % kSpmvStages;
             if (s + t < n_strips) {
                 wait(bar0 + 8 * st, (unsigned)((s + t) / kSpmvStages) & 1u);
-                if (rr[t] < r1) {  // the row's entries inside the stage
-                    const int* rp = reinterpret_cast<const int*>(stage + kSpmvStageCap * 12) + warp * 8 + (lane >> 2);
-                    const int base = kb[s + t] & ~3;
-                    o[t] = rp[0] + sub - base;
-                    o1[t] = rp[1] - base;
-                }
+                const int base = kb[s + t] & ~3;  // the row's entries inside the stage
+                o[t] -= base;
+                o1[t] -= base;
             }
+            cs[t] = reinterpret_cast<const int*>(ring + (size_t)st * (kSpmvStageCap * 12));
+            vs[t] = reinterpret_cast<const double*>(ring + (size_t)st * (kSpmvStageCap * 12) + kSpmvStageCap * 4);
         }
         int c[2][kSpmvBatch];
         double xv[2][kSpmvBatch];
@@ -2342,7 +2339,7 @@ void spmv_v4(const Launch& L, const int* rowptr, const int* col, const double* v
     // large matrices whose strips fit a stage: col/val through a shared-memory ring (EXG_SPMV_STREAM=0
     // keeps the direct loads)
     static const int stream = getenv("EXG_SPMV_STREAM") ? atoi(getenv("EXG_SPMV_STREAM")) : 1;
-    const int per = (int)((((long long)n_rows + L.num_sms - 1) / L.num_sms + 3) / 4 * 4);
+    const int per = (int)(((long long)n_rows + L.num_sms - 1) / L.num_sms);
     if (stream > 0 && n_rows >= 64 * 1024 && max_strip > 0 && max_strip + 8 <= kSpmvStageCap &&
         per <= kSpmvMaxStrips * kSpmvStripRows) {
         static bool attr = false;

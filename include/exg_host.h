@@ -235,6 +235,19 @@ const int* exg_tran_dims(const exg_tran_result* r);
 /* wall seconds: setup LU, DC solve, stepping loop */
 exg_status exg_tran_timing(const exg_tran_result* r, double* lu_s, double* dc_s, double* loop_s);
 
+
+/* Waveform CSV, byte for byte what the reference's CLI writes
+ * (write_waveform_csv, proj/tools/common.hpp:35-46: a "time,<columns>" header,
+ * then one line per time point, every value as printf("%.17g")).  samples is
+ * row-major n_times x n_cols (exg_tran_samples' layout).  Rows are formatted
+ * by `threads` host threads (<= 0: all cores) into one buffered write; SURVEY
+ * 8(f).4.  EXG_E_CONTRACT when the file cannot be written. */
+exg_status exg_write_waveform_csv(const char* path, int n_times, int n_cols, const double* times,
+                                  const double* samples, const char* const* columns, int threads);
+/* the same for a transient's recorded waveform (columns: exg_tran_n_rec names, the
+ * reference's Waveform::columns) */
+exg_status exg_tran_write_csv(const exg_tran_result* r, const char* path, const char* const* columns, int threads);
+
 #ifdef __cplusplus
 }
 #endif

@@ -221,6 +221,15 @@ class Ref:
     def basis_free(self, bh):
         self.lib.ref_basis_free(bh)
 
+    def write_waveform_csv(self, path, times, samples, columns):
+        """The reference CLI's writer (proj/tools/common.hpp:35-46), unmodified."""
+        times, samples = _d(times), _d(samples)
+        names = (C.c_char_p * len(columns))(*[c.encode() for c in columns])
+        self.lib.ref_write_waveform_csv.argtypes = [C.c_char_p, C.c_int, C.c_int, C.POINTER(C.c_double),
+                                                    C.POINTER(C.c_double), C.POINTER(C.c_char_p)]
+        self._check(self.lib.ref_write_waveform_csv(str(path).encode(), len(times), len(columns),
+                                                    _ptr(times, C.c_double), _ptr(samples, C.c_double), names))
+
     def dense_expm(self, a):
         a = _d(a)
         n = a.shape[0]

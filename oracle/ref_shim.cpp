@@ -16,6 +16,7 @@
 // Factorization's members are private (sparse_lu.hpp:46-51); factors computed
 // elsewhere are installed through the standard explicit-instantiation access
 // rule (no reference source is modified or copied).
+#include "common.hpp"  // proj/tools: the CLI's writers (header-only)
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -739,5 +740,19 @@ int ref_tran_wall(void* rp, double* wall) {
 
 void ref_reset_lu_count() { reset_lu_factor_count(); }
 unsigned long long ref_lu_count() { return lu_factor_count(); }
+
+// write_waveform_csv of the reference's CLI (proj/tools/common.hpp:35-46), unmodified, on a
+// row-major n_times x n_cols sample block: the checker of exg_write_waveform_csv
+int ref_write_waveform_csv(const char* path, int n_times, int n_cols, const double* times,
+                           const double* samples, const char* const* columns) {
+    GUARD_BEGIN
+    Waveform wf;
+    for (int c = 0; c < n_cols; ++c) wf.columns.emplace_back(columns[c]);
+    wf.times.assign(times, times + n_times);
+    wf.samples.resize(n_times);
+    for (int r = 0; r < n_times; ++r) wf.samples[r].assign(samples + (size_t)r * n_cols, samples + (size_t)(r + 1) * n_cols);
+    exsim::cli::write_waveform_csv(path, wf);
+    GUARD_END
+}
 
 }  // extern "C"

@@ -195,6 +195,8 @@ _DEV_PROTOS = {
     "exg_tran_n_dims": (I, [P]),
     "exg_tran_dims": (PI, [P]),
     "exg_tran_timing": (I, [P, PD, PD, PD]),
+    "exg_tran_write_csv": (I, [P, C.c_char_p, C.POINTER(C.c_char_p), I]),
+    "exg_write_waveform_csv": (I, [C.c_char_p, I, I, PD, PD, C.POINTER(C.c_char_p), I]),
 }
 
 

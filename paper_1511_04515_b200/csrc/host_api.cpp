@@ -1,4 +1,10 @@
 // extern "C" glue for the host-side API declared in include/exg_host.h.
+#include <algorithm>
+#include <vector>
+#include <string>
+#include <cstdio>
+#include <thread>
+#include <charconv>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -302,6 +308,56 @@ exg_status exg_stream_plan_solve(int upper, int n, const int* ptr, const int* co
                                   S.n_entries,   S.n_slots,   (long long)S.data.size(), S.max_record, P.n_partials};
         std::memcpy(stats, st, sizeof st);
     }
+    HOST_GUARD_END
+}
+
+exg_status exg_write_waveform_csv(const char* path, int n_times, int n_cols, const double* times,
+                                  const double* samples, const char* const* columns, int threads) {
+    HOST_GUARD_BEGIN
+    if (!path || n_times < 0 || n_cols < 0 || (n_times && !times) || (n_times && n_cols && !samples) ||
+        (n_cols && !columns))
+        throw exg::Error{EXG_E_CONTRACT, "exg_write_waveform_csv: bad arguments"};
+    FILE* f = std::fopen(path, "wb");
+    if (!f) throw exg::Error{EXG_E_CONTRACT, std::string("cannot write '") + path + "'"};
+    std::string head = "time";
+    for (int c = 0; c < n_cols; ++c) {
+        head += ',';
+        head += columns[c];
+    }
+    head += '\n';
+    // rows are independent: each thread formats a contiguous slice into its own buffer
+    unsigned T = threads > 0 ? (unsigned)threads : std::max(1u, std::thread::hardware_concurrency());
+    T = (unsigned)std::max<long long>(1, std::min<long long>(T, ((long long)n_times * (n_cols + 1) + 65535) / 65536));
+    std::vector<std::string> part(T);
+    auto work = [&](unsigned t) {
+        const long long r0 = (long long)n_times * t / T, r1 = (long long)n_times * (t + 1) / T;
+        std::string& o = part[t];
+        o.reserve((size_t)(r1 - r0) * (size_t)(n_cols + 1) * 20);
+        char buf[48];
+        // std::to_chars(general, 17) prints what printf("%.17g") prints in the C locale (both are
+        // correctly rounded to 17 significant digits; same exponent and zero-stripping rules)
+        auto put = [&](double v) {
+            const auto res = std::to_chars(buf, buf + sizeof buf, v, std::chars_format::general, 17);
+            o.append(buf, (size_t)(res.ptr - buf));
+        };
+        for (long long r = r0; r < r1; ++r) {
+            put(times[r]);
+            const double* row = samples + (size_t)r * n_cols;
+            for (int c = 0; c < n_cols; ++c) {
+                o += ',';
+                put(row[c]);
+            }
+            o += '\n';
+        }
+    };
+    std::vector<std::thread> th;
+    for (unsigned t = 1; t < T; ++t) th.emplace_back(work, t);
+    work(0);
+    for (auto& x : th) x.join();
+    bool ok = std::fwrite(head.data(), 1, head.size(), f) == head.size();
+    for (unsigned t = 0; ok && t < T; ++t) ok = std::fwrite(part[t].data(), 1, part[t].size(), f) == part[t].size();
+    ok = (std::fclose(f) == 0) && ok;
+    if (!ok) throw exg::Error{EXG_E_CONTRACT, std::string("cannot write '") + path + "'"};
     HOST_GUARD_END
 }
 

@@ -484,6 +484,11 @@ exg_status exg_tran_records(const exg_tran_result* r, double* t, double* h, int*
 }
 int exg_tran_n_dims(const exg_tran_result* r) { return static_cast<int>(r->dims.size()); }
 const int* exg_tran_dims(const exg_tran_result* r) { return r->dims.data(); }
+exg_status exg_tran_write_csv(const exg_tran_result* r, const char* path, const char* const* columns, int threads) {
+    if (!r) return EXG_E_CONTRACT;
+    return exg_write_waveform_csv(path, static_cast<int>(r->times.size()), r->n_rec, r->times.data(),
+                                  r->samples.data(), columns, threads);
+}
 exg_status exg_tran_timing(const exg_tran_result* r, double* lu_s, double* dc_s, double* loop_s) {
     *lu_s = r->lu_s;
     *dc_s = r->dc_s;

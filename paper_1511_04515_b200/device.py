@@ -198,7 +198,10 @@ class Context:
         self._check(F.lib.exg_synchronize(self._h))
 
     # ---- whole transient
-    def transient(self, sys: System, ctl: F.exg_step_control, t_stop: float, rec_idx) -> TransientResult:
+    def transient(self, sys: System, ctl: F.exg_step_control, t_stop: float, rec_idx, csv_path=None,
+                  csv_columns=None) -> TransientResult:
+        """exg_transient; csv_path: also write the recorded waveform as the reference CLI's CSV
+        (exg_tran_write_csv; csv_columns default to the record indices)."""
         ri = F.i32(rec_idx)
         rh = C.c_void_p()
         self._check(F.lib.exg_transient(self._h, sys._h, C.byref(ctl), t_stop,
@@ -206,6 +209,10 @@ class Context:
         L = F.lib
         try:
             nt, nr, ns = L.exg_tran_n_times(rh), L.exg_tran_n_rec(rh), L.exg_tran_n_steps(rh)
+            if csv_path is not None:
+                cols = csv_columns if csv_columns is not None else [f"x{i}" for i in (ri if ri.size else range(nr))]
+                names = (C.c_char_p * max(nr, 1))(*[str(c).encode() for c in cols])
+                self._check(L.exg_tran_write_csv(rh, str(csv_path).encode(), names, 0))
             times = np.ctypeslib.as_array(L.exg_tran_times(rh), (nt,)).copy()
             samples = np.ctypeslib.as_array(L.exg_tran_samples(rh), (nt * nr,)).copy().reshape(nt, nr) \
                 if nt * nr else np.zeros((nt, nr))

@@ -225,3 +225,15 @@ def lu_factor(A: Csr, pivot_tol: float = 0.1) -> Factorization:
         return Factorization(n, L, U, rperm, cperm, o.value, nu.value)
     finally:
         F.lib.exg_factor_free(h)
+
+
+def write_waveform_csv(path, times, samples, columns, threads: int = 0) -> None:
+    """The reference CLI's waveform CSV (write_waveform_csv, proj/tools/common.hpp:35-46), byte for
+    byte, formatted by several host threads.  samples: n_times x n_cols."""
+    times = F.f64(times)
+    samples = np.ascontiguousarray(np.asarray(samples, dtype=np.float64).reshape(len(times), len(columns)))
+    names = (C.c_char_p * max(len(columns), 1))(*[c.encode() for c in columns])
+    rc = F.lib.exg_write_waveform_csv(str(path).encode(), len(times), len(columns), F.as_ptr(times, C.c_double),
+                                      F.as_ptr(samples, C.c_double), names, threads)
+    if rc != F.EXG_OK:
+        raise_for(rc, F.lib.exg_host_error_message().decode())

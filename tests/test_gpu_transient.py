@@ -58,6 +58,26 @@ def test_config0_vs_transient_as_shipped(ref, mode, weight):
     compare(got, want)
 
 
+def test_transient_waveform_csv(ref, tmp_path):
+    """The drop-in's waveform output (exg_tran_write_csv) is the reference CLI's CSV
+    (write_waveform_csv, proj/tools/common.hpp:35-46) of the same samples, byte for byte, and the
+    17-digit text reads back to the recorded doubles."""
+    s = ex.System.generate(0)
+    ctl = s.step_control()
+    ctl.fixed_step = 1
+    ctl.h_init = 1e-12
+    rec = probes(s)
+    cols = [f"v(n{i})" for i in rec]
+    path = tmp_path / "wave.csv"
+    with Context(0, trsv_mode=F.EXG_TRSV_FAST, weight_mode=F.EXG_WEIGHT_GSPMV) as c:
+        got = c.transient(s, ctl, 2e-10, rec, csv_path=path, csv_columns=cols)
+    want = tmp_path / "ref.csv"
+    ref.write_waveform_csv(want, got.times, got.samples, cols)
+    assert path.read_bytes() == want.read_bytes()
+    back = np.loadtxt(path, delimiter=",", skiprows=1)
+    assert np.array_equal(back[:, 0], got.times) and np.array_equal(back[:, 1:], got.samples)
+
+
 @pytest.mark.parametrize("cfg,kw,t_stop", [
     (1, dict(width=64), 2e-9),
     (2, dict(width=12), 1e-9),

@@ -124,3 +124,28 @@ def test_nonlinear_host_mirror_bit_identical(ref, kw):
         assert np.array_equal(s.residual_F(x, x2), ref.residual_F(rh, x, x2))
     finally:
         ref.system_free(rh)
+
+
+# ---- waveform CSV: the reference CLI's writer, byte for byte --------------------
+@pytest.mark.parametrize("n_times,n_cols,threads", [(0, 3, 0), (1, 0, 1), (7, 1, 3), (4001, 16, 0), (20000, 5, 8)])
+def test_waveform_csv_matches_reference_writer(ref, tmp_path, n_times, n_cols, threads):
+    """exg_write_waveform_csv against write_waveform_csv of proj/tools/common.hpp:35-46 (unmodified,
+    through oracle/_ref): identical bytes, whatever the thread count; values include zeros of both
+    signs, denormals, huge and non-finite numbers (the reference prints them with %.17g too)."""
+    from paper_1511_04515_b200.host import write_waveform_csv
+    rng = np.random.default_rng(n_times + n_cols)
+    times = np.cumsum(rng.uniform(1e-13, 2e-11, n_times))
+    samples = rng.normal(0.0, 1.0, (n_times, n_cols)) * 10.0 ** rng.integers(-12, 3, (n_times, n_cols))
+    if samples.size >= 8:
+        samples.flat[:8] = [0.0, -0.0, 5e-324, -2.2250738585072014e-308, 1.7976931348623157e308, np.inf, -np.inf, np.nan]
+    cols = [f"v(n{c}_{c * 7})" for c in range(n_cols)]
+    a, b = tmp_path / "ours.csv", tmp_path / "ref.csv"
+    write_waveform_csv(a, times, samples, cols, threads)
+    ref.write_waveform_csv(b, times, samples.reshape(n_times, n_cols), cols)
+    assert a.read_bytes() == b.read_bytes()
+
+
+def test_waveform_csv_unwritable_path_is_a_contract_error(tmp_path):
+    from paper_1511_04515_b200.host import write_waveform_csv
+    with pytest.raises(ex.ContractError):
+        write_waveform_csv(tmp_path / "no_such_dir" / "w.csv", [0.0], [[1.0]], ["a"])
